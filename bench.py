@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark: rows/sec scored (500 trees, depth 8) on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+                    [--impl ours|reference] [--strategy auto] [--no-e2e] [--no-cpu]
+
+One "step" is one pass of the whole hot path over one batch: a single fused
+hb_predict_proba (or hb_predict for regression) launch over all rows of the
+rank's shard (X tile staging, the strategy's traversal, ensemble accumulate,
+epilogue, store). Rows are sharded across ranks with no data-path collective
+(weak scaling: every rank scores its own n_rows). Timing: W untimed warm-up
+steps, then K steps bracketed by barrier + cuda synchronize, CUDA events on
+the launching stream, max over ranks. X (> L2) is resident in HBM before the
+timed region. ``e2e`` repeats the metric through hb_predict_host from pinned
+host memory (H2D of X and D2H of the result inside the timed region).
+
+--impl reference times the CPU oracle (the only reference this tier has) on a
+bounded sample per step, on the host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "rows/sec scored (500 trees, depth 8) at 1/2/4/8 B200; % of HBM/tensor roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--rows", type=int, default=0, help="override rows per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--strategy", default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        load = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- oracle (CPU baseline)
+def time_oracle(e, cfg, budget_s=12.0, max_rows=None, threads=0):
+    """Oracle throughput on a bounded prefix sample of the workload, all host
+    cores (std pthreads over row blocks). Returns (rows/s, cores, sample)."""
+    import oracle
+    import synth
+    max_rows = max_rows or cfg.n_rows
+    probe = min(2000, max_rows)
+    Xp = synth.gen_X(cfg.seed_x, probe, cfg.n_features)
+    t = time.perf_counter()
+    _, used = oracle.predict_mt(e, Xp, threads=threads)
+    dt = max(time.perf_counter() - t, 1e-4)
+    rate = probe / dt
+    rows = int(min(max_rows, max(probe, rate * budget_s)))
+    X = synth.gen_X(cfg.seed_x, rows, cfg.n_features)
+    t = time.perf_counter()
+    _, used = oracle.predict_mt(e, X, threads=threads)
+    dt = time.perf_counter() - t
+    return rows / dt, used, f"first {rows} rows of {cfg.name} (seed {cfg.seed_x:#x}), full model", dt
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import synth
+    cfg, e = synth.make_config(args.config)
+    cpu_model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    # size each step for ~4 s of CPU work
+    rate0, used, _, _ = time_oracle(e, cfg, budget_s=1.0)
+    rows = int(min(cfg.n_rows, max(1000, rate0 * 4.0)))
+    import oracle
+    X = synth.gen_X(cfg.seed_x, rows, cfg.n_features)
+    for _ in range(args.warmup):
+        oracle.predict_mt(e, X[: max(1, rows // 8)])
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        _, used = oracle.predict_mt(e, X)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.mean(times))
+    value = rows / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(cfg, e, rows, args),
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": used, "kind": "oracle",
+                         "sample": f"first {rows} rows of {cfg.name} per step", "cpu": cpu_model},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, e, rows, args):
+    return {"workload": f"{cfg.name}: {cfg.note}", "rows_per_gpu": rows, "n_trees": e.n_trees,
+            "max_depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": e.n_outputs,
+            "family": cfg.family, "parallelism": f"rows sharded over {args.gpus} GPU(s), no collective",
+            "l2": "inputs larger than L2 (X streamed once per step); model (<13 MB) L2-resident by design"}
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2010_04804_b200 as hb
+    import synth
+    import synth.dev
+
+    cfg, e = synth.make_config(args.config)
+    n = args.rows or cfg.n_rows
+    m = hb.Model(e, strategy=args.strategy, device=local)
+    info = m.info
+    cls = e.task == synth.TASK_CLASSIFICATION
+    kind = "proba" if cls else "predict"
+    X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, row_offset=rank * n, device=local)
+    shape, dt = m.out_shape(n, kind)
+    out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
+    stream = torch.cuda.current_stream(local)
+
+    def step():
+        m.run(X, kind, out=out, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):     # timing rule: >= 3 warm-up steps
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local)
+    time.sleep(0.25)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    per_launch = [a.elapsed_time(b) for a, b in evs]
+    if dist:
+        tt = torch.tensor([total_ms], device=X.device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    rows_all = n * world
+    value = rows_all / (ms_per_step * 1e-3)
+
+    # ---- roofline of the dominant (only) kernel of the step
+    kern_ms = float(np.mean(per_launch))
+    D = info["max_depth"]
+    w = info["leaf_width"]
+    # per (row, tree) and level one 8-B node record + one 4-B X
+    # value; per tree one leaf of 4w B (PTT: D levels by construction).
+    per_row = e.n_trees * (D * 12 + 4 * w)
+    achieved = per_row * n / (kern_ms * 1e-3) / 1e9
+    peaks = {}
+    if rank == 0:
+        try:
+            import tools
+            tools.build()
+            peaks = tools.peaks(local)
+        except Exception as ex:  # pragma: no cover
+            peaks = {"error": str(ex)}
+    smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
+    prof = load_profile(args.config, info["strategy_name"])
+    hbm_bytes = n * (cfg.n_features * 4 + (8 if (cls and e.n_outputs == 1) else 4 * e.n_outputs))
+    measured = {}
+    try:
+        measured = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = measured.get("hbm_gbs", 6650.0)
+    roofline = {
+        "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+        "frac": achieved / smem_peak, "traffic": prof.get("dram_bytes_per_launch"),
+        "kernel": f"{info['strategy_name']}_kernel", "kernel_ms": kern_ms,
+        "algorithmic_bytes_per_row": per_row,
+        "peak_source": "measured LDS.128 microbenchmark (tools/peaks.cu), this run" if peaks.get("smem_gbs")
+        else "spec 148 SM x 128 B/clk x 1.965 GHz",
+        "smem_peak_spec_gbs": 148 * 128 * 1.965,
+        "l2_peak_gbs": peaks.get("l2_gbs"),
+        "hbm": {"achieved": hbm_bytes / (kern_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "frac": hbm_bytes / (kern_ms * 1e-3) / 1e9 / hbm_peak,
+                "peak_source": "MEASURED_PEAKS.json" if measured else "fallback 6.65 TB/s"},
+    }
+
+    # ---- e2e through the public host API (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        del out
+        Xh = torch.empty((n, cfg.n_features), dtype=torch.float32).pin_memory()
+        Xh.copy_(X.cpu())
+        oh = torch.empty(shape, dtype=getattr(torch, dt)).pin_memory()
+        m.predict_host(Xh, kind, out=oh)  # warm (allocates staging)
+        if dist:
+            dist.barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            m.predict_host(Xh, kind, out=oh)
+            ts.append(time.perf_counter() - t0)
+        t_e2e = float(np.mean(ts))
+        if dist:
+            tt = torch.tensor([t_e2e], device=X.device, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": rows_all / t_e2e, "unit": "rows/s", "ms_per_step": t_e2e * 1e3,
+               "h2d_bytes_per_step": int(n * cfg.n_features * 4),
+               "d2h_bytes_per_step": int(oh.numel() * oh.element_size()), "steps": args.e2e_steps,
+               "api": "hb_predict_host (chunked H2D / score / D2H on two streams)"}
+        del Xh, oh
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rate, used, sample, secs = time_oracle(e, cfg, budget_s=12.0)
+        cpu = {"value": rate, "unit": "rows/s", "cores": used, "kind": "oracle", "sample": sample,
+               "seconds": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded splitmix64 grid X; random balanced depth-8 forest)",
+            "config": dict(workload_config(cfg, e, n, args), strategy=info["strategy_name"],
+                           output=kind),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def load_profile(config, strat):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(f"{config}:{strat}", {})
+    except (OSError, ValueError):
+        return {}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,196 @@
+/*
+ * hb.h — C ABI of the B200 (sm_100a) tree-ensemble scoring library (libhb.so).
+ *
+ * The library implements the hot path Hummingbird (Nakandala et al., OSDI'20,
+ * arXiv 2010.04804; /root/reference/PAPER.md, cited as P:<line>) compiles
+ * tree ensembles into: batch scoring with the GEMM strategy (Alg. 1),
+ * TreeTraversal (Alg. 2) or PerfectTreeTraversal (Alg. 3,
+ * P:243-286), picked from tree depth as in Sec. 5.1.
+ *
+ * Conventions for every entry point
+ *  - Status codes: every call returns hb_status; on failure hb_last_error()
+ *    returns a thread-local, human-readable message (valid until the next
+ *    failing call on the same thread).
+ *  - Ownership: hb_compile deep-copies the ensemble; the caller may free it on
+ *    return. The model owns its device memory on `device` until hb_free.
+ *  - Device pointers: X / out of the hb_predict* family are caller-owned
+ *    DEVICE pointers on the model's device (checked with
+ *    cudaPointerGetAttributes; host or foreign-device pointers give
+ *    HB_E_INVALID). The library never allocates per call on these paths.
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream). Calls only enqueue work and return once the launch succeeded;
+ *    asynchronous kernel faults surface at the caller's synchronisation.
+ *  - Threading: a compiled model is immutable; concurrent predicts on
+ *    different streams are safe. hb_free must not race with in-flight work.
+ *  - Layout: X is fp32 row-major, row r at X + r * ldx, ldx >= n_features.
+ *    n_rows == 0 is a no-op returning HB_OK.
+ */
+#ifndef HB_H
+#define HB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_ABI_VERSION 1
+
+typedef enum {
+  HB_OK = 0,
+  HB_E_INVALID = 1,      /* bad argument (NULL, sizes, pointer kind, device)      */
+  HB_E_TREE = 2,         /* ensemble fails validation (message names tree/node)   */
+  HB_E_UNSUPPORTED = 3,  /* valid but outside what this build supports            */
+  HB_E_OOM = 4,          /* device allocation failed                              */
+  HB_E_CUDA = 5          /* a CUDA runtime call or kernel launch failed           */
+} hb_status;
+
+/* Decision predicate; true => LEFT child ("< comparisons"; Alg. 2
+ * Where(T_V < T_T, T_L, T_R)). LE is the sklearn/LightGBM convention.
+ * IEEE fp32 compare: NaN makes the predicate false, so NaN goes RIGHT. */
+typedef enum { HB_CMP_LT = 0, HB_CMP_LE = 1 } hb_cmp;
+
+/* Ensemble reduction over the tree dimension. MEAN divides output k
+ * by the number of trees feeding it in the WHOLE ensemble. */
+typedef enum { HB_AGG_SUM = 0, HB_AGG_MEAN = 1 } hb_agg;
+
+/* Post transform of the margin (Table 2: sigmoid, exp, logsumexp). */
+typedef enum { HB_POST_IDENTITY = 0, HB_POST_SIGMOID = 1, HB_POST_SOFTMAX = 2 } hb_post;
+
+typedef enum { HB_TASK_REGRESSION = 0, HB_TASK_CLASSIFICATION = 1 } hb_task;
+
+/* Compilation strategy (Sec. 4.1). AUTO applies the depth heuristic of
+ * Sec. 5.1: GEMM if D_max <= 3, PTT if D_max <= 10, else TT
+ * (reading R24; env HB_GEMM_MAX_DEPTH / HB_PTT_MAX_DEPTH override). */
+typedef enum {
+  HB_STRATEGY_AUTO = 0,
+  HB_STRATEGY_GEMM = 1,
+  HB_STRATEGY_TT = 2,
+  HB_STRATEGY_PTT = 3
+} hb_strategy;
+
+/* What a scoring launch writes (hb_predict_ex). */
+typedef enum {
+  HB_OUT_PREDICT = 0,    /* regression: float[n*K] post applied; classification: int32[n] label */
+  HB_OUT_PROBA = 1,      /* classification: float[n*C], C = K==1 ? 2 : K; binary gives [1-p, p]  */
+  HB_OUT_RAW = 2,        /* float[n*K]: sum of leaf values of THIS model's trees (tree-shard partial) */
+  HB_OUT_MARGIN = 3,     /* float[n*K]: (MEAN ? raw/ntrees_k : raw) + base, no post               */
+  HB_OUT_LEAF = 4,       /* int32[n*T_model]: tree-local ORIGINAL node id of the reached leaf     */
+  HB_OUT_LEAF_HASH = 5   /* uint64[n]: sum_t mix64((uint64)t_global << 32 | leaf) mod 2^64        */
+} hb_output;
+
+/*
+ * The ensemble, one flat array per node attribute (Tables 3/5 of P:143-204
+ * describe the same per-node information as tensors).
+ *  node_offset [n_trees+1]  tree t owns nodes [node_offset[t], node_offset[t+1]);
+ *                           tree-local id 0 is the root.
+ *  feature     [n_nodes]    0-based feature id; read at internal nodes only.
+ *  threshold   [n_nodes]    fp32; read at internal nodes only; must not be NaN
+ *                           (+-Inf allowed).
+ *  left, right [n_nodes]    tree-local child ids; -1/-1 marks a leaf.
+ *  leaf_value  [n_nodes*leaf_width]  read at leaves only; must be finite.
+ *  leaf_width               1 (scalar leaves, routed by tree_output) or n_outputs
+ *                           (vector leaves, e.g. RF class distributions).
+ *  tree_output [n_trees]    output column of each scalar-leaf tree; NULL => t % K.
+ *  base_score  [n_outputs]  margin-space constant added after aggregation; NULL => 0.
+ */
+typedef struct {
+  int32_t n_trees;
+  int32_t n_features;
+  int32_t n_outputs;            /* K: 1 for regression / binary margin */
+  const int64_t *node_offset;
+  const int32_t *feature;
+  const float *threshold;
+  const int32_t *left;
+  const int32_t *right;
+  const float *leaf_value;
+  int32_t leaf_width;
+  const int32_t *tree_output;
+  const float *base_score;
+  int32_t cmp;                  /* hb_cmp      */
+  int32_t agg;                  /* hb_agg      */
+  int32_t post;                 /* hb_post     */
+  int32_t task;                 /* hb_task     */
+} hb_ensemble;
+
+typedef struct hb_model hb_model;
+
+typedef struct {
+  int32_t strategy;             /* the strategy actually compiled (never AUTO) */
+  int32_t max_depth;            /* D_max over this model's trees               */
+  int32_t tree_begin;           /* first global tree id of this model          */
+  int32_t n_trees;              /* trees in this model                         */
+  int32_t n_trees_total;        /* trees in the ensemble it was compiled from  */
+  int32_t n_features;
+  int32_t n_outputs;
+  int32_t leaf_width;
+  int32_t device;
+  int32_t x_in_smem;            /* 1 if the scorer stages X row tiles in SMEM  */
+  int64_t device_bytes;         /* device memory owned by the model            */
+  int64_t tree_stride_bytes;    /* bytes per tree in the compiled layout       */
+} hb_model_info;
+
+/* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the
+ * first offending tree/node. Rules: n_trees >= 1, n_features >= 1,
+ * n_outputs >= 1, leaf_width in {1, K}; offsets monotone; each tree a rooted
+ * binary tree (one parent per non-root node, no cycles, all nodes reachable,
+ * left == -1 <=> right == -1); feature in range; threshold not NaN; leaf values
+ * finite; tree_output in [0, K); SIGMOID => K == 1; SOFTMAX => K >= 2;
+ * CLASSIFICATION => (K == 1 and SIGMOID) or K >= 2. */
+hb_status hb_validate(const hb_ensemble *e);
+
+/* Validate, select the strategy, build its layout (Tables 3/5/6) and upload it
+ * to `device`. Forced PTT beyond its memory/depth budget -> HB_E_UNSUPPORTED
+ * (AUTO falls back to TT). */
+hb_status hb_compile(const hb_ensemble *e, int32_t strategy, int32_t device, hb_model **out);
+
+/* Same for the tree shard [tree_begin, tree_end): the model keeps the global
+ * per-output tree counts (for MEAN) and global tree ids (for leaf hashes) so
+ * partial sums of shards reduce to the unsharded result.
+ * For vector-free multiclass (leaf_width == 1, K > 1) tree_begin should be a
+ * multiple of K to keep shards balanced (not required for correctness). */
+hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tree_end,
+                           int32_t strategy, int32_t device, hb_model **out);
+
+/* One fused scoring launch writing `kind` (hb_output) for rows [0, n_rows). */
+hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
+                        int32_t kind, void *out, void *stream);
+
+/* = hb_predict_ex(HB_OUT_PREDICT). */
+hb_status hb_predict(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
+                     void *out, void *stream);
+/* = hb_predict_ex(HB_OUT_PROBA); HB_E_UNSUPPORTED on a regression model. */
+hb_status hb_predict_proba(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
+                           float *out, void *stream);
+/* = hb_predict_ex(HB_OUT_RAW). */
+hb_status hb_predict_raw(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
+                         float *out, void *stream);
+/* = hb_predict_ex(HB_OUT_LEAF). */
+hb_status hb_predict_leaf(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
+                          int32_t *out, void *stream);
+
+/* Epilogue only: from raw sums over ALL trees (e.g. the NCCL-reduced tree-shard
+ * partials, float[n*K] on the device) write `kind` in {PREDICT, PROBA, MARGIN}
+ * using the model's global tree counts, base score and post transform. */
+hb_status hb_finalize(const hb_model *m, const float *raw, int64_t n_rows, int32_t kind,
+                      void *out, void *stream);
+
+/* End-to-end scoring from HOST memory: rows are streamed in chunks through
+ * double-buffered device staging (H2D copy of chunk i+1 overlaps scoring of
+ * chunk i on a second stream) and results copied back. Synchronous: returns
+ * when `out_host` is filled. Pinned host buffers (cudaHostAlloc /
+ * torch.pin_memory) are needed for the copies to overlap. kind as in
+ * hb_predict_ex except LEAF. */
+hb_status hb_predict_host(const hb_model *m, const float *X_host, int64_t n_rows, int64_t ldx,
+                          int32_t kind, void *out_host);
+
+hb_status hb_model_get_info(const hb_model *m, hb_model_info *info);
+void hb_free(hb_model *m);
+const char *hb_last_error(void);
+int32_t hb_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HB_H */

@@ -1,0 +1,155 @@
+// hb_device.cuh — device helpers shared by the scoring kernels: mbarrier /
+// cp.async.bulk (TMA bulk-copy engine) wrappers and the fused epilogue.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hb.h"
+
+namespace hb {
+namespace dev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA engine; completion is
+// signalled on `bar` as transaction bytes (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// Per-lane X row staging: lane `lane` of a warp owns row `row`; the warp's
+// slice is feature-major xs[f * 32 + lane] so that every later data-dependent
+// read X[row, f] hits bank `lane` (conflict-free whatever f each lane needs).
+__device__ __forceinline__ void load_x_slice(float *xs, const float *__restrict__ X, int64_t row,
+                                             int64_t n, int64_t ldx, int F, int lane, bool vec4) {
+  if (row < n) {
+    const float *xr = X + row * ldx;
+    int f = 0;
+    if (vec4) {
+      for (; f + 4 <= F; f += 4) {
+        float4 v = __ldg(reinterpret_cast<const float4 *>(xr + f));
+        xs[(f + 0) * 32 + lane] = v.x;
+        xs[(f + 1) * 32 + lane] = v.y;
+        xs[(f + 2) * 32 + lane] = v.z;
+        xs[(f + 3) * 32 + lane] = v.w;
+      }
+    }
+    for (; f < F; ++f) xs[f * 32 + lane] = __ldg(xr + f);
+  } else {
+    for (int f = 0; f < F; ++f) xs[f * 32 + lane] = 0.f;
+  }
+}
+
+// Fused epilogue for one row (a10/a11 of SURVEY §8): margin = acc / div +
+// base, post transform, proba / label, coalesced-enough row-major stores.
+template <int NACC>
+__device__ __forceinline__ void write_row(int kind, const float (&acc)[NACC], int K, int task,
+                                          int post, const float *__restrict__ scale /* divisor: ntrees_k (MEAN) or 1 */,
+                                          const float *__restrict__ base, int64_t row, void *out) {
+  if (kind == HB_OUT_RAW) {
+    float *o = static_cast<float *>(out) + row * K;
+#pragma unroll
+    for (int k = 0; k < NACC; ++k)
+      if (k < K) o[k] = acc[k];
+    return;
+  }
+  float m[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) m[k] = (k < K) ? acc[k] / __ldg(scale + k) + __ldg(base + k) : 0.f;
+  if (kind == HB_OUT_MARGIN) {
+    float *o = static_cast<float *>(out) + row * K;
+#pragma unroll
+    for (int k = 0; k < NACC; ++k)
+      if (k < K) o[k] = m[k];
+    return;
+  }
+  if (kind == HB_OUT_PREDICT && task == HB_TASK_CLASSIFICATION) {
+    int32_t lab = 0;
+    if (K == 1) {
+      lab = m[0] > 0.f ? 1 : 0;
+    } else {
+      float best = m[0];
+#pragma unroll
+      for (int k = 1; k < NACC; ++k)
+        if (k < K && m[k] > best) { best = m[k]; lab = k; }
+    }
+    static_cast<int32_t *>(out)[row] = lab;
+    return;
+  }
+  // post transform (PREDICT for regression, PROBA for classification)
+  float p[NACC];
+  if (post == HB_POST_SIGMOID) {
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) p[k] = 1.f / (1.f + expf(-m[k]));
+  } else if (post == HB_POST_SOFTMAX) {
+    float mx = m[0];
+#pragma unroll
+    for (int k = 1; k < NACC; ++k)
+      if (k < K) mx = fmaxf(mx, m[k]);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) {
+      p[k] = (k < K) ? expf(m[k] - mx) : 0.f;
+      s += p[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) p[k] = p[k] / s;
+  } else {
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) p[k] = m[k];
+  }
+  if (kind == HB_OUT_PROBA && K == 1) {
+    float2 v = make_float2(1.f - p[0], p[0]);
+    reinterpret_cast<float2 *>(out)[row] = v;
+    return;
+  }
+  float *o = static_cast<float *>(out) + row * K;
+#pragma unroll
+  for (int k = 0; k < NACC; ++k)
+    if (k < K) o[k] = p[k];
+}
+
+}  // namespace dev
+}  // namespace hb

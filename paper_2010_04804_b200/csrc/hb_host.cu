@@ -1,0 +1,699 @@
+// hb_host.cu — the C ABI (include/hb.h): validation, strategy selection
+// (Sec. 5.1), layout compilation for the three strategies
+// (Tables 3/5/6) and the scoring entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hb_internal.h"
+
+namespace hb {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+void set_error(const std::string &s) { g_err = s; }
+
+hb_status fail(hb_status st, const std::string &s) {
+  g_err = s;
+  return st;
+}
+
+hb_status cuda_fail(cudaError_t e, const char *what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? HB_E_OOM : HB_E_CUDA;
+}
+
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (cache[device] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+// Keeps the caller's current device intact around library calls.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------------ validation
+struct TreeInfo {
+  int depth = 0;
+  int n_nodes = 0;
+};
+
+static hb_status validate_impl(const hb_ensemble *e, std::vector<TreeInfo> *info) {
+  if (!e) return fail(HB_E_INVALID, "ensemble is NULL");
+  const int T = e->n_trees, F = e->n_features, K = e->n_outputs, w = e->leaf_width;
+  if (T < 1) return fail(HB_E_TREE, "n_trees must be >= 1");
+  if (F < 1) return fail(HB_E_TREE, "n_features must be >= 1");
+  if (K < 1) return fail(HB_E_TREE, "n_outputs must be >= 1");
+  if (w != 1 && w != K) return fail(HB_E_TREE, "leaf_width must be 1 or n_outputs");
+  if (!e->node_offset || !e->feature || !e->threshold || !e->left || !e->right || !e->leaf_value)
+    return fail(HB_E_INVALID, "ensemble array pointer is NULL");
+  if (e->cmp != HB_CMP_LT && e->cmp != HB_CMP_LE)
+    return fail(HB_E_UNSUPPORTED, "cmp must be HB_CMP_LT or HB_CMP_LE (GT/GE would change NaN routing)");
+  if (e->agg != HB_AGG_SUM && e->agg != HB_AGG_MEAN) return fail(HB_E_TREE, "bad agg");
+  if (e->post < HB_POST_IDENTITY || e->post > HB_POST_SOFTMAX) return fail(HB_E_TREE, "bad post");
+  if (e->task != HB_TASK_REGRESSION && e->task != HB_TASK_CLASSIFICATION)
+    return fail(HB_E_TREE, "bad task");
+  if (e->post == HB_POST_SIGMOID && K != 1) return fail(HB_E_TREE, "SIGMOID requires n_outputs == 1");
+  if (e->post == HB_POST_SOFTMAX && K < 2) return fail(HB_E_TREE, "SOFTMAX requires n_outputs >= 2");
+  if (e->task == HB_TASK_CLASSIFICATION && !((K == 1 && e->post == HB_POST_SIGMOID) || K >= 2))
+    return fail(HB_E_TREE, "CLASSIFICATION requires (K == 1 and SIGMOID) or K >= 2");
+  if (e->node_offset[0] != 0) return fail(HB_E_TREE, "node_offset[0] must be 0");
+  if (e->tree_output && w == 1)
+    for (int t = 0; t < T; ++t)
+      if (e->tree_output[t] < 0 || e->tree_output[t] >= K)
+        return fail(HB_E_TREE, "tree " + std::to_string(t) + ": tree_output out of range");
+  if (e->base_score)
+    for (int k = 0; k < K; ++k)
+      if (!std::isfinite(e->base_score[k])) return fail(HB_E_TREE, "base_score must be finite");
+  if (info) info->assign(T, TreeInfo());
+  std::vector<int> pc, depth, queue;
+  for (int t = 0; t < T; ++t) {
+    const int64_t a = e->node_offset[t], b = e->node_offset[t + 1];
+    const std::string where = "tree " + std::to_string(t);
+    if (b <= a) return fail(HB_E_TREE, where + ": has no nodes (offsets not increasing)");
+    if (b - a > (int64_t)INT32_MAX) return fail(HB_E_TREE, where + ": too many nodes");
+    const int n = (int)(b - a);
+    pc.assign(n, 0);
+    for (int i = 0; i < n; ++i) {
+      const int L = e->left[a + i], R = e->right[a + i];
+      const std::string at = where + " node " + std::to_string(i);
+      if ((L == -1) != (R == -1)) return fail(HB_E_TREE, at + ": exactly one child is -1");
+      if (L != -1) {
+        if (L < 0 || L >= n || R < 0 || R >= n) return fail(HB_E_TREE, at + ": child id out of range");
+        if (L == R) return fail(HB_E_TREE, at + ": left == right");
+        pc[L]++;
+        pc[R]++;
+        const int f = e->feature[a + i];
+        if (f < 0 || f >= F) return fail(HB_E_TREE, at + ": feature out of range");
+        if (std::isnan(e->threshold[a + i])) return fail(HB_E_TREE, at + ": threshold is NaN");
+      } else {
+        for (int k = 0; k < w; ++k)
+          if (!std::isfinite(e->leaf_value[(a + i) * w + k]))
+            return fail(HB_E_TREE, at + ": leaf value not finite");
+      }
+    }
+    if (pc[0] != 0) return fail(HB_E_TREE, where + ": root (node 0) has a parent");
+    for (int i = 1; i < n; ++i)
+      if (pc[i] != 1)
+        return fail(HB_E_TREE, where + " node " + std::to_string(i) + ": has " +
+                                   std::to_string(pc[i]) + " parents (must be exactly 1)");
+    depth.assign(n, -1);
+    queue.clear();
+    queue.push_back(0);
+    depth[0] = 0;
+    int maxd = 0;
+    for (size_t q = 0; q < queue.size(); ++q) {
+      const int i = queue[q];
+      const int L = e->left[a + i];
+      if (L == -1) {
+        maxd = std::max(maxd, depth[i]);
+        continue;
+      }
+      const int R = e->right[a + i];
+      depth[L] = depth[R] = depth[i] + 1;
+      queue.push_back(L);
+      queue.push_back(R);
+    }
+    if ((int)queue.size() != n)
+      return fail(HB_E_TREE, where + ": not all nodes reachable from the root (cycle)");
+    if (info) {
+      (*info)[t].depth = maxd;
+      (*info)[t].n_nodes = n;
+    }
+  }
+  return HB_OK;
+}
+
+// ------------------------------------------------------------------ layouts
+static inline int tree_out(const hb_ensemble *e, int t) {
+  return e->tree_output ? e->tree_output[t] : t % e->n_outputs;
+}
+
+static inline uint32_t f2u(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
+
+static size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct HostLayout {
+  std::vector<uint8_t> trees;
+  std::vector<int32_t> leafmap;
+  size_t stride = 0;
+  int nslots = 0;
+};
+
+// PTT (Table 6, perfect padding P:243). Per tree record:
+//   uint2 node[2^D]: node[0] = {tree_output, 0}; node[p] for heap position
+//   p in [1, 2^D) = {N'_F, N'_T}; then float leaf[2^D][w] = N'_C.
+// A leaf at depth D_k < D becomes a perfect subtree whose decision nodes
+// compare feature 0 against +Inf ("free to perform arbitrary comparisons")
+// and whose 2^(D-D_k) leaves copy the leaf; leafmap keeps the original id.
+static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, HostLayout *L) {
+  const int w = e->leaf_width;
+  const int P = 1 << D;
+  L->nslots = P;
+  L->stride = round16((size_t)8 * P + (size_t)4 * w * P);
+  L->trees.assign((size_t)Tpad * L->stride, 0);
+  L->leafmap.assign((size_t)Tpad * P, -1);
+  std::vector<int> orig(2 * P);
+  const float pinf = INFINITY;
+  for (int lt = 0; lt < Tpad; ++lt) {
+    uint8_t *rec = L->trees.data() + (size_t)lt * L->stride;
+    uint32_t *node = reinterpret_cast<uint32_t *>(rec);
+    float *leaf = reinterpret_cast<float *>(rec + (size_t)8 * P);
+    if (lt >= t1 - t0) {  // zero tree (padding to the tree group)
+      for (int p = 1; p < P; ++p) node[2 * p] = 0, node[2 * p + 1] = f2u(pinf);
+      continue;
+    }
+    const int t = t0 + lt;
+    const int64_t a = e->node_offset[t];
+    node[0] = (uint32_t)(w == 1 ? tree_out(e, t) : 0);
+    orig[1] = 0;
+    for (int p = 1; p < P; ++p) {
+      const int o = orig[p];
+      if (e->left[a + o] != -1) {
+        node[2 * p] = (uint32_t)e->feature[a + o];
+        node[2 * p + 1] = f2u(e->threshold[a + o]);
+        orig[2 * p] = e->left[a + o];
+        orig[2 * p + 1] = e->right[a + o];
+      } else {
+        node[2 * p] = 0;
+        node[2 * p + 1] = f2u(pinf);
+        orig[2 * p] = orig[2 * p + 1] = o;
+      }
+    }
+    for (int p = P; p < 2 * P; ++p) {
+      const int o = orig[p];
+      const int slot = p - P;
+      for (int k = 0; k < w; ++k) leaf[(size_t)slot * w + k] = e->leaf_value[(a + o) * w + k];
+      L->leafmap[(size_t)lt * P + slot] = o;
+    }
+    if (D == 0) {  // single-leaf tree: root is the only slot
+      for (int k = 0; k < w; ++k) leaf[k] = e->leaf_value[a * w + k];
+      L->leafmap[(size_t)lt * P] = 0;
+    }
+  }
+}
+
+// TT (Table 5). Nodes renumbered BFS with siblings adjacent so that
+// N_L = N_R - 1; per tree record: 16-B header {tree_output}, uint2
+// node[nslots] = {N_F | N_R << 16, N_T}, float leaf[nslots][w] = N_C. Leaves
+// self-loop (N_R = self, N_T = NaN => predicate false for LT and LE). Padded
+// to the max node count over trees.
+static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLayout *L) {
+  const int w = e->leaf_width;
+  int maxn = 1;
+  for (int t = t0; t < t1; ++t)
+    maxn = std::max<int>(maxn, (int)(e->node_offset[t + 1] - e->node_offset[t]));
+  if (maxn > 65535) return fail(HB_E_UNSUPPORTED, "TT: trees with more than 65535 nodes");
+  if (e->n_features > 65536) return fail(HB_E_UNSUPPORTED, "TT: more than 65536 features");
+  L->nslots = maxn;
+  L->stride = round16(16 + (size_t)8 * maxn + (size_t)4 * w * maxn);
+  L->trees.assign((size_t)Tpad * L->stride, 0);
+  L->leafmap.assign((size_t)Tpad * maxn, -1);
+  const uint32_t qnan = 0x7FC00000u;
+  std::vector<int> neworder;
+  for (int lt = 0; lt < Tpad; ++lt) {
+    uint8_t *rec = L->trees.data() + (size_t)lt * L->stride;
+    uint32_t *hdr = reinterpret_cast<uint32_t *>(rec);
+    uint32_t *node = reinterpret_cast<uint32_t *>(rec + 16);
+    float *leaf = reinterpret_cast<float *>(rec + 16 + (size_t)8 * maxn);
+    // default: every slot is a self-looping zero leaf
+    for (int j = 0; j < maxn; ++j) node[2 * j] = (uint32_t)j << 16, node[2 * j + 1] = qnan;
+    if (lt >= t1 - t0) continue;
+    const int t = t0 + lt;
+    const int64_t a = e->node_offset[t];
+    const int n = (int)(e->node_offset[t + 1] - a);
+    hdr[0] = (uint32_t)(w == 1 ? tree_out(e, t) : 0);
+    neworder.assign(1, 0);  // new id -> original id
+    for (size_t q = 0; q < neworder.size(); ++q) {
+      const int o = neworder[q];
+      if (e->left[a + o] != -1) {
+        neworder.push_back(e->left[a + o]);
+        neworder.push_back(e->right[a + o]);
+      }
+    }
+    std::vector<int> newid(n);
+    for (int j = 0; j < n; ++j) newid[neworder[j]] = j;
+    for (int j = 0; j < n; ++j) {
+      const int o = neworder[j];
+      L->leafmap[(size_t)lt * maxn + j] = o;
+      if (e->left[a + o] != -1) {
+        const int r = newid[e->right[a + o]];
+        node[2 * j] = (uint32_t)e->feature[a + o] | ((uint32_t)r << 16);
+        node[2 * j + 1] = f2u(e->threshold[a + o]);
+      } else {
+        for (int k = 0; k < w; ++k) leaf[(size_t)j * w + k] = e->leaf_value[(a + o) * w + k];
+      }
+    }
+  }
+  return HB_OK;
+}
+
+// Launch configuration: as many 32-row warps as SMEM allows
+// for the feature-major X slices (NW * F * 128 B), the rest for a 2-4 stage
+// ring of tree chunks.
+static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool allow_t_global,
+                       LaunchCfg *c) {
+  const long budget = kSmemBudget;
+  for (int nw : {16, 12, 8, 4}) {
+    const long xb = (long)nw * F * 128;
+    if (xb + 4 * (long)stride > budget) continue;
+    const long rem = budget - xb;
+    int ns = (rem >= 3 * 8 * (long)stride) ? 3 : 2;
+    int ch = (int)std::min<long>(32, rem / (ns * (long)stride)) & ~1;
+    ch = std::min(ch, Tpad);
+    if (ch < 2) continue;
+    c->nw = nw;
+    c->ns = ns;
+    c->ch = ch;
+    c->x_smem = 1;
+    c->t_smem = 1;
+    c->smem_bytes = (int)(xb + (long)ns * ch * stride + 16 * ns);
+    return true;
+  }
+  // X does not fit: read rows from global memory, keep the tree ring.
+  if (allow_x_global) {
+    const long rem = budget;
+    if (4 * (long)stride <= rem) {
+      int ns = (rem >= 3 * 8 * (long)stride) ? 3 : 2;
+      int ch = std::min<int>((int)std::min<long>(32, rem / (ns * (long)stride)) & ~1, Tpad);
+      c->nw = 16;
+      c->ns = ns;
+      c->ch = ch;
+      c->x_smem = 0;
+      c->t_smem = 1;
+      c->smem_bytes = (int)((long)ns * ch * stride + 16 * ns);
+      return true;
+    }
+    if (allow_t_global) {  // neither fits: both through L2/L1
+      const long xb = 16L * F * 128;
+      c->nw = 16;
+      c->ns = 1;
+      c->ch = std::min(Tpad, 32) & ~1;
+      c->x_smem = xb <= budget ? 1 : 0;
+      c->t_smem = 0;
+      c->smem_bytes = c->x_smem ? (int)xb : 0;
+      return true;
+    }
+  }
+  return false;
+}
+
+static int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
+// Sec. 5.1: GEMM for shallow trees, PTT up to D = 10, TT beyond
+// (reading R24 for the GPU thresholds).
+static int select_strategy(int D) {
+  const int gemm_max = env_int("HB_GEMM_MAX_DEPTH", 3);
+  const int ptt_max = std::min(env_int("HB_PTT_MAX_DEPTH", kPttMaxDepth), kPttMaxDepth);
+  if (D <= gemm_max && gemm_supported(D)) return HB_STRATEGY_GEMM;
+  if (D <= ptt_max) return HB_STRATEGY_PTT;
+  return HB_STRATEGY_TT;
+}
+
+static void free_model(Model *m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  cudaFree(m->d_trees);
+  cudaFree(m->d_leafmap);
+  cudaFree(m->d_scale);
+  cudaFree(m->d_base);
+  cudaFree(m->d_gemm);
+  delete m;
+}
+
+template <typename T>
+static hb_status upload(const std::vector<T> &h, T **d, size_t *acct) {
+  const size_t bytes = std::max<size_t>(h.size() * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(d), bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(model)");
+  *acct += bytes;
+  if (!h.empty()) {
+    e = cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(model)");
+  }
+  return HB_OK;
+}
+
+static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy, int device,
+                              hb_model **out) {
+  if (!out) return fail(HB_E_INVALID, "out is NULL");
+  *out = nullptr;
+  std::vector<TreeInfo> info;
+  hb_status st = validate_impl(e, &info);
+  if (st != HB_OK) return st;
+  if (t0 < 0 || t1 > e->n_trees || t0 >= t1) return fail(HB_E_INVALID, "bad tree range");
+  if (strategy < HB_STRATEGY_AUTO || strategy > HB_STRATEGY_PTT)
+    return fail(HB_E_INVALID, "bad strategy");
+  const int K = e->n_outputs;
+  if (K > kMaxOutputs) return fail(HB_E_UNSUPPORTED, "n_outputs > 16 is not supported by this build");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(HB_E_INVALID, "device " + std::to_string(device) + " is not a CUDA device");
+  DeviceGuard guard(device);
+  if (!guard.ok) return fail(HB_E_CUDA, "cudaSetDevice failed");
+
+  std::unique_ptr<Model, void (*)(Model *)> m(new Model(), free_model);
+  m->device = device;
+  m->n_trees = t1 - t0;
+  m->tree_begin = t0;
+  m->n_trees_total = e->n_trees;
+  m->n_trees_pad = (m->n_trees + kTreeGroup - 1) / kTreeGroup * kTreeGroup;
+  m->n_features = e->n_features;
+  m->n_outputs = K;
+  m->leaf_width = e->leaf_width;
+  m->cmp = e->cmp;
+  m->agg = e->agg;
+  m->post = e->post;
+  m->task = e->task;
+  m->nacc = K == 1 ? 1 : (K <= 4 ? 4 : (K <= 8 ? 8 : 16));
+  int D = 0;
+  for (int t = t0; t < t1; ++t) D = std::max(D, info[t].depth);
+  m->depth = D;
+
+  int strat = strategy == HB_STRATEGY_AUTO ? select_strategy(D) : strategy;
+  HostLayout L;
+  if (strat == HB_STRATEGY_GEMM) {
+    st = compile_gemm(e, t0, t1, m.get());
+    if (st != HB_OK) return st;
+  } else {
+    if (strat == HB_STRATEGY_PTT) {
+      bool ok = D <= kPttMaxDepth;
+      if (ok) {
+        build_ptt(e, t0, t1, D, m->n_trees_pad, &L);
+        ok = choose_cfg(e->n_features, L.stride, m->n_trees_pad, false, false, &m->cfg);
+      }
+      if (!ok) {
+        if (strategy == HB_STRATEGY_PTT)
+          return fail(HB_E_UNSUPPORTED,
+                      "PTT: depth " + std::to_string(D) + " / n_features " +
+                          std::to_string(e->n_features) +
+                          " exceed the perfect-tree / SMEM budget (use TT or AUTO)");
+        strat = HB_STRATEGY_TT;
+        L = HostLayout();
+      }
+    }
+    if (strat == HB_STRATEGY_TT) {
+      st = build_tt(e, t0, t1, m->n_trees_pad, &L);
+      if (st != HB_OK) return st;
+      if (!choose_cfg(e->n_features, L.stride, m->n_trees_pad, true, true, &m->cfg))
+        return fail(HB_E_UNSUPPORTED, "TT: no launch configuration fits");
+    }
+    m->stride = L.stride;
+    m->nslots = L.nslots;
+    st = upload(L.trees, reinterpret_cast<uint8_t **>(&m->d_trees), &m->device_bytes);
+    if (st != HB_OK) return st;
+    st = upload(L.leafmap, &m->d_leafmap, &m->device_bytes);
+    if (st != HB_OK) return st;
+  }
+  m->strategy = strat;
+
+  // global per-output tree counts (MEAN divisor) and base score
+  std::vector<float> div(K, 1.f), base(K, 0.f);
+  if (e->agg == HB_AGG_MEAN) {
+    std::vector<double> cnt(K, 0.0);
+    for (int t = 0; t < e->n_trees; ++t) {
+      if (e->leaf_width == 1) cnt[tree_out(e, t)] += 1.0;
+      else for (int k = 0; k < K; ++k) cnt[k] += 1.0;
+    }
+    for (int k = 0; k < K; ++k) div[k] = cnt[k] > 0 ? (float)cnt[k] : 1.f;
+  }
+  if (e->base_score)
+    for (int k = 0; k < K; ++k) base[k] = e->base_score[k];
+  st = upload(div, &m->d_scale, &m->device_bytes);
+  if (st != HB_OK) return st;
+  st = upload(base, &m->d_base, &m->device_bytes);
+  if (st != HB_OK) return st;
+  *out = reinterpret_cast<hb_model *>(m.release());
+  return HB_OK;
+}
+
+static const Model *M(const hb_model *m) { return reinterpret_cast<const Model *>(m); }
+
+static hb_status check_dev_ptr(const void *p, int device, const char *what) {
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HB_E_INVALID, std::string(what) + " is not a CUDA pointer");
+  }
+  if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+    return fail(HB_E_INVALID, std::string(what) + " is not a device pointer");
+  if (attr.device != device)
+    return fail(HB_E_INVALID, std::string(what) + " lives on device " + std::to_string(attr.device) +
+                                  ", model on device " + std::to_string(device));
+  return HB_OK;
+}
+
+static size_t out_row_bytes(const Model &m, int kind) {
+  switch (kind) {
+    case HB_OUT_PREDICT:
+      return m.task == HB_TASK_CLASSIFICATION ? 4 : 4 * (size_t)m.n_outputs;
+    case HB_OUT_PROBA: return m.n_outputs == 1 ? 8 : 4 * (size_t)m.n_outputs;
+    case HB_OUT_RAW:
+    case HB_OUT_MARGIN: return 4 * (size_t)m.n_outputs;
+    case HB_OUT_LEAF: return 4 * (size_t)m.n_trees;
+    case HB_OUT_LEAF_HASH: return 8;
+  }
+  return 0;
+}
+
+static hb_status check_kind(const Model &m, int kind) {
+  if (kind < HB_OUT_PREDICT || kind > HB_OUT_LEAF_HASH) return fail(HB_E_INVALID, "bad output kind");
+  if (kind == HB_OUT_PROBA && m.task != HB_TASK_CLASSIFICATION)
+    return fail(HB_E_UNSUPPORTED, "predict_proba on a regression model");
+  return HB_OK;
+}
+
+static hb_status run(const Model &m, const RunArgs &a) {
+  switch (m.strategy) {
+    case HB_STRATEGY_PTT: return launch_ptt(m, a);
+    case HB_STRATEGY_TT: return launch_tt(m, a);
+    case HB_STRATEGY_GEMM: return launch_gemm(m, a);
+  }
+  return fail(HB_E_INVALID, "corrupt model");
+}
+
+static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int64_t ldx, int kind,
+                              void *out, void *stream, bool check_ptrs) {
+  if (!hm) return fail(HB_E_INVALID, "model is NULL");
+  const Model &m = *M(hm);
+  hb_status st = check_kind(m, kind);
+  if (st != HB_OK) return st;
+  if (n < 0) return fail(HB_E_INVALID, "n_rows < 0");
+  if (ldx < m.n_features) return fail(HB_E_INVALID, "ldx < n_features");
+  if (n == 0) return HB_OK;
+  if (!X || !out) return fail(HB_E_INVALID, "X or out is NULL");
+  DeviceGuard g(m.device);
+  if (check_ptrs) {
+    st = check_dev_ptr(X, m.device, "X");
+    if (st != HB_OK) return st;
+    st = check_dev_ptr(out, m.device, "out");
+    if (st != HB_OK) return st;
+  }
+  RunArgs a{X, n, ldx, kind, out, static_cast<cudaStream_t>(stream), nullptr};
+  return run(m, a);
+}
+
+// ------------------------------------------------------------------ host streaming
+struct HostStage {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t s[2] = {nullptr, nullptr};
+  float *x[2] = {nullptr, nullptr};
+  uint8_t *o[2] = {nullptr, nullptr};
+  size_t xcap = 0, ocap = 0;
+  ~HostStage() {}
+};
+
+static HostStage &host_stage(int device) {
+  static std::mutex mu;
+  static std::deque<HostStage> stages;  // one per device, never freed
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &s : stages)
+    if (s.device == device) return s;
+  stages.emplace_back();
+  stages.back().device = device;
+  return stages.back();
+}
+
+static hb_status host_impl(const hb_model *hm, const float *Xh, int64_t n, int64_t ldx, int kind,
+                           void *outh) {
+  if (!hm) return fail(HB_E_INVALID, "model is NULL");
+  const Model &m = *M(hm);
+  hb_status st = check_kind(m, kind);
+  if (st != HB_OK) return st;
+  if (kind == HB_OUT_LEAF) return fail(HB_E_UNSUPPORTED, "hb_predict_host: LEAF output not supported");
+  if (n < 0 || ldx < m.n_features) return fail(HB_E_INVALID, "bad n_rows / ldx");
+  if (n == 0) return HB_OK;
+  if (!Xh || !outh) return fail(HB_E_INVALID, "X or out is NULL");
+  DeviceGuard g(m.device);
+  HostStage &hs = host_stage(m.device);
+  std::lock_guard<std::mutex> lk(hs.mu);
+  cudaError_t e;
+  for (int i = 0; i < 2; ++i)
+    if (!hs.s[i] && (e = cudaStreamCreateWithFlags(&hs.s[i], cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+  const size_t orow = out_row_bytes(m, kind);
+  const size_t xrow = (size_t)ldx * 4;
+  // chunks of ~64 MB of X (at least 64K rows) so copies pipeline with scoring
+  const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(65536, (64LL << 20) / (int64_t)xrow));
+  if (hs.xcap < chunk * xrow || hs.ocap < chunk * orow) {
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(hs.x[i]);
+      cudaFree(hs.o[i]);
+      hs.x[i] = nullptr;
+      hs.o[i] = nullptr;
+    }
+    hs.xcap = hs.ocap = 0;
+    for (int i = 0; i < 2; ++i) {
+      if ((e = cudaMalloc(&hs.x[i], chunk * xrow)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(stage)");
+      if ((e = cudaMalloc(&hs.o[i], chunk * orow)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(stage)");
+    }
+    hs.xcap = chunk * xrow;
+    hs.ocap = chunk * orow;
+  }
+  int ci = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += chunk, ci ^= 1) {
+    const int64_t rows = std::min(chunk, n - r0);
+    cudaStream_t s = hs.s[ci];
+    if ((e = cudaMemcpyAsync(hs.x[ci], reinterpret_cast<const uint8_t *>(Xh) + r0 * xrow,
+                             rows * xrow, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    RunArgs a{hs.x[ci], rows, ldx, kind, hs.o[ci], s, nullptr};
+    st = run(m, a);
+    if (st != HB_OK) return st;
+    if ((e = cudaMemcpyAsync(static_cast<uint8_t *>(outh) + r0 * orow, hs.o[ci], rows * orow,
+                             cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+  }
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamSynchronize(hs.s[i])) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return HB_OK;
+}
+
+}  // namespace hb
+
+// ====================================================================== C ABI
+using namespace hb;
+
+extern "C" {
+
+hb_status hb_validate(const hb_ensemble *e) { return validate_impl(e, nullptr); }
+
+hb_status hb_compile(const hb_ensemble *e, int32_t strategy, int32_t device, hb_model **out) {
+  if (!e) return fail(HB_E_INVALID, "ensemble is NULL");
+  return compile_impl(e, 0, e->n_trees, strategy, device, out);
+}
+
+hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tree_end,
+                           int32_t strategy, int32_t device, hb_model **out) {
+  return compile_impl(e, tree_begin, tree_end, strategy, device, out);
+}
+
+hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n, int64_t ldx, int32_t kind,
+                        void *out, void *stream) {
+  return predict_impl(m, X, n, ldx, kind, out, stream, true);
+}
+
+hb_status hb_predict(const hb_model *m, const float *X, int64_t n, int64_t ldx, void *out,
+                     void *stream) {
+  return predict_impl(m, X, n, ldx, HB_OUT_PREDICT, out, stream, true);
+}
+
+hb_status hb_predict_proba(const hb_model *m, const float *X, int64_t n, int64_t ldx, float *out,
+                           void *stream) {
+  return predict_impl(m, X, n, ldx, HB_OUT_PROBA, out, stream, true);
+}
+
+hb_status hb_predict_raw(const hb_model *m, const float *X, int64_t n, int64_t ldx, float *out,
+                         void *stream) {
+  return predict_impl(m, X, n, ldx, HB_OUT_RAW, out, stream, true);
+}
+
+hb_status hb_predict_leaf(const hb_model *m, const float *X, int64_t n, int64_t ldx, int32_t *out,
+                          void *stream) {
+  return predict_impl(m, X, n, ldx, HB_OUT_LEAF, out, stream, true);
+}
+
+hb_status hb_finalize(const hb_model *hm, const float *raw, int64_t n, int32_t kind, void *out,
+                      void *stream) {
+  if (!hm) return fail(HB_E_INVALID, "model is NULL");
+  const Model &m = *M(hm);
+  if (kind != HB_OUT_PREDICT && kind != HB_OUT_PROBA && kind != HB_OUT_MARGIN)
+    return fail(HB_E_INVALID, "hb_finalize: kind must be PREDICT, PROBA or MARGIN");
+  hb_status st = check_kind(m, kind);
+  if (st != HB_OK) return st;
+  if (n < 0) return fail(HB_E_INVALID, "n_rows < 0");
+  if (n == 0) return HB_OK;
+  if (!raw || !out) return fail(HB_E_INVALID, "raw or out is NULL");
+  DeviceGuard g(m.device);
+  if ((st = check_dev_ptr(raw, m.device, "raw")) != HB_OK) return st;
+  if ((st = check_dev_ptr(out, m.device, "out")) != HB_OK) return st;
+  RunArgs a{nullptr, n, 0, kind, out, static_cast<cudaStream_t>(stream), raw};
+  return launch_finalize(m, a);
+}
+
+hb_status hb_predict_host(const hb_model *m, const float *X, int64_t n, int64_t ldx, int32_t kind,
+                          void *out) {
+  return host_impl(m, X, n, ldx, kind, out);
+}
+
+hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
+  if (!hm || !info) return fail(HB_E_INVALID, "NULL argument");
+  const Model &m = *M(hm);
+  info->strategy = m.strategy;
+  info->max_depth = m.depth;
+  info->tree_begin = m.tree_begin;
+  info->n_trees = m.n_trees;
+  info->n_trees_total = m.n_trees_total;
+  info->n_features = m.n_features;
+  info->n_outputs = m.n_outputs;
+  info->leaf_width = m.leaf_width;
+  info->device = m.device;
+  info->x_in_smem = m.cfg.x_smem;
+  info->device_bytes = (int64_t)m.device_bytes;
+  info->tree_stride_bytes = (int64_t)m.stride;
+  return HB_OK;
+}
+
+void hb_free(hb_model *m) { free_model(reinterpret_cast<Model *>(m)); }
+
+const char *hb_last_error(void) { return g_err.c_str(); }
+
+int32_t hb_abi_version(void) { return HB_ABI_VERSION; }
+
+}  // extern "C"

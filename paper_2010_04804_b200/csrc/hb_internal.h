@@ -1,0 +1,85 @@
+// hb_internal.h — model object, compiled layouts and kernel entry points of
+// libhb.so. Not part of the ABI (include/hb.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "hb.h"
+
+namespace hb {
+
+constexpr int kMaxOutputs = 16;       // NACC upper bound of the fused epilogue
+constexpr int kPttMaxDepth = 10;      // P:308 "PTT when D <= 10"; template range 0..10
+constexpr int kTreeGroup = 2;         // trees walked concurrently per lane (ILP)
+constexpr int kSmemBudget = 227 * 1024 - 2048;
+
+// Kernel launch configuration chosen at compile time from F and the per-tree
+// record size.
+struct LaunchCfg {
+  int nw = 16;          // compute warps per CTA (32 rows each)
+  int ns = 2;           // tree-chunk pipeline stages
+  int ch = 2;           // trees per chunk (multiple of kTreeGroup)
+  int x_smem = 1;       // X row tile staged in SMEM (feature-major per warp)
+  int t_smem = 1;       // tree chunks staged in SMEM via cp.async.bulk
+  int smem_bytes = 0;   // dynamic SMEM per CTA
+  int ctas_per_sm = 1;
+};
+
+struct Model {
+  int device = 0;
+  int strategy = HB_STRATEGY_PTT;
+  int depth = 0;            // D_max of this model's trees
+  int n_trees = 0;          // real trees in this model
+  int n_trees_pad = 0;      // padded to a multiple of kTreeGroup (zero trees)
+  int tree_begin = 0;
+  int n_trees_total = 0;
+  int n_features = 0;
+  int n_outputs = 0;
+  int leaf_width = 1;
+  int cmp = 0, agg = 0, post = 0, task = 0;
+  int nacc = 1;             // accumulator template bucket >= n_outputs
+
+  // compiled layout
+  size_t stride = 0;        // bytes per tree record (multiple of 16)
+  int nslots = 0;           // PTT: 2^D leaf slots; TT: max node count
+  void *d_trees = nullptr;  // n_trees_pad * stride bytes
+  int32_t *d_leafmap = nullptr;   // [n_trees_pad * nslots] original node id
+  float *d_scale = nullptr; // [K]: 1/ntrees_k (MEAN) or 1 (SUM)
+  float *d_base = nullptr;  // [K]
+  // GEMM-only tensors (Table 3 form, see hb_gemm.cu)
+  void *d_gemm = nullptr;
+  size_t gemm_bytes = 0;
+  int gemm_ni = 0, gemm_nl = 0;
+
+  size_t device_bytes = 0;
+  LaunchCfg cfg;
+};
+
+// thread-local error text
+void set_error(const std::string &s);
+hb_status fail(hb_status st, const std::string &s);
+hb_status cuda_fail(cudaError_t e, const char *what);
+
+// arguments of one scoring launch
+struct RunArgs {
+  const float *X;
+  int64_t n, ldx;
+  int kind;                 // hb_output
+  void *out;
+  cudaStream_t stream;
+  const float *raw_in;      // finalize only
+};
+
+bool gemm_supported(int depth);
+hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);
+
+hb_status launch_ptt(const Model &m, const RunArgs &a);
+hb_status launch_tt(const Model &m, const RunArgs &a);
+hb_status launch_gemm(const Model &m, const RunArgs &a);
+hb_status launch_finalize(const Model &m, const RunArgs &a);
+
+}  // namespace hb

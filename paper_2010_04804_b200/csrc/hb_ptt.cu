@@ -1,0 +1,249 @@
+// hb_ptt.cu — PerfectTreeTraversal scorer for sm_100a (Alg. 3,
+// P:259-284; perfect padding P:243; Table 6).
+//
+// Alg. 3 per (row, tree):  T_I <- 1;  repeat D: T_F <- N'_F[T_I];
+// T_V <- X[r, T_F]; T_T <- N'_T[T_I]; T_I <- 2 T_I + (T_V < T_T ? 0 : 1);
+// R <- N'_C[T_I - 2^D]. Here one lane owns one row and walks every tree with
+// D unrolled ("we unroll all iterations"), two trees at a time for ILP.
+//
+// Data movement:
+//  * X: each warp stages its 32 rows feature-major in SMEM (xs[f*32 + lane]),
+//    so the data-dependent read X[r, f] is bank-conflict free.
+//  * Trees: the compiled PTT records (per tree: heap-ordered {feature, thr}
+//    nodes then the 2^D leaf values) stream through an NS-stage SMEM ring,
+//    filled by a dedicated producer warp with cp.async.bulk (TMA bulk copy,
+//    UBLKCP) and mbarrier transaction counts; consumer warps release a stage
+//    with one mbarrier arrive each.
+//  * Persistent CTAs (one per SM) loop over row tiles of 32*NW rows; the tree
+//    stream simply restarts for every tile.
+#include <cuda_runtime.h>
+
+#include "hb_device.cuh"
+#include "hb_internal.h"
+
+namespace hb {
+
+struct PttParams {
+  const float *X;
+  int64_t n, ldx;
+  int F;
+  int vec4;
+  const uint8_t *trees;
+  uint32_t stride;
+  int n_trees_pad, n_trees, tree_begin;
+  const int32_t *leafmap;
+  int nslots;
+  const float *scale, *base;
+  int K, w, task, post, kind;
+  void *out;
+  int nw, ns, ch, ntiles;
+};
+
+template <int D, bool LE, int NACC>
+__global__ void __launch_bounds__(32 * 17, 1) ptt_kernel(const PttParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = p.nw, ns = p.ns, ch = p.ch;
+  const size_t xbytes = (size_t)nw * p.F * 128;
+  uint8_t *stages = smem + xbytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(stages + (size_t)ns * ch * p.stride);
+  uint64_t *empty = full + ns;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], nw);
+    }
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int nchunks = (p.n_trees_pad + ch - 1) / ch;
+  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  if (warp == nw) {
+    // ---------------- producer warp: stream tree chunks through the ring
+    if (lane == 0) {
+      const long total = (long)my_tiles * nchunks;
+      for (long it = 0; it < total; ++it) {
+        const int s = (int)(it % ns);
+        const uint32_t ph = (uint32_t)((it / ns) & 1);
+        dev::mbar_wait(&empty[s], ph ^ 1u);
+        const int c = (int)(it % nchunks);
+        const int t0 = c * ch;
+        const int nt = min(ch, p.n_trees_pad - t0);
+        const uint32_t bytes = (uint32_t)nt * p.stride;
+        dev::mbar_arrive_expect_tx(&full[s], bytes);
+        dev::bulk_g2s(stages + (size_t)s * ch * p.stride, p.trees + (size_t)t0 * p.stride, bytes,
+                      &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
+  float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
+  const float *xl = xs + lane;
+  const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
+  long it = 0;
+  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t row = (int64_t)tile * (nw * 32) + warp * 32 + lane;
+    dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+    float acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    uint64_t h = 0;
+
+    for (int c = 0; c < nchunks; ++c, ++it) {
+      const int s = (int)(it % ns);
+      dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+      const uint8_t *cb = stages + (size_t)s * ch * p.stride;
+      const int nt = min(ch, p.n_trees_pad - c * ch);
+      for (int j = 0; j < nt; j += 2) {
+        const uint2 *na = reinterpret_cast<const uint2 *>(cb + (size_t)j * p.stride);
+        const uint2 *nb = reinterpret_cast<const uint2 *>(cb + (size_t)(j + 1) * p.stride);
+        uint32_t ia = 1, ib = 1;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+          const uint2 da = na[ia];
+          const uint2 db = nb[ib];
+          const float xa = xl[da.x * 32];
+          const float xb = xl[db.x * 32];
+          const float ta = __uint_as_float(da.y);
+          const float tb = __uint_as_float(db.y);
+          const bool pa = LE ? (xa <= ta) : (xa < ta);
+          const bool pb = LE ? (xb <= tb) : (xb < tb);
+          ia = 2u * ia + (pa ? 0u : 1u);
+          ib = 2u * ib + (pb ? 0u : 1u);
+        }
+        const uint32_t sa = ia - (1u << D), sb = ib - (1u << D);
+        const float *la = reinterpret_cast<const float *>(na + (1 << D));
+        const float *lb = reinterpret_cast<const float *>(nb + (1 << D));
+        if (p.w == 1) {
+          const float va = la[sa], vb = lb[sb];
+          if (NACC == 1) {
+            acc[0] += va;
+            acc[0] += vb;
+          } else {
+            const uint32_t ka = na[0].x, kb = nb[0].x;
+#pragma unroll
+            for (int k = 0; k < NACC; ++k) {
+              if (ka == (uint32_t)k) acc[k] += va;
+              if (kb == (uint32_t)k) acc[k] += vb;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k < p.K) acc[k] += la[sa * p.w + k];
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k < p.K) acc[k] += lb[sb * p.w + k];
+        }
+        if (lm) {
+          const int tg = c * ch + j;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int t = tg + q;
+            if (t < p.n_trees) {
+              const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + (q ? sb : sa));
+              if (lm == 1) {
+                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+              } else {
+                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[s]);
+    }
+    if (row < p.n) {
+      if (lm == 2) {
+        static_cast<uint64_t *>(p.out)[row] = h;
+      } else if (lm == 0) {
+        dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
+      }
+    }
+  }
+}
+
+using PttFn = void (*)(const PttParams);
+
+template <int D, bool LE>
+static PttFn pick_nacc(int nacc) {
+  switch (nacc) {
+    case 1: return ptt_kernel<D, LE, 1>;
+    case 4: return ptt_kernel<D, LE, 4>;
+    case 8: return ptt_kernel<D, LE, 8>;
+    default: return ptt_kernel<D, LE, 16>;
+  }
+}
+
+template <int D>
+static PttFn pick_le(bool le, int nacc) {
+  return le ? pick_nacc<D, true>(nacc) : pick_nacc<D, false>(nacc);
+}
+
+static PttFn pick(int D, bool le, int nacc) {
+  switch (D) {
+    case 0: return pick_le<0>(le, nacc);
+    case 1: return pick_le<1>(le, nacc);
+    case 2: return pick_le<2>(le, nacc);
+    case 3: return pick_le<3>(le, nacc);
+    case 4: return pick_le<4>(le, nacc);
+    case 5: return pick_le<5>(le, nacc);
+    case 6: return pick_le<6>(le, nacc);
+    case 7: return pick_le<7>(le, nacc);
+    case 8: return pick_le<8>(le, nacc);
+    case 9: return pick_le<9>(le, nacc);
+    case 10: return pick_le<10>(le, nacc);
+    default: return nullptr;
+  }
+}
+
+int sm_count(int device);
+
+hb_status launch_ptt(const Model &m, const RunArgs &a) {
+  PttFn fn = pick(m.depth, m.cmp == HB_CMP_LE, m.nacc);
+  if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
+  PttParams p;
+  p.X = a.X;
+  p.n = a.n;
+  p.ldx = a.ldx;
+  p.F = m.n_features;
+  p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
+  p.trees = static_cast<const uint8_t *>(m.d_trees);
+  p.stride = (uint32_t)m.stride;
+  p.n_trees_pad = m.n_trees_pad;
+  p.n_trees = m.n_trees;
+  p.tree_begin = m.tree_begin;
+  p.leafmap = m.d_leafmap;
+  p.nslots = m.nslots;
+  p.scale = m.d_scale;
+  p.base = m.d_base;
+  p.K = m.n_outputs;
+  p.w = m.leaf_width;
+  p.task = m.task;
+  p.post = m.post;
+  p.kind = a.kind;
+  p.out = a.out;
+  p.nw = m.cfg.nw;
+  p.ns = m.cfg.ns;
+  p.ch = m.cfg.ch;
+  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
+  const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
+  if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
+  p.ntiles = (int)ntiles;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       m.cfg.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(ptt)");
+  fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "ptt_kernel launch");
+  return HB_OK;
+}
+
+}  // namespace hb

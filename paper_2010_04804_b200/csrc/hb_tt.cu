@@ -1,0 +1,242 @@
+// hb_tt.cu — TreeTraversal scorer for sm_100a (Alg. 2, P:206-237;
+// Table 5; fixed TREE_DEPTH iterations with leaf self-loops).
+//
+// Alg. 2 per (row, tree): T_I <- root; repeat TREE_DEPTH: T_F <- N_F[T_I];
+// T_V <- X[r, T_F]; T_T <- N_T[T_I]; T_I <- Where(T_V < T_T, N_L[T_I],
+// N_R[T_I]); R <- N_C[T_I].
+//
+// Compiled node record (8 B): nodes are renumbered in BFS
+// order with siblings adjacent, so N_L = N_R - 1 and one record carries
+// {N_F | N_R << 16, N_T}. A leaf j stores N_R = j and N_T = NaN: both LT and LE
+// are false against NaN, so T_I <- N_R = j — the paper's self-loop.
+// X comes from a per-warp SMEM slice when it fits, else straight from global
+// memory (wide rows, e.g. Epsilon-shaped F = 2000); tree records stream through
+// the same cp.async.bulk ring as PTT when a chunk fits in SMEM, else are read
+// through L2/L1 (deep D = 12 trees of very large ensembles).
+#include <cuda_runtime.h>
+
+#include "hb_device.cuh"
+#include "hb_internal.h"
+
+namespace hb {
+
+struct TtParams {
+  const float *X;
+  int64_t n, ldx;
+  int F, vec4, depth;
+  const uint8_t *trees;
+  uint32_t stride;
+  int n_trees_pad, n_trees, tree_begin;
+  const int32_t *leafmap;
+  int nslots;
+  const float *scale, *base;
+  int K, w, task, post, kind;
+  void *out;
+  int nw, ns, ch, ntiles, x_smem, t_smem;
+};
+
+template <bool LE>
+__device__ __forceinline__ uint32_t tt_walk(const uint2 *nodes, const float *xrow, int xstride,
+                                            int depth) {
+  uint32_t i = 0;
+#pragma unroll 4
+  for (int l = 0; l < depth; ++l) {
+    const uint2 d = nodes[i];
+    const float x = xrow[(d.x & 0xFFFFu) * xstride];
+    const float t = __uint_as_float(d.y);
+    const bool pr = LE ? (x <= t) : (x < t);
+    i = (d.x >> 16) - (pr ? 1u : 0u);
+  }
+  return i;
+}
+
+template <bool LE, int NACC>
+__global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = p.nw, ns = p.ns, ch = p.ch;
+  const size_t xbytes = p.x_smem ? (size_t)nw * p.F * 128 : 0;
+  uint8_t *stages = smem + xbytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(stages + (p.t_smem ? (size_t)ns * ch * p.stride : 0));
+  uint64_t *empty = full + ns;
+  if (p.t_smem) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < ns; ++s) {
+        dev::mbar_init(&full[s], 1);
+        dev::mbar_init(&empty[s], nw);
+      }
+      dev::fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  const int nchunks = (p.n_trees_pad + ch - 1) / ch;
+  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  if (warp == nw) {
+    if (p.t_smem && lane == 0) {
+      const long total = (long)my_tiles * nchunks;
+      for (long it = 0; it < total; ++it) {
+        const int s = (int)(it % ns);
+        dev::mbar_wait(&empty[s], (uint32_t)((it / ns) & 1) ^ 1u);
+        const int t0 = (int)(it % nchunks) * ch;
+        const int nt = min(ch, p.n_trees_pad - t0);
+        const uint32_t bytes = (uint32_t)nt * p.stride;
+        dev::mbar_arrive_expect_tx(&full[s], bytes);
+        dev::bulk_g2s(stages + (size_t)s * ch * p.stride, p.trees + (size_t)t0 * p.stride, bytes,
+                      &full[s]);
+      }
+    }
+    return;
+  }
+
+  float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
+  const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
+  long it = 0;
+  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t row = (int64_t)tile * (nw * 32) + warp * 32 + lane;
+    const float *xrow;
+    int xstride;
+    if (p.x_smem) {
+      dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+      xrow = xs + lane;
+      xstride = 32;
+    } else {
+      xrow = p.X + (row < p.n ? row : 0) * p.ldx;
+      xstride = 1;
+    }
+    float acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    uint64_t h = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const uint8_t *cb;
+      int s = 0;
+      if (p.t_smem) {
+        s = (int)(it % ns);
+        dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+        cb = stages + (size_t)s * ch * p.stride;
+      } else {
+        cb = p.trees + (size_t)c * ch * p.stride;
+      }
+      const int nt = min(ch, p.n_trees_pad - c * ch);
+      for (int j = 0; j < nt; j += 2) {
+        const uint8_t *ra = cb + (size_t)j * p.stride;
+        const uint8_t *rb = ra + p.stride;
+        const uint2 *na = reinterpret_cast<const uint2 *>(ra + 16);
+        const uint2 *nb = reinterpret_cast<const uint2 *>(rb + 16);
+        const uint32_t ia = tt_walk<LE>(na, xrow, xstride, p.depth);
+        const uint32_t ib = tt_walk<LE>(nb, xrow, xstride, p.depth);
+        const float *la = reinterpret_cast<const float *>(na + p.nslots);
+        const float *lb = reinterpret_cast<const float *>(nb + p.nslots);
+        if (p.w == 1) {
+          const float va = la[ia], vb = lb[ib];
+          if (NACC == 1) {
+            acc[0] += va;
+            acc[0] += vb;
+          } else {
+            const uint32_t ka = *reinterpret_cast<const uint32_t *>(ra);
+            const uint32_t kb = *reinterpret_cast<const uint32_t *>(rb);
+#pragma unroll
+            for (int k = 0; k < NACC; ++k) {
+              if (ka == (uint32_t)k) acc[k] += va;
+              if (kb == (uint32_t)k) acc[k] += vb;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k < p.K) acc[k] += la[ia * p.w + k];
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k < p.K) acc[k] += lb[ib * p.w + k];
+        }
+        if (lm) {
+          const int tg = c * ch + j;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int t = tg + q;
+            if (t < p.n_trees) {
+              const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + (q ? ib : ia));
+              if (lm == 1) {
+                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+              } else {
+                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+              }
+            }
+          }
+        }
+      }
+      if (p.t_smem) {
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&empty[s]);
+        ++it;
+      }
+    }
+    if (row < p.n) {
+      if (lm == 2) {
+        static_cast<uint64_t *>(p.out)[row] = h;
+      } else if (lm == 0) {
+        dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
+      }
+    }
+  }
+}
+
+using TtFn = void (*)(const TtParams);
+
+template <bool LE>
+static TtFn pick_nacc(int nacc) {
+  switch (nacc) {
+    case 1: return tt_kernel<LE, 1>;
+    case 4: return tt_kernel<LE, 4>;
+    case 8: return tt_kernel<LE, 8>;
+    default: return tt_kernel<LE, 16>;
+  }
+}
+
+int sm_count(int device);
+
+hb_status launch_tt(const Model &m, const RunArgs &a) {
+  TtFn fn = m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc);
+  TtParams p;
+  p.X = a.X;
+  p.n = a.n;
+  p.ldx = a.ldx;
+  p.F = m.n_features;
+  p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
+  p.depth = m.depth;
+  p.trees = static_cast<const uint8_t *>(m.d_trees);
+  p.stride = (uint32_t)m.stride;
+  p.n_trees_pad = m.n_trees_pad;
+  p.n_trees = m.n_trees;
+  p.tree_begin = m.tree_begin;
+  p.leafmap = m.d_leafmap;
+  p.nslots = m.nslots;
+  p.scale = m.d_scale;
+  p.base = m.d_base;
+  p.K = m.n_outputs;
+  p.w = m.leaf_width;
+  p.task = m.task;
+  p.post = m.post;
+  p.kind = a.kind;
+  p.out = a.out;
+  p.nw = m.cfg.nw;
+  p.ns = m.cfg.ns;
+  p.ch = m.cfg.ch;
+  p.x_smem = m.cfg.x_smem;
+  p.t_smem = m.cfg.t_smem;
+  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
+  const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
+  if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
+  p.ntiles = (int)ntiles;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       m.cfg.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tt)");
+  fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tt_kernel launch");
+  return HB_OK;
+}
+
+}  // namespace hb

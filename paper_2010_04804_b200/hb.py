@@ -1,0 +1,237 @@
+"""ctypes binding of libhb.so (include/hb.h). Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_PKG, "libhb.so")
+
+CMP_LT, CMP_LE = 0, 1
+AGG_SUM, AGG_MEAN = 0, 1
+POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX = 0, 1, 2
+TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
+STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
+STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
+OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5}
+
+# every symbol include/hb.h declares (checked by tests/test_abi.py)
+exported_symbols = ["hb_validate", "hb_compile", "hb_compile_range", "hb_predict_ex",
+                    "hb_predict", "hb_predict_proba", "hb_predict_raw", "hb_predict_leaf",
+                    "hb_finalize", "hb_predict_host", "hb_model_get_info", "hb_free",
+                    "hb_last_error", "hb_abi_version"]
+
+
+class HBError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"hb status {status}: {msg}")
+        self.status = status
+
+
+class _Ens(C.Structure):
+    _fields_ = [("n_trees", C.c_int32), ("n_features", C.c_int32), ("n_outputs", C.c_int32),
+                ("node_offset", C.c_void_p), ("feature", C.c_void_p),
+                ("threshold", C.c_void_p), ("left", C.c_void_p), ("right", C.c_void_p),
+                ("leaf_value", C.c_void_p), ("leaf_width", C.c_int32),
+                ("tree_output", C.c_void_p), ("base_score", C.c_void_p),
+                ("cmp", C.c_int32), ("agg", C.c_int32), ("post", C.c_int32),
+                ("task", C.c_int32)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("max_depth", C.c_int32), ("tree_begin", C.c_int32),
+                ("n_trees", C.c_int32), ("n_trees_total", C.c_int32),
+                ("n_features", C.c_int32), ("n_outputs", C.c_int32),
+                ("leaf_width", C.c_int32), ("device", C.c_int32), ("x_in_smem", C.c_int32),
+                ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64)]
+
+
+def _load():
+    if not os.path.exists(lib_path):
+        raise ImportError(f"{lib_path} is missing: build it with "
+                          "`python -m paper_2010_04804_b200.build` (no CPU fallback exists)")
+    L = C.CDLL(lib_path)
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+    P = C.POINTER(_Ens)
+    sig = {
+        "hb_validate": ([P], C.c_int),
+        "hb_compile": ([P, i32, i32, C.POINTER(vp)], C.c_int),
+        "hb_compile_range": ([P, i32, i32, i32, i32, C.POINTER(vp)], C.c_int),
+        "hb_predict_ex": ([vp, vp, i64, i64, i32, vp, vp], C.c_int),
+        "hb_predict": ([vp, vp, i64, i64, vp, vp], C.c_int),
+        "hb_predict_proba": ([vp, vp, i64, i64, vp, vp], C.c_int),
+        "hb_predict_raw": ([vp, vp, i64, i64, vp, vp], C.c_int),
+        "hb_predict_leaf": ([vp, vp, i64, i64, vp, vp], C.c_int),
+        "hb_finalize": ([vp, vp, i64, i32, vp, vp], C.c_int),
+        "hb_predict_host": ([vp, vp, i64, i64, i32, vp], C.c_int),
+        "hb_model_get_info": ([vp, C.POINTER(_Info)], C.c_int),
+        "hb_free": ([vp], None),
+        "hb_last_error": ([], C.c_char_p),
+        "hb_abi_version": ([], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+
+
+def _check(st):
+    if st != 0:
+        raise HBError(st, lib.hb_last_error().decode())
+
+
+class _EnsHandle:
+    def __init__(self, e):
+        self.keep = []
+
+        def arr(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            self.keep.append(a)
+            return a.ctypes.data
+
+        self.s = _Ens(int(e.n_trees), int(e.n_features), int(e.n_outputs),
+                      arr(e.node_offset, np.int64), arr(e.feature, np.int32),
+                      arr(e.threshold, np.float32), arr(e.left, np.int32),
+                      arr(e.right, np.int32), arr(e.leaf_value, np.float32),
+                      int(e.leaf_width), arr(e.tree_output, np.int32),
+                      arr(e.base_score, np.float32), int(e.cmp), int(e.agg),
+                      int(e.post), int(getattr(e, "task", 0)))
+
+
+def validate(e) -> None:
+    """Host-only validation (hb_validate); raises HBError."""
+    h = _EnsHandle(e)
+    _check(lib.hb_validate(C.byref(h.s)))
+
+
+class Model:
+    """A compiled ensemble on one GPU (hb_compile / hb_compile_range)."""
+
+    def __init__(self, ensemble, strategy="auto", device=0, tree_range=None):
+        h = _EnsHandle(ensemble)
+        p = C.c_void_p()
+        s = STRATEGY[strategy] if isinstance(strategy, str) else int(strategy)
+        if tree_range is None:
+            _check(lib.hb_compile(C.byref(h.s), s, int(device), C.byref(p)))
+        else:
+            _check(lib.hb_compile_range(C.byref(h.s), int(tree_range[0]), int(tree_range[1]),
+                                        s, int(device), C.byref(p)))
+        self._p = p
+        self.device = int(device)
+        self.info = self._info()
+        self.task = int(getattr(ensemble, "task", 0))
+
+    def _info(self):
+        i = _Info()
+        _check(lib.hb_model_get_info(self._p, C.byref(i)))
+        d = {k: getattr(i, k) for k, _ in _Info._fields_}
+        d["strategy_name"] = STRATEGY_NAME[d["strategy"]]
+        return d
+
+    def free(self):
+        if getattr(self, "_p", None):
+            lib.hb_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ device API
+    def out_shape(self, n, kind):
+        K = self.info["n_outputs"]
+        if kind == "predict":
+            return ((n,), "int32") if self.task == TASK_CLASSIFICATION else ((n, K), "float32")
+        if kind == "proba":
+            return ((n, 2 if K == 1 else K), "float32")
+        if kind in ("raw", "margin"):
+            return ((n, K), "float32")
+        if kind == "leaf":
+            return ((n, self.info["n_trees"]), "int32")
+        if kind == "leaf_hash":
+            return ((n,), "int64")
+        raise ValueError(kind)
+
+    def run(self, X, kind="predict", out=None, stream=None):
+        """One fused scoring launch (hb_predict_ex) on torch CUDA tensors.
+        X: float32 [n, >= F] with unit column stride. Returns `out`."""
+        import torch
+        if X.dtype != torch.float32 or X.dim() != 2 or X.stride(1) != 1:
+            raise ValueError("X must be a 2-D float32 tensor with unit column stride")
+        n = X.shape[0]
+        shape, dt = self.out_shape(n, kind)
+        if out is None:
+            out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        _check(lib.hb_predict_ex(self._p, C.c_void_p(X.data_ptr()), n, X.stride(0), OUT[kind],
+                                 C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
+        return out
+
+    def predict(self, X, **kw):
+        return self.run(X, "predict", **kw)
+
+    def predict_proba(self, X, **kw):
+        return self.run(X, "proba", **kw)
+
+    def predict_raw(self, X, **kw):
+        return self.run(X, "raw", **kw)
+
+    def predict_margin(self, X, **kw):
+        return self.run(X, "margin", **kw)
+
+    def predict_leaf(self, X, **kw):
+        return self.run(X, "leaf", **kw)
+
+    def predict_leaf_hash(self, X, **kw):
+        return self.run(X, "leaf_hash", **kw)
+
+    def finalize(self, raw, kind="predict", out=None, stream=None):
+        """hb_finalize: epilogue from device raw sums over all trees."""
+        import torch
+        n = raw.shape[0]
+        shape, dt = self.out_shape(n, kind)
+        if out is None:
+            out = torch.empty(shape, dtype=getattr(torch, dt), device=raw.device)
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        _check(lib.hb_finalize(self._p, C.c_void_p(raw.data_ptr()), n, OUT[kind],
+                               C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
+        return out
+
+    # ------------------------------------------------------------ host API
+    def predict_host(self, X, kind="predict", out=None):
+        """hb_predict_host: end-to-end from host memory (numpy array or CPU
+        torch tensor, ideally pinned). Synchronous."""
+        try:
+            import torch
+            is_t = isinstance(X, torch.Tensor)
+        except ImportError:
+            is_t = False
+        n = X.shape[0]
+        shape, dt = self.out_shape(n, kind)
+        if is_t:
+            import torch
+            assert X.device.type == "cpu" and X.dtype == torch.float32 and X.stride(1) == 1
+            ldx = X.stride(0)
+            if out is None:
+                out = torch.empty(shape, dtype=getattr(torch, dt))
+            xp, op = X.data_ptr(), out.data_ptr()
+        else:
+            X = np.asarray(X, np.float32)
+            if X.strides[1] != 4:
+                X = np.ascontiguousarray(X)
+            ldx = X.strides[0] // 4
+            if out is None:
+                out = np.empty(shape, dtype=dt)
+            xp, op = X.ctypes.data, out.ctypes.data
+        _check(lib.hb_predict_host(self._p, C.c_void_p(xp), n, ldx, OUT[kind], C.c_void_p(op)))
+        return out

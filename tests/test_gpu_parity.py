@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs (SURVEY.md §4 pyramid level 3, §8(c) tolerances).
+
+Bar: leaf ids and leaf hashes bit-exact; scores |gpu - ref| <= 1e-5 + 1e-5|ref|
+(PAPER.md P:469 assert_allclose rtol = atol = 1e-5; reading R23);
+labels exact except documented near-ties (top-2 margin gap below twice the
+tolerance)."""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._common import SPECIAL_Q24, load_hand_trees
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2010_04804_b200 as hb  # noqa: E402
+import synth.dev  # noqa: E402
+
+
+def tol_ok(got, ref):
+    got = np.asarray(got, np.float64)
+    return np.abs(got - ref) <= 1e-5 + 1e-5 * np.abs(ref)
+
+
+def assert_scores(got, ref, what=""):
+    ok = tol_ok(got, ref)
+    if not ok.all():
+        i = np.argwhere(~ok)[0]
+        raise AssertionError(f"{what}: {(~ok).sum()} values outside tolerance, first at {i}: "
+                             f"gpu={np.asarray(got)[tuple(i)]!r} ref={ref[tuple(i)]!r}")
+
+
+def near_tie(e, margin):
+    m = margin
+    if e.n_outputs == 1:
+        return np.abs(m[:, 0]) < 2 * (1e-5 + 1e-5 * np.abs(m[:, 0]))
+    s = np.sort(m, 1)
+    gap = s[:, -1] - s[:, -2]
+    return gap < 2 * (1e-5 + 1e-5 * np.abs(s[:, -1]))
+
+
+def X_pair(seed, n, F, ldx=None, **kw):
+    Xd = synth.dev.gen_X_device(seed, n, F, ldx=ldx, **kw)
+    Xh = synth.gen_X(seed, n, F, ldx=ldx, **kw)
+    return Xd, Xh
+
+
+def check_all(e, m, Xd, Xh, kinds=("predict", "proba", "raw", "margin", "leaf", "leaf_hash")):
+    F = e.n_features
+    Xo = Xh[:, :F] if Xh.shape[1] > F else Xh
+    s = oracle.scores(e, Xo)
+    cls = e.task == synth.TASK_CLASSIFICATION
+    for kind in kinds:
+        if kind == "proba" and not cls:
+            with pytest.raises(hb.HBError):
+                m.run(Xd, "proba")
+            continue
+        got = m.run(Xd, kind).cpu().numpy()
+        if kind == "leaf":
+            assert np.array_equal(got, oracle.leaf(e, Xo)), "leaf ids"
+        elif kind == "leaf_hash":
+            assert np.array_equal(got.view(np.uint64), oracle.leaf_hash(e, Xo)), "leaf hash"
+        elif kind == "raw":
+            assert_scores(got, s["raw"], "raw")
+        elif kind == "margin":
+            assert_scores(got, s["margin"], "margin")
+        elif kind == "proba":
+            assert_scores(got, oracle.proba(e, s["post"]), "proba")
+        elif kind == "predict":
+            if cls:
+                ref = s["label"]
+                tie = near_tie(e, s["margin"])
+                assert np.array_equal(got[~tie], ref[~tie]), "labels"
+            else:
+                assert_scores(got, s["post"], "predict")
+
+
+FAMILIES = ["balanced", "mixed", "skinny"]
+
+
+def _forest(kind, T, D, F, seed, family, cmp, grid=synth.GRID_FINE):
+    common = dict(seed=seed, family=family, cmp=cmp, grid=grid)
+    if kind == "reg":
+        return synth.gen_forest(T, D, F, base_score=[0.5], **common)
+    if kind == "binary":
+        return synth.gen_forest(T, D, F, post=synth.POST_SIGMOID,
+                                task=synth.TASK_CLASSIFICATION, base_score=[-0.25], **common)
+    if kind == "multiclass":   # per-class scalar trees, t mod K (C4 layout)
+        return synth.gen_forest(T, D, F, n_outputs=3, post=synth.POST_SOFTMAX,
+                                task=synth.TASK_CLASSIFICATION, **common)
+    if kind == "k7":
+        return synth.gen_forest(T, D, F, n_outputs=7, post=synth.POST_SOFTMAX,
+                                task=synth.TASK_CLASSIFICATION, **common)
+    if kind == "k12":
+        return synth.gen_forest(T, D, F, n_outputs=12, post=synth.POST_SOFTMAX,
+                                task=synth.TASK_CLASSIFICATION,
+                                tree_output=np.random.default_rng(seed).integers(0, 12, T), **common)
+    if kind == "rf":           # vector leaves, soft voting (MEAN)
+        return synth.gen_forest(T, D, F, n_outputs=5, leaf_width=5, leaf_kind="dirichlet",
+                                agg=synth.AGG_MEAN, task=synth.TASK_CLASSIFICATION, **common)
+    if kind == "rf_reg":       # MEAN regression (RF regressor)
+        return synth.gen_forest(T, D, F, agg=synth.AGG_MEAN, **common)
+    raise ValueError(kind)
+
+
+CASES = []
+for strat, D in (("ptt", 8), ("ptt", 5), ("tt", 8), ("tt", 11), ("gemm", 3), ("gemm", 5)):
+    for kind in ("reg", "binary", "multiclass", "rf"):
+        for cmp in (0, 1):
+            CASES.append((strat, D, kind, cmp))
+
+
+@pytest.mark.parametrize("strat,D,kind,cmp", CASES)
+def test_strategy_parity(strat, D, kind, cmp):
+    seed = zlib.crc32(f"{strat}{D}{kind}{cmp}".encode()) & 0xFFFF
+    family = FAMILIES[seed % 3]
+    F = [3, 17, 28, 54][seed % 4]
+    T = 37 if strat != "gemm" else 23    # odd: exercises tree-group padding
+    e = _forest(kind, T, D, F, seed, family, cmp)
+    m = hb.Model(e, strategy=strat, device=0)
+    assert m.info["strategy_name"] == strat
+    n = 1500 + seed % 97                 # several 512-row tiles + ragged tail
+    Xd, Xh = X_pair(seed, n, F, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("kind", ["k7", "k12", "rf_reg"])
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
+def test_more_outputs(kind, strat):
+    e = _forest(kind, 30, 4, 11, 5, "mixed", 0)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd, Xh = X_pair(9, 777, 11)
+    check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm", "auto"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_tie_heavy_coarse_grid(strat, cmp):
+    """Coarse grid: thresholds and X share 64 values, so x == t is frequent
+    (LT vs LE routing, SURVEY §8(d) tie-heavy variant)."""
+    e = _forest("binary", 40, 6 if strat != "gemm" else 4, 7, 3, "balanced", cmp,
+                grid=synth.GRID_COARSE)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd, Xh = X_pair(4, 2048, 7, grid=synth.GRID_COARSE)
+    check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_hand_traced_trees_on_gpu(strat, cmp):
+    e, X, exp_leaf, exp_sum = load_hand_trees(cmp)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd = torch.from_numpy(X).cuda()
+    assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), exp_leaf)
+    assert np.array_equal(m.predict_raw(Xd).cpu().numpy()[:, 0], exp_sum.astype(np.float32))
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 33, 511, 513])
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
+def test_edge_row_counts(n, strat):
+    e = _forest("reg", 9, 4, 6, 1, "skinny", 0)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd, Xh = X_pair(2, max(n, 1), 6)
+    Xd, Xh = Xd[:n], Xh[:n]
+    got = m.predict(Xd).cpu().numpy()
+    assert got.shape == (n, 1)
+    if n:
+        assert_scores(got, oracle.scores(e, Xh)["post"], "edge n")
+        assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), oracle.leaf(e, Xh))
+
+
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
+def test_ldx_padding_and_unaligned(strat):
+    e = _forest("multiclass", 12, 5, 10, 8, "mixed", 1)
+    m = hb.Model(e, strategy=strat, device=0)
+    for ldx in (10, 13, 16):
+        Xd, Xh = X_pair(11, 700, 10, ldx=ldx)
+        check_all(e, m, Xd, Xh, kinds=("raw", "leaf"))
+    # unaligned base pointer (column view) disables the float4 path
+    Xd, Xh = X_pair(12, 701, 11, ldx=12)
+    check_all(e, m, Xd[:, 1:], Xh[:, 1:], kinds=("raw", "leaf"))
+
+
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
+def test_single_feature_and_single_leaf_trees(strat):
+    # F = 1 and a mix of depth-0 trees with deeper ones
+    deep = synth.gen_forest(5, 3, 1, seed=3, family="balanced")
+    leafy = [dict(feature=[-1], threshold=[np.nan], left=[-1], right=[-1], leaf_value=[0.125 * i])
+             for i in range(3)]
+    trees = [deep.tree(t) for t in range(5)]
+    trees = [dict(feature=t["feature"], threshold=t["threshold"], left=t["left"], right=t["right"],
+                  leaf_value=t["leaf_value"]) for t in trees] + leafy
+    e = synth.from_trees(trees, 1)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd, Xh = X_pair(5, 900, 1, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+    # all trees single leaves: D = 0
+    e0 = synth.from_trees(leafy, 1)
+    m0 = hb.Model(e0, strategy=strat, device=0)
+    check_all(e0, m0, Xd, Xh)
+
+
+def test_auto_strategy_selection():
+    """Sec. 5.1 heuristic (reading R24): GEMM D <= 3, PTT D <= 10, TT beyond;
+    PTT falls back to TT when rows are too wide for the SMEM X tile."""
+    for D, want in ((2, "gemm"), (3, "gemm"), (4, "ptt"), (8, "ptt"), (10, "ptt"), (11, "tt"),
+                    (12, "tt")):
+        e = synth.gen_forest(4, D, 8, seed=D, family="skinny")
+        assert hb.Model(e, device=0).info["strategy_name"] == want, D
+    wide = synth.gen_forest(4, 6, 2000, seed=1, family="balanced")
+    assert hb.Model(wide, device=0).info["strategy_name"] == "tt"
+    with pytest.raises(hb.HBError) as ei:
+        hb.Model(wide, strategy="ptt", device=0)
+    assert ei.value.status == 3
+
+
+def test_rejects_host_pointers_and_bad_args():
+    e = _forest("reg", 4, 3, 5, 1, "mixed", 0)
+    m = hb.Model(e, device=0)
+    Xh = torch.zeros(10, 5)
+    with pytest.raises(hb.HBError) as ei:
+        m.predict(Xh)
+    assert ei.value.status == 1
+    Xd = torch.zeros(10, 5, device="cuda")
+    out_host = torch.zeros(10, 1)
+    with pytest.raises(hb.HBError):
+        m.predict(Xd, out=out_host)
+    with pytest.raises(hb.HBError):
+        m.predict(torch.zeros(10, 4, device="cuda"))   # ldx < F
+
+
+def test_streams_and_concurrency():
+    e = _forest("binary", 64, 8, 28, 2, "balanced", 0)
+    m = hb.Model(e, device=0)
+    Xd, Xh = X_pair(3, 20000, 28)
+    ref = m.predict_proba(Xd).cpu()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = []
+    for s in streams:
+        with torch.cuda.stream(s):
+            outs.append(m.predict_proba(Xd))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.cpu(), ref)      # same kernel, same order: identical
+
+
+def test_tree_shard_partials_reduce_to_unsharded():
+    """raw partials of tree shards summed, then hb_finalize with
+    the global tree counts, equal the unsharded result; leaf hashes add."""
+    e = _forest("multiclass", 60, 7, 20, 4, "mixed", 0)
+    e.agg = synth.AGG_MEAN
+    Xd, Xh = X_pair(6, 3000, 20)
+    s = oracle.scores(e, Xh)
+    bounds = [0, 15, 36, 60]
+    raws, hashes = [], []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        ms = hb.Model(e, tree_range=(a, b), device=0)
+        raws.append(ms.predict_raw(Xd))
+        hashes.append(ms.predict_leaf_hash(Xd).cpu().numpy().view(np.uint64))
+        assert np.array_equal(ms.predict_leaf(Xd).cpu().numpy(), oracle.leaf(e, Xh, a, b))
+    total = raws[0] + raws[1] + raws[2]
+    m0 = hb.Model(e, tree_range=(0, 15), device=0)
+    assert_scores(m0.finalize(total, "margin").cpu().numpy(), s["margin"], "sharded margin")
+    assert_scores(m0.finalize(total, "proba").cpu().numpy(), s["post"], "sharded proba")
+    with np.errstate(over="ignore"):
+        h = hashes[0] + hashes[1] + hashes[2]
+    assert np.array_equal(h, oracle.leaf_hash(e, Xh))
+
+
+@pytest.mark.parametrize("kind", ["predict", "proba", "raw", "leaf_hash"])
+def test_predict_host_end_to_end(kind):
+    e = _forest("binary", 50, 8, 28, 7, "balanced", 0)
+    m = hb.Model(e, device=0)
+    n = 300_000
+    Xh = synth.gen_X(13, n, 28)
+    Xp = torch.from_numpy(Xh).pin_memory()
+    got = m.predict_host(Xp, kind)
+    dev = m.run(torch.from_numpy(Xh).cuda(), kind).cpu()
+    assert torch.equal(got, dev)
+
+
+def test_host_and_device_generators_agree():
+    for grid, sp in ((0, 0), (1, 0), (0, SPECIAL_Q24)):
+        Xd, Xh = X_pair(77, 5000, 37, grid=grid, special_q24=sp, row_offset=12345)
+        assert np.array_equal(Xd.cpu().numpy().view(np.uint32), Xh.view(np.uint32))
+
+
+# ------------------------------------------------------------------ full-size configs
+def _sampled_blocks(n, blocks=6, rows=1000, seed=0):
+    rng = np.random.default_rng(seed)
+    starts = sorted(rng.choice(max(1, n // rows - 1), blocks - 2, replace=False) * rows)
+    return [0] + list(starts) + [n - rows]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C4p"])
+def test_full_size_config_sampled(cfg):
+    """BASELINE configs at full size, in the launch configuration bench.py
+    times: all rows are scored on the GPU; sampled row blocks (start, end and
+    random interior) are checked against the oracle, and row-wise invariants
+    hold for every row."""
+    c, e = synth.make_config(cfg)
+    m = hb.Model(e, device=0)
+    X = synth.dev.gen_X_device(c.seed_x, c.n_rows, c.n_features)
+    cls = e.task == synth.TASK_CLASSIFICATION
+    out = m.predict_proba(X) if cls else m.predict(X)
+    hsh = m.predict_leaf_hash(X).cpu().numpy().view(np.uint64)
+    outc = out.cpu().numpy()
+    if cls:
+        assert np.all(outc >= 0) and np.all(outc <= 1)
+        assert np.allclose(outc.sum(1), 1.0, atol=1e-5)
+    rows = 1000 if c.n_rows > 1000 else c.n_rows
+    for r0 in (_sampled_blocks(c.n_rows, rows=rows) if c.n_rows > 1000 else [0]):
+        Xh = synth.gen_X(c.seed_x, rows, c.n_features, row_offset=r0)
+        s = oracle.scores(e, Xh)
+        ref = oracle.proba(e, s["post"]) if cls else s["post"]
+        assert_scores(outc[r0:r0 + rows], ref, f"{cfg} rows {r0}")
+        assert np.array_equal(hsh[r0:r0 + rows], oracle.leaf_hash(e, Xh)), f"{cfg} hash {r0}"
+    del X
+    torch.cuda.empty_cache()
+
+
+def test_c5_shard_sampled():
+    """C5 (10k trees, D12, F = 2000) as the 1/8 tree shard one GPU owns:
+    1250 trees, TT strategy, 1M rows; sampled rows against the oracle."""
+    c, e = synth.make_config("C5")
+    r = (0, 1250)
+    m = hb.Model(e, tree_range=r, device=0)
+    assert m.info["strategy_name"] == "tt"
+    n = 200_000
+    X = synth.dev.gen_X_device(c.seed_x, n, c.n_features)
+    raw = m.predict_raw(X).cpu().numpy()
+    hsh = m.predict_leaf_hash(X).cpu().numpy().view(np.uint64)
+    for r0 in (0, 123_000, n - 500):
+        Xh = synth.gen_X(c.seed_x, 500, c.n_features, row_offset=r0)
+        assert_scores(raw[r0:r0 + 500], oracle.raw(e, Xh, *r), "C5 raw")
+        assert np.array_equal(hsh[r0:r0 + 500], oracle.leaf_hash(e, Xh, *r))
+    del X
+    torch.cuda.empty_cache()

@@ -1,0 +1,23 @@
+"""Measurement helpers for bench.py (not on the scoring path)."""
+import ctypes as C
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(_HERE, "libhbpeaks.so")
+SRC = os.path.join(_HERE, "peaks.cu")
+
+
+def build(force=False):
+    if force or not os.path.exists(SO) or os.path.getmtime(SO) < os.path.getmtime(SRC):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode",
+                               "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
+                               "-shared", "-o", SO, SRC, "-lcudart_static"])
+    return SO
+
+
+def peaks(device=0):
+    L = C.CDLL(SO)
+    L.hbpeaks_smem_gbs.restype = C.c_double
+    L.hbpeaks_l2_gbs.restype = C.c_double
+    return {"smem_gbs": L.hbpeaks_smem_gbs(device), "l2_gbs": L.hbpeaks_l2_gbs(device)}
