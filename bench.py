@@ -257,7 +257,10 @@ def run_ours(args):
     hbm_peak = measured.get("hbm_gbs", 6650.0)
     roofline = {
         "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-        "frac": achieved / smem_peak, "traffic": prof.get("dram_bytes_per_launch"),
+        "frac": achieved / smem_peak,
+        "traffic": prof.get("smem_ld_bytes_per_launch") if prof.get("rows") == n else None,
+        "traffic_dram": prof.get("dram_bytes_per_launch") if prof.get("rows") == n else None,
+        "traffic_source": prof.get("source"),
         "kernel": f"{info['strategy_name']}_kernel", "kernel_ms": kern_ms,
         "algorithmic_bytes_per_row": per_row,
         "peak_source": "measured LDS.128 microbenchmark (tools/peaks.cu), this run" if peaks.get("smem_gbs")
