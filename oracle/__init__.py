@@ -158,7 +158,7 @@ def scores(e, X, threads=1):
 
 
 def proba(e, post_scores):
-    """Class probabilities as the ABI returns them (reading R13):
+    """Class probabilities as the ABI returns them (reading R27):
     binary sigmoid models give [1-p, p]; K >= 2 gives the post scores."""
     if e.n_outputs == 1:
         p = post_scores[:, 0]

@@ -119,7 +119,7 @@ void oracle_post(const oracle_ensemble *e, const double *margin, int64_t n, doub
   }
 }
 
-/* Labels (reading R14): K == 1 -> 1 iff margin > 0 (sigmoid > 0.5);
+/* Labels (reading R22): K == 1 -> 1 iff margin > 0 (sigmoid > 0.5);
  * K >= 2 -> argmax with the lowest index on ties. */
 void oracle_label(const oracle_ensemble *e, const double *margin, int64_t n, int32_t *out) {
   int32_t K = e->n_outputs;
