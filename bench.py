@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--shard", default=None, choices=["rows", "trees"],
+                    help="default: trees for C5, rows otherwise")
     return ap.parse_args()
 
 
@@ -162,10 +164,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg, e, rows, args):
+def workload_config(cfg, e, rows, args, mode="rows"):
+    par = (f"rows sharded over {args.gpus} GPU(s), no collective" if mode == "rows" else
+           f"trees sharded over {args.gpus} GPU(s), one NCCL reduce of fp32 partials + finalize")
     return {"workload": f"{cfg.name}: {cfg.note}", "rows_per_gpu": rows, "n_trees": e.n_trees,
             "max_depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": e.n_outputs,
-            "family": cfg.family, "parallelism": f"rows sharded over {args.gpus} GPU(s), no collective",
+            "family": cfg.family, "parallelism": par,
             "l2": "inputs larger than L2 (X streamed once per step); model (<13 MB) L2-resident by design"}
 
 
@@ -182,20 +186,44 @@ def run_ours(args):
     import paper_2010_04804_b200 as hb
     import synth
     import synth.dev
+    from paper_2010_04804_b200.dist import max_over_ranks, reduce_partials, tree_shard
 
     cfg, e = synth.make_config(args.config)
     n = args.rows or cfg.n_rows
-    m = hb.Model(e, strategy=args.strategy, device=local)
-    info = m.info
+    mode = args.shard or ("trees" if cfg.name == "C5" else "rows")
     cls = e.task == synth.TASK_CLASSIFICATION
     kind = "proba" if cls else "predict"
-    X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, row_offset=rank * n, device=local)
-    shape, dt = m.out_shape(n, kind)
-    out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
     stream = torch.cuda.current_stream(local)
+    if mode == "rows":
+        # rows sharded, model replicated, no data-path collective (weak scaling)
+        t0, t1 = 0, e.n_trees
+        m = hb.Model(e, strategy=args.strategy, device=local)
+        X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, row_offset=rank * n,
+                                   device=local)
+        shape, dt = m.out_shape(n, kind)
+        out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
 
-    def step():
-        m.run(X, kind, out=out, stream=stream)
+        def step():
+            m.run(X, kind, out=out, stream=stream)
+        launches_per_step = 1
+    else:
+        # trees sharded, all rows on every rank; one NCCL reduce of fp32
+        # partials to rank 0, which finalizes (strong scaling)
+        t0, t1 = tree_shard(e.n_trees, rank, world, e.n_outputs, e.leaf_width)
+        m = hb.Model(e, strategy=args.strategy, device=local, tree_range=(t0, t1))
+        X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, device=local)
+        raw = torch.empty((n, e.n_outputs), dtype=torch.float32, device=X.device)
+        shape, dt = m.out_shape(n, kind)
+        out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
+
+        def step():
+            m.run(X, "raw", out=raw, stream=stream)
+            if dist:
+                reduce_partials(raw, dst=0)
+            if rank == 0:
+                m.finalize(raw, kind, out=out, stream=stream)
+        launches_per_step = 2
+    info = m.info
 
     for _ in range(max(args.warmup, 3)):     # timing rule: >= 3 warm-up steps
         step()
@@ -214,20 +242,26 @@ def run_ours(args):
     t_start.record(stream)
     for i in range(args.steps):
         evs[i][0].record(stream)
-        step()
-        evs[i][1].record(stream)
+        if mode == "rows":
+            step()
+            evs[i][1].record(stream)
+        else:
+            m.run(X, "raw", out=raw, stream=stream)     # the scorer launch alone
+            evs[i][1].record(stream)
+            if dist:
+                reduce_partials(raw, dst=0)
+            if rank == 0:
+                m.finalize(raw, kind, out=out, stream=stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
     total_ms = t_start.elapsed_time(t_end)
     per_launch = [a.elapsed_time(b) for a, b in evs]
     if dist:
-        tt = torch.tensor([total_ms], device=X.device, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+        total_ms = max_over_ranks(total_ms, device=X.device)
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    rows_all = n * world
+    rows_all = n * world if mode == "rows" else n
     value = rows_all / (ms_per_step * 1e-3)
 
     # ---- roofline of the dominant (only) kernel of the step
@@ -236,7 +270,7 @@ def run_ours(args):
     w = info["leaf_width"]
     # per (row, tree) and level one 8-B node record + one 4-B X
     # value; per tree one leaf of 4w B (PTT: D levels by construction).
-    per_row = e.n_trees * (D * 12 + 4 * w)
+    per_row = (t1 - t0) * (D * 12 + 4 * w)
     achieved = per_row * n / (kern_ms * 1e-3) / 1e9
     peaks = {}
     if rank == 0:
@@ -274,7 +308,7 @@ def run_ours(args):
 
     # ---- e2e through the public host API (pinned host buffers)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and mode == "rows":
         del out
         Xh = torch.empty((n, cfg.n_features), dtype=torch.float32).pin_memory()
         Xh.copy_(X.cpu())
@@ -289,9 +323,7 @@ def run_ours(args):
             ts.append(time.perf_counter() - t0)
         t_e2e = float(np.mean(ts))
         if dist:
-            tt = torch.tensor([t_e2e], device=X.device, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
+            t_e2e = max_over_ranks(t_e2e, device=X.device)
         e2e = {"value": rows_all / t_e2e, "unit": "rows/s", "ms_per_step": t_e2e * 1e3,
                "h2d_bytes_per_step": int(n * cfg.n_features * 4),
                "d2h_bytes_per_step": int(oh.numel() * oh.element_size()), "steps": args.e2e_steps,
@@ -308,12 +340,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak" if mode == "rows" else "strong",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded splitmix64 grid X; random balanced depth-8 forest)",
-            "config": dict(workload_config(cfg, e, n, args), strategy=info["strategy_name"],
-                           output=kind),
+            "config": dict(workload_config(cfg, e, n, args, mode), strategy=info["strategy_name"],
+                           output=kind, trees_per_gpu=t1 - t0),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * launches_per_step,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -129,6 +129,8 @@ typedef struct {
   int32_t x_in_smem;            /* 1 if the scorer stages X row tiles in SMEM  */
   int64_t device_bytes;         /* device memory owned by the model            */
   int64_t tree_stride_bytes;    /* bytes per tree in the compiled layout       */
+  int32_t tensor_cores;         /* 1 if the scorer runs tcgen05 MMAs (GEMM)    */
+  int32_t reserved;
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the

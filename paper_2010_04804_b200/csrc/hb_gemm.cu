@@ -234,6 +234,7 @@ static GemmFn pick_nacc(int nacc) {
 }
 
 hb_status launch_gemm(const Model &m, const RunArgs &a) {
+  if (m.gemm_tc) return launch_gemm_tc(m, a);
   const GemmGeom g = gemm_geom(m.gemm_ni, m.gemm_nl, m.leaf_width);
   GemmParams p;
   p.X = a.X;

@@ -1,0 +1,471 @@
+// hb_gemm_tc.cu — GEMM strategy on the 5th-generation tensor cores (tcgen05).
+//
+// PAPER.md Alg. 1, Table 3, batched over trees:
+//   T <- X.A ; T <- T < B ; S <- T.C ; T <- S == D ; R <- T.E
+// Only the path contraction S = T.C runs on the tensor cores; the node
+// evaluation gathers X[r, feature] and compares in fp32 (reading R3: a dense
+// X.A would be poisoned by Inf/NaN and a tf32/bf16 product would flip
+// compares), and R = T.E is a gather of the single selected leaf.
+//
+// Exactness: T in {0,1} and C in {-1,0,+1} are exact in bf16; |S| <= 8 is exact
+// in the fp32 TMEM accumulator. So S == D is decided on exact integers and the
+// selected leaf is bit-identical to the walk (tests: exhaustive 2^7 patterns).
+//
+// Tiling: one CTA = 4 warps = 128 rows = UMMA M (TMEM lane =
+// row). Trees with |I| <= 8 and |L| <= 8 (D <= 3, the depths AUTO sends here)
+// are taken in PAIRS: one kind::f16 UMMA of shape M128 x N16 x K16 evaluates
+// the block-diagonal [C_a 0; 0 C_b] for two trees at once. A group of 8 pairs
+// (16 trees) occupies a 128 x 128 bf16 A tile (8 K-slabs of 4 KB, canonical
+// K-major core-matrix layout, no swizzle) and 128 TMEM columns. Per group:
+//   1. every thread evaluates its row's 16 x 8 node predicates -> bf16 bits
+//      into the A tile (16-B stores, one core-matrix row each),
+//   2. fence.proxy.async + barrier; one thread issues 8 tcgen05.mma and a
+//      tcgen05.commit to an mbarrier,
+//   3. every warp tcgen05.ld's its 32 lanes x 16 columns per pair, compares
+//      with D, gathers E and accumulates.
+// Group records (the B images, thresholds, features, D, E) are pre-built on
+// the host in their exact SMEM image and double-buffered with cp.async.bulk.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <vector>
+
+#include "hb_device.cuh"
+#include "hb_internal.h"
+
+namespace hb {
+
+constexpr int kTcPairs = 8;                 // pairs of trees per group
+constexpr int kTcTrees = 2 * kTcPairs;      // 16 trees per group
+constexpr int kTcCols = 16 * kTcPairs;      // TMEM columns per group
+constexpr int kTcRows = 128;                // rows per CTA tile (UMMA M)
+constexpr float kTcDPad = 99.f;             // unreachable D for padded leaf columns
+
+// Group record (SMEM image), all offsets 16-B aligned:
+//   bimg  [kTcPairs][512 B]   B operand: per pair 16 (N) x 16 (K) bf16, K-major
+//                             core matrices (8 rows x 16 B), LBO = 128, SBO = 256
+//   feat  [kTcTrees][8] u32   feature id of internal node i (pads: 0)
+//   thr   [kTcTrees][8] f32   threshold (pads: +Inf)
+//   dval  [kTcTrees][8] f32   D_j (pads: 99)
+//   tout  [kTcTrees]    u32   tree_output
+//   e     [kTcTrees][8][w] f32
+struct TcGeom {
+  int w;
+  size_t off_b, off_feat, off_thr, off_d, off_tout, off_e, stride;
+};
+
+static TcGeom tc_geom(int w) {
+  TcGeom g;
+  g.w = w;
+  size_t o = 0;
+  g.off_b = o;    o += 512 * kTcPairs;
+  g.off_feat = o; o += 4 * 8 * kTcTrees;
+  g.off_thr = o;  o += 4 * 8 * kTcTrees;
+  g.off_d = o;    o += 4 * 8 * kTcTrees;
+  g.off_tout = o; o += 4 * kTcTrees;
+  g.off_e = o;    o += 4 * 8 * (size_t)kTcTrees * w;
+  g.stride = (o + 127) & ~size_t(127);
+  return g;
+}
+
+static inline uint16_t bf16_bits(float f) {  // exact for {-1, 0, 1}
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return (uint16_t)(u >> 16);
+}
+
+bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1) {
+  for (int t = t0; t < t1; ++t) {
+    const int64_t a = e->node_offset[t], b = e->node_offset[t + 1];
+    int ni = 0, nl = 0;
+    for (int64_t i = a; i < b; ++i) (e->left[i] == -1 ? nl : ni)++;
+    if (ni > 8 || nl > 8) return false;
+  }
+  return true;
+}
+
+hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
+  const int w = e->leaf_width;
+  const TcGeom g = tc_geom(w);
+  const int T = t1 - t0;
+  const int ngroups = (T + kTcTrees - 1) / kTcTrees;
+  std::vector<uint8_t> buf((size_t)ngroups * g.stride, 0);
+  std::vector<int32_t> leafmap((size_t)ngroups * kTcTrees * 8, -1);
+  std::vector<int> ipos, lpos, stack;
+  for (int gi = 0; gi < ngroups; ++gi) {
+    uint8_t *rec = buf.data() + (size_t)gi * g.stride;
+    uint16_t *bimg = reinterpret_cast<uint16_t *>(rec + g.off_b);
+    uint32_t *feat = reinterpret_cast<uint32_t *>(rec + g.off_feat);
+    float *thr = reinterpret_cast<float *>(rec + g.off_thr);
+    float *dval = reinterpret_cast<float *>(rec + g.off_d);
+    uint32_t *tout = reinterpret_cast<uint32_t *>(rec + g.off_tout);
+    float *E = reinterpret_cast<float *>(rec + g.off_e);
+    for (int q = 0; q < kTcTrees; ++q) {
+      for (int i = 0; i < 8; ++i) {
+        thr[q * 8 + i] = INFINITY;
+        dval[q * 8 + i] = kTcDPad;
+      }
+      const int lt = gi * kTcTrees + q;
+      if (lt >= T) {  // zero tree: column 0 (C = 0, D = 0) always matches, E = 0
+        dval[q * 8] = 0.f;
+        continue;
+      }
+      const int t = t0 + lt;
+      const int64_t a = e->node_offset[t];
+      const int n = (int)(e->node_offset[t + 1] - a);
+      tout[q] = (uint32_t)(w == 1 ? (e->tree_output ? e->tree_output[t] : t % e->n_outputs) : 0);
+      ipos.assign(n, -1);
+      lpos.assign(n, -1);
+      int ci = 0, cl = 0;
+      for (int i = 0; i < n; ++i) {
+        if (e->left[a + i] != -1) ipos[i] = ci++;
+        else lpos[i] = cl++;
+      }
+      for (int i = 0; i < n; ++i) {
+        if (ipos[i] >= 0) {
+          feat[q * 8 + ipos[i]] = (uint32_t)e->feature[a + i];
+          thr[q * 8 + ipos[i]] = e->threshold[a + i];
+        } else {
+          for (int k = 0; k < w; ++k)
+            E[((size_t)q * 8 + lpos[i]) * w + k] = e->leaf_value[(a + i) * w + k];
+          leafmap[(size_t)lt * 8 + lpos[i]] = i;
+        }
+      }
+      // C (Table 3): +1 left subtree, -1 right subtree; D_j = #left edges (R5)
+      int dcount[8] = {0};
+      const int pair = q >> 1, half = q & 1;
+      for (int i = 0; i < n; ++i) {
+        if (ipos[i] < 0) continue;
+        for (int side = 0; side < 2; ++side) {
+          stack.assign(1, side == 0 ? e->left[a + i] : e->right[a + i]);
+          while (!stack.empty()) {
+            const int k = stack.back();
+            stack.pop_back();
+            if (e->left[a + k] == -1) {
+              const int j = lpos[k];
+              // B[nrow][kcol] with nrow = leaf column (half*8 + j), kcol = node (half*8 + i)
+              const int nrow = half * 8 + j, kcol = half * 8 + ipos[i];
+              const int core = (nrow >> 3) * 2 + (kcol >> 3);  // SBO = 256 B = 2 cores, LBO = 128 B
+              bimg[pair * 256 + core * 64 + (nrow & 7) * 8 + (kcol & 7)] =
+                  bf16_bits(side == 0 ? 1.f : -1.f);
+              if (side == 0) dcount[j]++;
+            } else {
+              stack.push_back(e->left[a + k]);
+              stack.push_back(e->right[a + k]);
+            }
+          }
+        }
+      }
+      for (int j = 0; j < cl; ++j) dval[q * 8 + j] = (float)dcount[j];
+    }
+  }
+  m->stride = g.stride;
+  m->nslots = 8;
+  m->n_trees_pad = ngroups * kTcTrees;
+  cudaError_t err = cudaMalloc(&m->d_trees, buf.size());
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(gemm_tc)");
+  m->device_bytes += buf.size();
+  err = cudaMemcpy(m->d_trees, buf.data(), buf.size(), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm_tc)");
+  err = cudaMalloc(&m->d_leafmap, leafmap.size() * 4);
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(gemm_tc leafmap)");
+  m->device_bytes += leafmap.size() * 4;
+  err = cudaMemcpy(m->d_leafmap, leafmap.data(), leafmap.size() * 4, cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm_tc leafmap)");
+  const long xb = 4L * e->n_features * 128;
+  m->cfg = LaunchCfg();
+  m->cfg.nw = 4;
+  m->cfg.x_smem = xb <= 64 * 1024 ? 1 : 0;
+  m->cfg.t_smem = 1;
+  m->cfg.smem_bytes = (int)((m->cfg.x_smem ? xb : 0) + 2 * g.stride + kTcRows * 16 * 2 * kTcPairs + 64);
+  m->cfg.ctas_per_sm = m->cfg.smem_bytes <= 100 * 1024 ? 2 : 1;
+  m->gemm_tc = 1;
+  return HB_OK;
+}
+
+// ------------------------------------------------------------------ device
+namespace tc {
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SM100 shared-memory matrix descriptor: start>>4 [0,14), LBO>>4 [16,30),
+  // SBO>>4 [32,46), version = 1 [46,48), base offset 0, layout SWIZZLE_NONE (0).
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// kind::f16 instruction descriptor: A = B = bf16, D = f32, both K-major,
+// N = 16 (n_dim = N >> 3), M = 128 (m_dim = M >> 4).
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(0)
+      : "memory");
+}
+
+__device__ __forceinline__ void commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   dev::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+}  // namespace tc
+
+struct TcParams {
+  const float *X;
+  int64_t n, ldx;
+  int F, vec4, x_smem;
+  const uint8_t *groups;
+  uint32_t stride, off_feat, off_thr, off_d, off_tout, off_e;
+  int ngroups, n_trees, tree_begin;
+  const int32_t *leafmap;
+  const float *scale, *base;
+  int K, w, task, post, kind;
+  void *out;
+  int ntiles;
+};
+
+template <bool LE, int NACC>
+__global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t xbytes = p.x_smem ? (size_t)4 * p.F * 128 : 0;
+  uint8_t *recbuf = smem + xbytes;                               // 2 x stride
+  uint8_t *atile = recbuf + 2 * (size_t)p.stride;                // kTcPairs x 4 KB
+  uint64_t *bars = reinterpret_cast<uint64_t *>(atile + (size_t)kTcPairs * 4096);
+  uint64_t *rec_full = bars;       // [2] group record landed
+  uint64_t *mma_done = bars + 2;   // MMA group finished
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3);
+
+  if (threadIdx.x == 0) {
+    dev::mbar_init(&rec_full[0], 1);
+    dev::mbar_init(&rec_full[1], 1);
+    dev::mbar_init(mma_done, 1);
+    dev::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     dev::smem_u32(tmem_slot)),
+                 "n"(kTcCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
+  const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
+  const uint32_t a_base = dev::smem_u32(atile);
+  uint32_t it = 0;            // global group counter of this CTA (record ring)
+  uint32_t mma_phase = 0;
+
+  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const uint32_t total = (uint32_t)my_tiles * p.ngroups;
+  if (threadIdx.x == 0 && total > 0) {
+    dev::mbar_arrive_expect_tx(&rec_full[0], p.stride);
+    dev::bulk_g2s(recbuf, p.groups, p.stride, &rec_full[0]);
+  }
+
+  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t row = (int64_t)tile * kTcRows + warp * 32 + lane;
+    const float *xrow;
+    int xstride;
+    if (p.x_smem) {
+      dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+      xrow = xs + lane;
+      xstride = 32;
+    } else {
+      xrow = p.X + (row < p.n ? row : 0) * p.ldx;
+      xstride = 1;
+    }
+    float acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    uint64_t h = 0;
+
+    for (int gi = 0; gi < p.ngroups; ++gi, ++it) {
+      const int buf = it & 1;
+      uint8_t *rec = recbuf + (size_t)buf * p.stride;
+      // prefetch the next group record into the other buffer (its last reader
+      // finished before the previous group's closing barrier)
+      if (threadIdx.x == 0 && it + 1 < total) {
+        const int ng = (gi + 1 == p.ngroups) ? 0 : gi + 1;
+        dev::mbar_arrive_expect_tx(&rec_full[buf ^ 1], p.stride);
+        dev::bulk_g2s(recbuf + (size_t)(buf ^ 1) * p.stride, p.groups + (size_t)ng * p.stride,
+                      p.stride, &rec_full[buf ^ 1]);
+      }
+      dev::mbar_wait(&rec_full[buf], (it >> 1) & 1);
+      const uint32_t *feat = reinterpret_cast<const uint32_t *>(rec + p.off_feat);
+      const float *thr = reinterpret_cast<const float *>(rec + p.off_thr);
+
+      // 1. T <- (X.A < B): 16 trees x 8 nodes -> bf16 {0,1} into the A tile.
+      //    Pair s is K-slab s: row r, k-chunk c (= tree 2s+c) at
+      //    s*4096 + (r>>3)*256 + c*128 + (r&7)*16.
+      const int r = threadIdx.x;
+#pragma unroll 2
+      for (int q = 0; q < kTcTrees; ++q) {
+        uint32_t bits[4];
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int i = i2 * 2 + hh;
+            const float x = xrow[feat[q * 8 + i] * xstride];
+            const float t = thr[q * 8 + i];
+            const bool pr = LE ? (x <= t) : (x < t);
+            v |= (pr ? 0x3F80u : 0u) << (16 * hh);
+          }
+          bits[i2] = v;
+        }
+        uint8_t *dst = atile + (size_t)(q >> 1) * 4096 + (r >> 3) * 256 + (q & 1) * 128 + (r & 7) * 16;
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(bits[0], bits[1], bits[2], bits[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+
+      // 2. S <- T.C on the tensor cores: one M128 x N16 x K16 UMMA per pair.
+      if (threadIdx.x == 0) {
+        const uint32_t b_base = dev::smem_u32(rec);
+#pragma unroll
+        for (int s = 0; s < kTcPairs; ++s) {
+          const uint64_t ad = tc::smem_desc(a_base + s * 4096, 128, 256);
+          const uint64_t bd = tc::smem_desc(b_base + s * 512, 128, 256);
+          tc::mma_bf16(tmem + s * 16, ad, bd);
+        }
+        tc::commit(mma_done);
+      }
+      dev::mbar_wait(mma_done, mma_phase);
+      mma_phase ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+
+      // 3. T <- S == D ; R <- T.E  (epilogue per pair: 16 TMEM columns)
+      const float *dval = reinterpret_cast<const float *>(rec + p.off_d);
+      const uint32_t *tout = reinterpret_cast<const uint32_t *>(rec + p.off_tout);
+      const float *E = reinterpret_cast<const float *>(rec + p.off_e);
+#pragma unroll 1
+      for (int s = 0; s < kTcPairs; ++s) {
+        float S[16];
+        tc::ld16(tmem + ((uint32_t)(warp * 32) << 16) + s * 16, S);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int q = 2 * s + hh;
+          int sel = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (S[hh * 8 + j] == dval[q * 8 + j]) sel = j;
+          if (p.w == 1) {
+            const float v = E[q * 8 + sel];
+            const uint32_t k0 = tout[q];
+#pragma unroll
+            for (int k = 0; k < NACC; ++k)
+              if (k0 == (uint32_t)k) acc[k] += v;
+          } else {
+#pragma unroll
+            for (int k = 0; k < NACC; ++k)
+              if (k < p.K) acc[k] += E[(q * 8 + sel) * p.w + k];
+          }
+          if (lm) {
+            const int t = gi * kTcTrees + q;
+            if (t < p.n_trees) {
+              const int32_t id = __ldg(p.leafmap + (size_t)t * 8 + sel);
+              if (lm == 1) {
+                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+              } else {
+                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+              }
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();   // A tile, TMEM and this record buffer are free again
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    if (row < p.n) {
+      if (lm == 2) static_cast<uint64_t *>(p.out)[row] = h;
+      else if (lm == 0) dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcCols));
+}
+
+using TcFn = void (*)(const TcParams);
+
+template <bool LE>
+static TcFn pick_nacc(int nacc) {
+  switch (nacc) {
+    case 1: return gemm_tc_kernel<LE, 1>;
+    case 4: return gemm_tc_kernel<LE, 4>;
+    case 8: return gemm_tc_kernel<LE, 8>;
+    default: return gemm_tc_kernel<LE, 16>;
+  }
+}
+
+int sm_count(int device);
+
+hb_status launch_gemm_tc(const Model &m, const RunArgs &a) {
+  const TcGeom g = tc_geom(m.leaf_width);
+  TcParams p;
+  p.X = a.X;
+  p.n = a.n;
+  p.ldx = a.ldx;
+  p.F = m.n_features;
+  p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
+  p.x_smem = m.cfg.x_smem;
+  p.groups = static_cast<const uint8_t *>(m.d_trees);
+  p.stride = (uint32_t)g.stride;
+  p.off_feat = (uint32_t)g.off_feat;
+  p.off_thr = (uint32_t)g.off_thr;
+  p.off_d = (uint32_t)g.off_d;
+  p.off_tout = (uint32_t)g.off_tout;
+  p.off_e = (uint32_t)g.off_e;
+  p.ngroups = m.n_trees_pad / kTcTrees;
+  p.n_trees = m.n_trees;
+  p.tree_begin = m.tree_begin;
+  p.leafmap = m.d_leafmap;
+  p.scale = m.d_scale;
+  p.base = m.d_base;
+  p.K = m.n_outputs;
+  p.w = m.leaf_width;
+  p.task = m.task;
+  p.post = m.post;
+  p.kind = a.kind;
+  p.out = a.out;
+  const int64_t ntiles = (a.n + kTcRows - 1) / kTcRows;
+  if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows");
+  p.ntiles = (int)ntiles;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
+  TcFn fn = m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       m.cfg.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(gemm_tc)");
+  fn<<<grid, 128, m.cfg.smem_bytes, a.stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "gemm_tc_kernel launch");
+  return HB_OK;
+}
+
+}  // namespace hb

@@ -407,7 +407,10 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   int strat = strategy == HB_STRATEGY_AUTO ? select_strategy(D) : strategy;
   HostLayout L;
   if (strat == HB_STRATEGY_GEMM) {
-    st = compile_gemm(e, t0, t1, m.get());
+    // tensor-core kernel for |I| <= 8, |L| <= 8 (D <= 3); CUDA-core exact
+    // contraction for deeper forced-GEMM trees
+    st = gemm_tc_eligible(e, t0, t1) && env_int("HB_GEMM_TC", 1) ? compile_gemm_tc(e, t0, t1, m.get())
+                                                                 : compile_gemm(e, t0, t1, m.get());
     if (st != HB_OK) return st;
   } else {
     if (strat == HB_STRATEGY_PTT) {
@@ -687,6 +690,8 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->x_in_smem = m.cfg.x_smem;
   info->device_bytes = (int64_t)m.device_bytes;
   info->tree_stride_bytes = (int64_t)m.stride;
+  info->tensor_cores = m.gemm_tc;
+  info->reserved = 0;
   return HB_OK;
 }
 

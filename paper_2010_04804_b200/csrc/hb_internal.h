@@ -54,6 +54,7 @@ struct Model {
   void *d_gemm = nullptr;
   size_t gemm_bytes = 0;
   int gemm_ni = 0, gemm_nl = 0;
+  int gemm_tc = 0;          // 1: tensor-core (tcgen05) GEMM kernel
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
@@ -76,6 +77,9 @@ struct RunArgs {
 
 bool gemm_supported(int depth);
 hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);
+bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1);
+hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m);
+hb_status launch_gemm_tc(const Model &m, const RunArgs &a);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);
 hb_status launch_tt(const Model &m, const RunArgs &a);

@@ -45,7 +45,8 @@ class _Info(C.Structure):
                 ("n_trees", C.c_int32), ("n_trees_total", C.c_int32),
                 ("n_features", C.c_int32), ("n_outputs", C.c_int32),
                 ("leaf_width", C.c_int32), ("device", C.c_int32), ("x_in_smem", C.c_int32),
-                ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64),
+                ("tensor_cores", C.c_int32), ("reserved", C.c_int32)]
 
 
 def _load():

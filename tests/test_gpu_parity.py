@@ -207,6 +207,52 @@ def test_single_feature_and_single_leaf_trees(strat):
     check_all(e0, m0, Xd, Xh)
 
 
+def _perfect_d3_sign_tree(cmp):
+    """Perfect depth-3 tree whose 7 internal nodes test features 0..6 at 0."""
+    feat, thr, L, R, val = [], [], [], [], []
+    # heap order: node i (0-based) children 2i+1, 2i+2; 7 internal, 8 leaves
+    for i in range(15):
+        if i < 7:
+            feat.append(i); thr.append(0.0); L.append(2 * i + 1); R.append(2 * i + 2)
+            val.append(np.nan)
+        else:
+            feat.append(-1); thr.append(np.nan); L.append(-1); R.append(-1)
+            val.append(float(i))
+    return synth.from_trees([dict(feature=feat, threshold=thr, left=L, right=R, leaf_value=val)],
+                            7, cmp=cmp)
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_gemm_path_contraction_exhaustive(tc, cmp, monkeypatch):
+    """P-i: every one of the 2^7 predicate patterns T of a perfect D3 tree
+    (rows with x_i in {-1, 0, +1} hit both sides of every threshold, and 0 is
+    the tie) selects exactly the walked leaf through S = T.C == D, on the
+    tensor-core kernel (HB_GEMM_TC=1) and the CUDA-core kernel."""
+    monkeypatch.setenv("HB_GEMM_TC", tc)
+    e = _perfect_d3_sign_tree(cmp)
+    m = hb.Model(e, strategy="gemm", device=0)
+    assert m.info["tensor_cores"] == int(tc)
+    import itertools
+    X = np.array(list(itertools.product([-1.0, 0.0, 1.0], repeat=7)), np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), oracle.leaf(e, X))
+    assert np.array_equal(m.predict_raw(Xd).cpu().numpy()[:, 0],
+                          oracle.raw(e, X)[:, 0].astype(np.float32))
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_gemm_tc_vs_cuda_core_many_trees(tc, monkeypatch):
+    """Many shallow trees (several 16-tree groups, ragged last group) on both
+    GEMM kernels, all outputs against the oracle."""
+    monkeypatch.setenv("HB_GEMM_TC", tc)
+    e = _forest("multiclass", 61, 3, 13, 21, "mixed", 1)
+    m = hb.Model(e, strategy="gemm", device=0)
+    assert m.info["tensor_cores"] == int(tc)
+    Xd, Xh = X_pair(22, 3001, 13, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+
+
 def test_auto_strategy_selection():
     """Sec. 5.1 heuristic (reading R24): GEMM D <= 3, PTT D <= 10, TT beyond;
     PTT falls back to TT when rows are too wide for the SMEM X tile."""
