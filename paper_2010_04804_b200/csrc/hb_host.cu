@@ -278,20 +278,30 @@ static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLa
   return HB_OK;
 }
 
+static int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
 // Launch configuration: as many 32-row warps as SMEM allows
 // for the feature-major X slices (NW * F * 128 B), the rest for a 2-4 stage
 // ring of tree chunks.
 static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool allow_t_global,
-                       LaunchCfg *c) {
+                       int max_nw, LaunchCfg *c) {
   const long budget = kSmemBudget;
-  for (int nw : {16, 12, 8, 4}) {
+  const int force_nw = env_int("HB_NW", 0);      // tuning override (bench sweeps)
+  for (int nw : {24, 16, 12, 8, 4}) {
+    if (force_nw && nw != force_nw) continue;
+    if (nw > max_nw) continue;
     const long xb = (long)nw * F * 128;
-    if (xb + 4 * (long)stride > budget) continue;
+    if (xb + 2L * kTreeGroup * (long)stride > budget) continue;
     const long rem = budget - xb;
     int ns = (rem >= 3 * 8 * (long)stride) ? 3 : 2;
-    int ch = (int)std::min<long>(32, rem / (ns * (long)stride)) & ~1;
+    if (env_int("HB_NS", 0)) ns = env_int("HB_NS", 0);
+    int ch = (int)std::min<long>(env_int("HB_CH", 32), rem / (ns * (long)stride)) & ~(kTreeGroup - 1);
     ch = std::min(ch, Tpad);
-    if (ch < 2) continue;
+    if (ch < kTreeGroup) continue;
     c->nw = nw;
     c->ns = ns;
     c->ch = ch;
@@ -303,9 +313,9 @@ static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool
   // X does not fit: read rows from global memory, keep the tree ring.
   if (allow_x_global) {
     const long rem = budget;
-    if (4 * (long)stride <= rem) {
+    if (2L * kTreeGroup * (long)stride <= rem) {
       int ns = (rem >= 3 * 8 * (long)stride) ? 3 : 2;
-      int ch = std::min<int>((int)std::min<long>(32, rem / (ns * (long)stride)) & ~1, Tpad);
+      int ch = std::min<int>((int)std::min<long>(32, rem / (ns * (long)stride)) & ~(kTreeGroup - 1), Tpad);
       c->nw = 16;
       c->ns = ns;
       c->ch = ch;
@@ -318,7 +328,7 @@ static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool
       const long xb = 16L * F * 128;
       c->nw = 16;
       c->ns = 1;
-      c->ch = std::min(Tpad, 32) & ~1;
+      c->ch = std::min(Tpad, 32) & ~(kTreeGroup - 1);
       c->x_smem = xb <= budget ? 1 : 0;
       c->t_smem = 0;
       c->smem_bytes = c->x_smem ? (int)xb : 0;
@@ -328,11 +338,6 @@ static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool
   return false;
 }
 
-static int env_int(const char *name, int dflt) {
-  const char *v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  return std::atoi(v);
-}
 
 // Sec. 5.1: GEMM for shallow trees, PTT up to D = 10, TT beyond
 // (reading R24 for the GPU thresholds).
@@ -417,7 +422,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
       bool ok = D <= kPttMaxDepth;
       if (ok) {
         build_ptt(e, t0, t1, D, m->n_trees_pad, &L);
-        ok = choose_cfg(e->n_features, L.stride, m->n_trees_pad, false, false, &m->cfg);
+        ok = choose_cfg(e->n_features, L.stride, m->n_trees_pad, false, false, 24, &m->cfg);
       }
       if (!ok) {
         if (strategy == HB_STRATEGY_PTT)
@@ -432,7 +437,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     if (strat == HB_STRATEGY_TT) {
       st = build_tt(e, t0, t1, m->n_trees_pad, &L);
       if (st != HB_OK) return st;
-      if (!choose_cfg(e->n_features, L.stride, m->n_trees_pad, true, true, &m->cfg))
+      if (!choose_cfg(e->n_features, L.stride, m->n_trees_pad, true, true, 16, &m->cfg))
         return fail(HB_E_UNSUPPORTED, "TT: no launch configuration fits");
     }
     m->stride = L.stride;

@@ -14,7 +14,7 @@ namespace hb {
 
 constexpr int kMaxOutputs = 16;       // NACC upper bound of the fused epilogue
 constexpr int kPttMaxDepth = 10;      // P:308 "PTT when D <= 10"; template range 0..10
-constexpr int kTreeGroup = 2;         // trees walked concurrently per lane (ILP)
+constexpr int kTreeGroup = 4;         // trees walked concurrently per lane (ILP)
 constexpr int kSmemBudget = 227 * 1024 - 2048;
 
 // Kernel launch configuration chosen at compile time from F and the per-tree

@@ -39,8 +39,8 @@ struct PttParams {
   int nw, ns, ch, ntiles;
 };
 
-template <int D, bool LE, int NACC>
-__global__ void __launch_bounds__(32 * 17, 1) ptt_kernel(const PttParams p) {
+template <int D, bool LE, int NACC, int G>
+__global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = p.nw, ns = p.ns, ch = p.ch;
@@ -83,12 +83,16 @@ __global__ void __launch_bounds__(32 * 17, 1) ptt_kernel(const PttParams p) {
 
   // ---------------- consumer warps
   float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
-  const float *xl = xs + lane;
+  const uint32_t xlane = dev::smem_u32(xs) + 4u * lane;   // X[row, f] at xlane + 128 f
+  const uint32_t stage0 = dev::smem_u32(stages);
+  const uint32_t leaf_off = 4u << D;                      // leaf(i) at tree + leaf_off + 4 i ... (w = 1)
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   long it = 0;
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t row = (int64_t)tile * (nw * 32) + warp * 32 + lane;
-    dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+    const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
+    const int64_t row = wrow0 + lane;
+    const bool active = wrow0 < p.n;        // whole warp beyond n: only keep the ring in step
+    if (active) dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
     float acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
@@ -97,60 +101,61 @@ __global__ void __launch_bounds__(32 * 17, 1) ptt_kernel(const PttParams p) {
     for (int c = 0; c < nchunks; ++c, ++it) {
       const int s = (int)(it % ns);
       dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
-      const uint8_t *cb = stages + (size_t)s * ch * p.stride;
-      const int nt = min(ch, p.n_trees_pad - c * ch);
-      for (int j = 0; j < nt; j += 2) {
-        const uint2 *na = reinterpret_cast<const uint2 *>(cb + (size_t)j * p.stride);
-        const uint2 *nb = reinterpret_cast<const uint2 *>(cb + (size_t)(j + 1) * p.stride);
-        uint32_t ia = 1, ib = 1;
+      if (active) {
+        const uint32_t cb = stage0 + (uint32_t)(s * ch) * p.stride;
+        const int nt = min(ch, p.n_trees_pad - c * ch);
+        for (int j = 0; j < nt; j += G) {
+          uint32_t tb[G], off[G];
 #pragma unroll
-        for (int l = 0; l < D; ++l) {
-          const uint2 da = na[ia];
-          const uint2 db = nb[ib];
-          const float xa = xl[da.x * 32];
-          const float xb = xl[db.x * 32];
-          const float ta = __uint_as_float(da.y);
-          const float tb = __uint_as_float(db.y);
-          const bool pa = LE ? (xa <= ta) : (xa < ta);
-          const bool pb = LE ? (xb <= tb) : (xb < tb);
-          ia = 2u * ia + (pa ? 0u : 1u);
-          ib = 2u * ib + (pb ? 0u : 1u);
-        }
-        const uint32_t sa = ia - (1u << D), sb = ib - (1u << D);
-        const float *la = reinterpret_cast<const float *>(na + (1 << D));
-        const float *lb = reinterpret_cast<const float *>(nb + (1 << D));
-        if (p.w == 1) {
-          const float va = la[sa], vb = lb[sb];
-          if (NACC == 1) {
-            acc[0] += va;
-            acc[0] += vb;
-          } else {
-            const uint32_t ka = na[0].x, kb = nb[0].x;
+          for (int g = 0; g < G; ++g) {
+            tb[g] = cb + (uint32_t)(j + g) * p.stride;
+            off[g] = 8u;                    // heap node 1 (the root), 8-B records
+          }
+          // Alg. 3: T_I <- 2 T_I + (X[r, N'_F[T_I]] < N'_T[T_I] ? 0 : 1), D times
 #pragma unroll
-            for (int k = 0; k < NACC; ++k) {
-              if (ka == (uint32_t)k) acc[k] += va;
-              if (kb == (uint32_t)k) acc[k] += vb;
+          for (int l = 0; l < D; ++l) {
+            uint2 nd[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) nd[g] = dev::lds_v2(tb[g] + off[g]);
+            float x[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) x[g] = dev::lds_f32(xlane + (nd[g].x << 7));
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const float t = __uint_as_float(nd[g].y);
+              const bool pr = LE ? (x[g] <= t) : (x[g] < t);
+              off[g] = 2u * off[g] + (pr ? 0u : 8u);
             }
           }
-        } else {
+          // R <- N'_C[T_I - 2^D]
 #pragma unroll
-          for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += la[sa * p.w + k];
-#pragma unroll
-          for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += lb[sb * p.w + k];
-        }
-        if (lm) {
-          const int tg = c * ch + j;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int t = tg + q;
-            if (t < p.n_trees) {
-              const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + (q ? sb : sa));
-              if (lm == 1) {
-                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+          for (int g = 0; g < G; ++g) {
+            const uint32_t slot = (off[g] >> 3) - (1u << D);
+            if (p.w == 1) {
+              const float v = dev::lds_f32(tb[g] + leaf_off + (off[g] >> 1));
+              if (NACC == 1) {
+                acc[0] += v;
               } else {
-                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+                const uint32_t k0 = dev::lds_u32(tb[g]);
+#pragma unroll
+                for (int k = 0; k < NACC; ++k)
+                  if (k0 == (uint32_t)k) acc[k] += v;
+              }
+            } else {
+              const uint32_t lb = tb[g] + (8u << D) + 4u * slot * (uint32_t)p.w;
+#pragma unroll
+              for (int k = 0; k < NACC; ++k)
+                if (k < p.K) acc[k] += dev::lds_f32(lb + 4u * k);
+            }
+            if (lm) {
+              const int t = c * ch + j + g;
+              if (t < p.n_trees) {
+                const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + slot);
+                if (lm == 1) {
+                  if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+                } else {
+                  h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+                }
               }
             }
           }
@@ -174,10 +179,10 @@ using PttFn = void (*)(const PttParams);
 template <int D, bool LE>
 static PttFn pick_nacc(int nacc) {
   switch (nacc) {
-    case 1: return ptt_kernel<D, LE, 1>;
-    case 4: return ptt_kernel<D, LE, 4>;
-    case 8: return ptt_kernel<D, LE, 8>;
-    default: return ptt_kernel<D, LE, 16>;
+    case 1: return ptt_kernel<D, LE, 1, kTreeGroup>;
+    case 4: return ptt_kernel<D, LE, 4, kTreeGroup>;
+    case 8: return ptt_kernel<D, LE, 8, kTreeGroup>;
+    default: return ptt_kernel<D, LE, 16, kTreeGroup>;
   }
 }
 
