@@ -437,8 +437,31 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     if (strat == HB_STRATEGY_TT) {
       st = build_tt(e, t0, t1, m->n_trees_pad, &L);
       if (st != HB_OK) return st;
-      if (!choose_cfg(e->n_features, L.stride, m->n_trees_pad, true, true, 16, &m->cfg))
-        return fail(HB_E_UNSUPPORTED, "TT: no launch configuration fits");
+      // rows that fit a 32-row-per-warp SMEM slice with room for a tree ring
+      // use tt_kernel; wider rows or trees too big for SMEM use tt_wide_kernel
+      const bool narrow = choose_cfg(e->n_features, L.stride, m->n_trees_pad, false, false, 16, &m->cfg);
+      const int force_wide = env_int("HB_TT_WIDE", -1);
+      if (!narrow || force_wide == 1) {
+        if (force_wide == 0) return fail(HB_E_UNSUPPORTED, "TT: no narrow configuration fits");
+        LaunchCfg c;
+        const int K = e->n_outputs;
+        const int nacc = K == 1 ? 1 : (K <= 4 ? 4 : (K <= 8 ? 8 : 16));
+        c.nw = 32;
+        c.wide_rows = 0;
+        for (int R : {32, 16, 8}) {
+          const long bytes = (long)e->n_features * R * 4 + (long)c.nw * R * (4L * nacc + 8);
+          if (bytes <= kSmemBudget) {
+            c.wide_rows = R;
+            c.smem_bytes = (int)bytes;
+            break;
+          }
+        }
+        if (!c.wide_rows) return fail(HB_E_UNSUPPORTED, "TT: rows too wide for an 8-row SMEM tile");
+        c.x_smem = 1;
+        c.t_smem = 0;
+        c.ch = kTreeGroup;
+        m->cfg = c;
+      }
     }
     m->stride = L.stride;
     m->nslots = L.nslots;

@@ -27,6 +27,7 @@ struct LaunchCfg {
   int t_smem = 1;       // tree chunks staged in SMEM via cp.async.bulk
   int smem_bytes = 0;   // dynamic SMEM per CTA
   int ctas_per_sm = 1;
+  int wide_rows = 0;    // TT only: >0 selects tt_wide_kernel with this many rows per CTA
 };
 
 struct Model {

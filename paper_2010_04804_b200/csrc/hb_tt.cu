@@ -182,6 +182,134 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
   }
 }
 
+// Wide-row TreeTraversal (Epsilon-shaped X, F up to thousands; deep trees
+// whose records do not fit SMEM). A CTA owns R rows whose X tile lives in SMEM
+// feature-major (xs[f*R + r]); lane = (tree slot, row) with 32/R tree slots per
+// warp, and all warps of the CTA walk disjoint trees of the same R rows. Node
+// records come through L1/L2 (__ldg): the top levels of a tree are shared by
+// the R rows and hit L1. Each lane walks two trees at once (memory-level
+// parallelism) and the walk stops early once every lane of the warp sits on a
+// leaf (the self-loop makes further iterations no-ops). Per-row sums
+// are combined with warp shuffles and one SMEM pass in a fixed order.
+template <bool LE, int NACC, int R>
+__global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int L = 32 / R;                       // tree slots per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const int sub = lane / R, r = lane % R;
+  float *xs = reinterpret_cast<float *>(smem);                       // [F][R]
+  float *red = xs + (size_t)p.F * R;                                 // [nwarps][R][NACC]
+  uint64_t *hred = reinterpret_cast<uint64_t *>(red + (size_t)nwarps * R * NACC);  // [nwarps][R]
+  const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
+  const int slots = nwarps * L;
+  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t row0 = (int64_t)tile * R;
+    // cooperative, coalesced X tile load (row-major global -> feature-major SMEM)
+    for (int idx = threadIdx.x; idx < R * p.F; idx += blockDim.x) {
+      const int rr = idx / p.F, f = idx - rr * p.F;
+      const int64_t gr = row0 + rr;
+      xs[f * R + rr] = gr < p.n ? __ldg(p.X + gr * p.ldx + f) : 0.f;
+    }
+    __syncthreads();
+    const int64_t row = row0 + r;
+    const float *xr = xs + r;
+    float acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    uint64_t h = 0;
+    for (int t0 = warp * L + sub; t0 < p.n_trees_pad; t0 += 2 * slots) {
+      const int t1 = t0 + slots;
+      const bool two = t1 < p.n_trees_pad;
+      const uint8_t *ra = p.trees + (size_t)t0 * p.stride;
+      const uint8_t *rb = p.trees + (size_t)(two ? t1 : t0) * p.stride;
+      const uint2 *na = reinterpret_cast<const uint2 *>(ra + 16);
+      const uint2 *nb = reinterpret_cast<const uint2 *>(rb + 16);
+      uint32_t ia = 0, ib = 0;
+      for (int l = 0; l < p.depth; ++l) {
+        const uint2 da = __ldg(na + ia);
+        const uint2 db = __ldg(nb + ib);
+        const float xa = xr[(da.x & 0xFFFFu) * R];
+        const float xb = xr[(db.x & 0xFFFFu) * R];
+        const float ta = __uint_as_float(da.y), tb = __uint_as_float(db.y);
+        const bool pa = LE ? (xa <= ta) : (xa < ta);
+        const bool pb = LE ? (xb <= tb) : (xb < tb);
+        const uint32_t na_i = (da.x >> 16) - (pa ? 1u : 0u);
+        const uint32_t nb_i = (db.x >> 16) - (pb ? 1u : 0u);
+        const bool done = (na_i == ia) && (nb_i == ib);   // both on a self-looping leaf
+        ia = na_i;
+        ib = nb_i;
+        if (__all_sync(0xFFFFFFFFu, done)) break;
+      }
+      const float *la = reinterpret_cast<const float *>(na + p.nslots);
+      const float *lb = reinterpret_cast<const float *>(nb + p.nslots);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q == 1 && !two) break;
+        const uint8_t *rec = q ? rb : ra;
+        const float *lv = q ? lb : la;
+        const uint32_t leaf = q ? ib : ia;
+        if (p.w == 1) {
+          const float v = __ldg(lv + leaf);
+          if (NACC == 1) {
+            acc[0] += v;
+          } else {
+            const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rec));
+#pragma unroll
+            for (int k = 0; k < NACC; ++k)
+              if (k0 == (uint32_t)k) acc[k] += v;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k < p.K) acc[k] += __ldg(lv + leaf * p.w + k);
+        }
+        if (lm) {
+          const int t = q ? t1 : t0;
+          if (t < p.n_trees) {
+            const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
+            if (lm == 1) {
+              if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+            } else {
+              h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+            }
+          }
+        }
+      }
+    }
+    // combine the L tree slots of a row inside the warp, then across warps
+#pragma unroll
+    for (int o = R; o < 32; o <<= 1) {
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) acc[k] += __shfl_xor_sync(0xFFFFFFFFu, acc[k], o);
+      h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+    }
+    if (sub == 0) {
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) red[(warp * R + r) * NACC + k] = acc[k];
+      hred[warp * R + r] = h;
+    }
+    __syncthreads();
+    if (warp == 0 && lane < R) {
+      float tot[NACC];
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) tot[k] = 0.f;
+      uint64_t ht = 0;
+      for (int w2 = 0; w2 < nwarps; ++w2) {
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) tot[k] += red[(w2 * R + lane) * NACC + k];
+        ht += hred[w2 * R + lane];
+      }
+      const int64_t orow = row0 + lane;
+      if (orow < p.n) {
+        if (lm == 2) static_cast<uint64_t *>(p.out)[orow] = ht;
+        else if (lm == 0) dev::write_row<NACC>(p.kind, tot, p.K, p.task, p.post, p.scale, p.base, orow, p.out);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 using TtFn = void (*)(const TtParams);
 
 template <bool LE>
@@ -196,8 +324,30 @@ static TtFn pick_nacc(int nacc) {
 
 int sm_count(int device);
 
+template <bool LE, int R>
+static TtFn pick_wide_nacc(int nacc) {
+  switch (nacc) {
+    case 1: return tt_wide_kernel<LE, 1, R>;
+    case 4: return tt_wide_kernel<LE, 4, R>;
+    case 8: return tt_wide_kernel<LE, 8, R>;
+    default: return tt_wide_kernel<LE, 16, R>;
+  }
+}
+
+template <bool LE>
+static TtFn pick_wide(int R, int nacc) {
+  switch (R) {
+    case 32: return pick_wide_nacc<LE, 32>(nacc);
+    case 16: return pick_wide_nacc<LE, 16>(nacc);
+    default: return pick_wide_nacc<LE, 8>(nacc);
+  }
+}
+
 hb_status launch_tt(const Model &m, const RunArgs &a) {
-  TtFn fn = m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc);
+  const bool wide = m.cfg.wide_rows > 0;
+  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc)
+                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc))
+                 : (m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc));
   TtParams p;
   p.X = a.X;
   p.n = a.n;
@@ -225,7 +375,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.ch = m.cfg.ch;
   p.x_smem = m.cfg.x_smem;
   p.t_smem = m.cfg.t_smem;
-  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
+  const int64_t rows_per_tile = wide ? (int64_t)m.cfg.wide_rows : (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
   p.ntiles = (int)ntiles;
@@ -233,7 +383,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        m.cfg.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tt)");
-  fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
+  const int threads = wide ? 32 * m.cfg.nw : 32 * (m.cfg.nw + 1);
+  fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "tt_kernel launch");
   return HB_OK;

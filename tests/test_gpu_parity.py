@@ -131,6 +131,28 @@ def test_strategy_parity(strat, D, kind, cmp):
     check_all(e, m, Xd, Xh)
 
 
+@pytest.mark.parametrize("kind", ["reg", "binary", "multiclass", "rf", "k7", "k12"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_tt_wide_kernel_parity(kind, cmp, monkeypatch):
+    """The wide-row TT kernel (R rows per CTA, lanes = tree slot x row, nodes
+    through L1/L2, early exit) forced on ordinary inputs, plus its natural use
+    on F = 2000 rows."""
+    monkeypatch.setenv("HB_TT_WIDE", "1")
+    seed = zlib.crc32(f"wide{kind}{cmp}".encode()) & 0xFFFF
+    e = _forest(kind, 45, 9, 37, seed, FAMILIES[seed % 3], cmp)
+    m = hb.Model(e, strategy="tt", device=0)
+    Xd, Xh = X_pair(seed, 1000 + seed % 53, 37, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+
+
+def test_tt_wide_rows_natural():
+    e = _forest("binary", 30, 12, 2000, 3, "mixed", 0)
+    m = hb.Model(e, device=0)
+    assert m.info["strategy_name"] == "tt" and m.info["x_in_smem"] == 1
+    Xd, Xh = X_pair(5, 333, 2000, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+
+
 @pytest.mark.parametrize("kind", ["k7", "k12", "rf_reg"])
 @pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
 def test_more_outputs(kind, strat):
