@@ -130,7 +130,7 @@ typedef struct {
   int64_t device_bytes;         /* device memory owned by the model            */
   int64_t tree_stride_bytes;    /* bytes per tree in the compiled layout       */
   int32_t tensor_cores;         /* 1 if the scorer runs tcgen05 MMAs (GEMM)    */
-  int32_t reserved;
+  int32_t node_record_bytes;    /* PTT/TT node record size (4 = rank-coded PTT) */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the

@@ -357,6 +357,7 @@ static void free_model(Model *m) {
   cudaFree(m->d_scale);
   cudaFree(m->d_base);
   cudaFree(m->d_gemm);
+  cudaFree(m->d_aux);
   delete m;
 }
 
@@ -418,7 +419,13 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
                                                                  : compile_gemm(e, t0, t1, m.get());
     if (st != HB_OK) return st;
   } else {
-    if (strat == HB_STRATEGY_PTT) {
+    bool done = false;
+    if (strat == HB_STRATEGY_PTT && D <= kPttMaxDepth) {
+      st = compile_ptt_rank(e, t0, t1, D, m.get());   // 4-B rank-coded nodes when eligible
+      if (st == HB_OK) done = true;
+      else if (st != HB_E_UNSUPPORTED) return st;
+    }
+    if (!done && strat == HB_STRATEGY_PTT) {
       bool ok = D <= kPttMaxDepth;
       if (ok) {
         build_ptt(e, t0, t1, D, m->n_trees_pad, &L);
@@ -434,7 +441,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         L = HostLayout();
       }
     }
-    if (strat == HB_STRATEGY_TT) {
+    if (!done && strat == HB_STRATEGY_TT) {
       st = build_tt(e, t0, t1, m->n_trees_pad, &L);
       if (st != HB_OK) return st;
       // rows that fit a 32-row-per-warp SMEM slice with room for a tree ring
@@ -463,12 +470,14 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         m->cfg = c;
       }
     }
-    m->stride = L.stride;
-    m->nslots = L.nslots;
-    st = upload(L.trees, reinterpret_cast<uint8_t **>(&m->d_trees), &m->device_bytes);
-    if (st != HB_OK) return st;
-    st = upload(L.leafmap, &m->d_leafmap, &m->device_bytes);
-    if (st != HB_OK) return st;
+    if (!done) {
+      m->stride = L.stride;
+      m->nslots = L.nslots;
+      st = upload(L.trees, reinterpret_cast<uint8_t **>(&m->d_trees), &m->device_bytes);
+      if (st != HB_OK) return st;
+      st = upload(L.leafmap, &m->d_leafmap, &m->device_bytes);
+      if (st != HB_OK) return st;
+    }
   }
   m->strategy = strat;
 
@@ -531,7 +540,7 @@ static hb_status check_kind(const Model &m, int kind) {
 
 static hb_status run(const Model &m, const RunArgs &a) {
   switch (m.strategy) {
-    case HB_STRATEGY_PTT: return launch_ptt(m, a);
+    case HB_STRATEGY_PTT: return m.ptt_rank ? launch_ptt_rank(m, a) : launch_ptt(m, a);
     case HB_STRATEGY_TT: return launch_tt(m, a);
     case HB_STRATEGY_GEMM: return launch_gemm(m, a);
   }
@@ -719,7 +728,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->device_bytes = (int64_t)m.device_bytes;
   info->tree_stride_bytes = (int64_t)m.stride;
   info->tensor_cores = m.gemm_tc;
-  info->reserved = 0;
+  info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : (m.ptt_rank ? 4 : 8);
   return HB_OK;
 }
 

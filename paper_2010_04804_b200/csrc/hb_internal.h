@@ -28,6 +28,7 @@ struct LaunchCfg {
   int smem_bytes = 0;   // dynamic SMEM per CTA
   int ctas_per_sm = 1;
   int wide_rows = 0;    // TT only: >0 selects tt_wide_kernel with this many rows per CTA
+  int stage_bytes = 0;  // PTT rank layout: bytes per ring stage
 };
 
 struct Model {
@@ -56,6 +57,11 @@ struct Model {
   size_t gemm_bytes = 0;
   int gemm_ni = 0, gemm_nl = 0;
   int gemm_tc = 0;          // 1: tensor-core (tcgen05) GEMM kernel
+  // PTT with rank-coded thresholds (hb_pttr.cu)
+  int ptt_rank = 0;
+  void *d_aux = nullptr;    // [fmeta | groups | eytzinger pool]
+  size_t aux_groups_off = 0, aux_pool_off = 0;
+  int rank_nfc = 0, rank_ngroups = 0;
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
@@ -81,6 +87,8 @@ hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);
 bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1);
 hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m);
 hb_status launch_gemm_tc(const Model &m, const RunArgs &a);
+hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m);
+hb_status launch_ptt_rank(const Model &m, const RunArgs &a);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);
 hb_status launch_tt(const Model &m, const RunArgs &a);

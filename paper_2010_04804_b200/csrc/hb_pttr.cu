@@ -1,0 +1,542 @@
+// hb_pttr.cu — PerfectTreeTraversal with rank-coded thresholds (sm_100a).
+//
+// Same algorithm as hb_ptt.cu (Alg. 3), same results bit
+// for bit, with 4-byte instead of 8-byte node records:
+//
+//  * Compile time: for every feature f used by the model, the distinct
+//    thresholds u_0 < ... < u_{m-1} (fp32 order) are collected. A node that
+//    tests (f, u_k) stores k and the compact feature index.
+//  * Per row tile, each X value is replaced by its rank code
+//        LT: c(x) = #{j : u_j <= x}      LE: c(x) = #{j : u_j <  x}
+//    and NaN by 0xFFFF. Then  x < u_k  <=>  c(x) <= k  (LE:  x <= u_k <=> c(x) <= k)
+//    for every x, so the integer walk takes exactly the fp32 walk's branches.
+//  * The code is computed by walking a perfect binary search tree over the u_j
+//    in Eytzinger (heap) order — itself a perfect-tree traversal: after L =
+//    bit_length(m) steps of  i <- 2 i + pred(e_i, x)  the rank is i - 2^L
+//    (padding slots hold NaN, so pred is false there, i.e. they sort last).
+//
+// Why: a warp-wide LDS.64 is served in two half-warp passes, so 8-B node
+// records cost >= 2 SMEM wavefronts per level; a 4-B record costs 1 when the
+// level's nodes are distinct banks. The bank-conflict model of DESIGN.md §4.1
+// (validated against ncu: 31.9 vs 31.1 wavefronts per warp-tree) gives 20.3
+// wavefronts per warp-tree for this layout, plus ~7% for the per-tile code
+// transform.
+//
+// Node record: u32 = (k << 16) | (fc * 128). The per-warp code tile holds
+// cell[fc][lane] = c(x) << 16 as u32, so lane l always reads bank l
+// (conflict-free whatever feature it needs), and "go left" is the single
+// unsigned compare  node >= cell  (k >= c  <=>  (k << 16 | off) >= c << 16);
+// fc * 128 is the byte offset of the feature's row of cells (n_fc <= 511).
+// Leaf layout makes the leaf address equal to the final heap byte offset: tree
+// record = node[2^D] (node[0] = tree_output) then leaf[2^D] (w = 1), so after D
+// levels off = 4 i with i in [2^D, 2^(D+1)) and leaf(i - 2^D) sits at off.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "hb_device.cuh"
+#include "hb_internal.h"
+
+namespace hb {
+
+struct RankAux {
+  // per compact feature: {orig feature, L, byte offset inside its group, group}
+  // per group: {byte offset in the eytzinger pool, bytes, fc_begin, fc_end}
+  std::vector<uint32_t> fmeta, groups;
+  std::vector<float> pool;
+  int n_fc = 0, n_groups = 0;
+  size_t max_feat_bytes = 0;
+};
+
+static int bit_length(uint32_t m) {
+  int L = 0;
+  while ((1u << L) <= m) ++L;
+  return L;  // 2^L - 1 >= m
+}
+
+static void eytz_fill(const std::vector<float> &sorted, std::vector<float> &out, int L, int p,
+                      size_t &next) {
+  if (p >= (1 << L)) return;
+  eytz_fill(sorted, out, L, 2 * p, next);
+  out[p] = next < sorted.size() ? sorted[next] : NAN;
+  ++next;
+  eytz_fill(sorted, out, L, 2 * p + 1, next);
+}
+
+static int env_int2(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
+// Builds the rank-coded layout; returns HB_E_UNSUPPORTED (and leaves m intact)
+// when the model does not qualify (caller then uses the fp32 PTT layout).
+hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m) {
+  if (env_int2("HB_PTT_RANK", -1) == 0) return HB_E_UNSUPPORTED;
+  const int F = e->n_features, w = e->leaf_width;
+  const int Tpad = m->n_trees_pad;
+  // 1. distinct thresholds per feature
+  std::vector<std::vector<float>> th(F);
+  for (int t = t0; t < t1; ++t)
+    for (int64_t i = e->node_offset[t]; i < e->node_offset[t + 1]; ++i)
+      if (e->left[i] != -1) {
+        float v = e->threshold[i];
+        if (v == 0.f) v = 0.f;  // -0 == +0 under IEEE compare
+        th[e->feature[i]].push_back(v);
+      }
+  std::vector<int> fc_of(F, -1);
+  RankAux A;
+  std::vector<std::vector<float>> sorted;
+  for (int f = 0; f < F; ++f) {
+    if (th[f].empty()) continue;
+    std::vector<float> &v = th[f];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    if (v.size() > 65534) return HB_E_UNSUPPORTED;
+    fc_of[f] = A.n_fc++;
+    sorted.push_back(v);
+  }
+  if (A.n_fc > 511) return HB_E_UNSUPPORTED;    // fc * 128 must fit 16 bits
+  // 2. tree records
+  const int P = 1 << D;
+  const size_t stride = (4 * (size_t)P + 4 * (size_t)w * P + 15) & ~size_t(15);
+  std::vector<uint8_t> buf((size_t)Tpad * stride, 0);
+  std::vector<int32_t> leafmap((size_t)Tpad * P, -1);
+  std::vector<int> orig(2 * P);
+  const uint32_t kPad = 0xFFFF0000u;  // k = 0xFFFF: always left; any column
+  for (int lt = 0; lt < Tpad; ++lt) {
+    uint8_t *rec = buf.data() + (size_t)lt * stride;
+    uint32_t *node = reinterpret_cast<uint32_t *>(rec);
+    float *leaf = reinterpret_cast<float *>(rec + 4 * (size_t)P);
+    for (int p = 1; p < P; ++p) node[p] = kPad;
+    if (lt >= t1 - t0) continue;   // zero tree
+    const int t = t0 + lt;
+    const int64_t a = e->node_offset[t];
+    node[0] = (uint32_t)(w == 1 ? (e->tree_output ? e->tree_output[t] : t % e->n_outputs) : 0);
+    orig[1] = 0;
+    for (int p = 1; p < P; ++p) {
+      const int o = orig[p];
+      if (e->left[a + o] != -1) {
+        const int f = e->feature[a + o];
+        float v = e->threshold[a + o];
+        if (v == 0.f) v = 0.f;
+        const std::vector<float> &u = sorted[fc_of[f]];
+        const uint32_t k = (uint32_t)(std::lower_bound(u.begin(), u.end(), v) - u.begin());
+        node[p] = (k << 16) | (uint32_t)(fc_of[f] * 128);
+        orig[2 * p] = e->left[a + o];
+        orig[2 * p + 1] = e->right[a + o];
+      } else {
+        orig[2 * p] = orig[2 * p + 1] = o;
+      }
+    }
+    if (D == 0) orig[1] = 0;
+    for (int p = P; p < 2 * P; ++p) {
+      const int o = D == 0 ? 0 : orig[p];
+      const int slot = p - P;
+      for (int k = 0; k < w; ++k) leaf[(size_t)slot * w + k] = e->leaf_value[(a + o) * w + k];
+      leafmap[(size_t)lt * P + slot] = o;
+    }
+  }
+  // 3. Eytzinger arrays, grouped later by stage size
+  std::vector<std::vector<float>> ey(A.n_fc);
+  std::vector<int> Ls(A.n_fc);
+  for (int c = 0; c < A.n_fc; ++c) {
+    const int L = bit_length((uint32_t)sorted[c].size());
+    Ls[c] = L;
+    ey[c].assign(std::max(4, 1 << L), NAN);   // >= 16 B, slot 0 unused
+    size_t next = 0;
+    eytz_fill(sorted[c], ey[c], L, 1, next);
+    A.max_feat_bytes = std::max(A.max_feat_bytes, ey[c].size() * 4);
+  }
+  // 4. launch configuration: X codes NW*n_fc*128 B + a 2-stage ring of large
+  //    items. Every consumer warp waits for every ring item, so items must be
+  //    big (>= 32 trees) for the per-item sync and bulk-copy latency to hide;
+  //    measured on B200: C3 24 warps x 2 stages x 32 trees =
+  //    636M rows/s vs 520M with 16-tree chunks.
+  const int force = env_int2("HB_PTT_RANK", -1);
+  LaunchCfg cfg;
+  bool ok = false;
+  const int force_nw = env_int2("HB_NW", 0);
+  const int min_ch = force == 1 ? kTreeGroup : std::min(32, Tpad);
+  for (int nw : {24, 16, 12, 8, 4}) {
+    if (force_nw && nw != force_nw) continue;
+    if (force != 1 && nw < 24) break;               // auto: only the full-occupancy shape
+    const long xb = (long)nw * A.n_fc * 128;
+    const long rem = (long)kSmemBudget - xb;
+    const int ns = env_int2("HB_NS", 2);
+    const long per = rem / ns - 16;
+    if (per < (long)A.max_feat_bytes || per < (long)kTreeGroup * (long)stride) continue;
+    int ch = (int)std::min<long>(env_int2("HB_CH", 64), per / (long)stride) & ~(kTreeGroup - 1);
+    ch = std::min(ch, Tpad);
+    if (ch < min_ch) continue;
+    const long stage = std::max<long>((long)ch * stride, (long)A.max_feat_bytes);
+    cfg.nw = nw;
+    cfg.ns = ns;
+    cfg.ch = ch;
+    cfg.x_smem = 1;
+    cfg.t_smem = 1;
+    cfg.stage_bytes = (int)((stage + 127) & ~127L);
+    cfg.smem_bytes = (int)(xb + (long)ns * cfg.stage_bytes + 16 * ns);
+    ok = cfg.smem_bytes <= kSmemBudget;
+    if (ok) break;
+  }
+  // auto: the per-tile rank transform (n_fc searches of depth L per row) must
+  // stay small next to the walk it shortens (T * D levels per row)
+  if (ok && force != 1) {
+    double lsum = 0;
+    for (int c = 0; c < A.n_fc; ++c) lsum += Ls[c];
+    if (lsum > 0.1 * (double)Tpad * (double)std::max(D, 1)) ok = false;
+  }
+  if (!ok) return HB_E_UNSUPPORTED;
+  // 5. group features into stage-sized bulk copies
+  {
+    size_t goff = 0, gbytes = 0;
+    int gbeg = 0;
+    auto close = [&](int end) {
+      A.groups.insert(A.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)gbeg, (uint32_t)end});
+      goff += gbytes;
+      gbytes = 0;
+      gbeg = end;
+      A.n_groups++;
+    };
+    for (int c = 0; c < A.n_fc; ++c) {
+      const size_t b = ey[c].size() * 4;
+      if (gbytes + b > (size_t)cfg.stage_bytes) close(c);
+      A.fmeta.insert(A.fmeta.end(), {0u, (uint32_t)Ls[c], (uint32_t)gbytes, (uint32_t)A.n_groups});
+      gbytes += b;
+      A.pool.insert(A.pool.end(), ey[c].begin(), ey[c].end());
+    }
+    if (gbytes) close(A.n_fc);
+    int c = 0;
+    for (int f = 0; f < F; ++f)
+      if (fc_of[f] >= 0) A.fmeta[4 * c++] = (uint32_t)f;
+  }
+  // 6. upload: trees, leafmap, aux = [fmeta | groups | pool]
+  cudaError_t err;
+  if ((err = cudaMalloc(&m->d_trees, buf.size())) != cudaSuccess) return cuda_fail(err, "cudaMalloc(pttr)");
+  m->device_bytes += buf.size();
+  if ((err = cudaMemcpy(m->d_trees, buf.data(), buf.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(err, "cudaMemcpy(pttr)");
+  if ((err = cudaMalloc(&m->d_leafmap, leafmap.size() * 4)) != cudaSuccess)
+    return cuda_fail(err, "cudaMalloc(pttr leafmap)");
+  m->device_bytes += leafmap.size() * 4;
+  if ((err = cudaMemcpy(m->d_leafmap, leafmap.data(), leafmap.size() * 4, cudaMemcpyHostToDevice)) !=
+      cudaSuccess)
+    return cuda_fail(err, "cudaMemcpy(pttr leafmap)");
+  const size_t fb = A.fmeta.size() * 4, gb = A.groups.size() * 4, pb = A.pool.size() * 4;
+  const size_t pool_off = (fb + gb + 127) & ~size_t(127);
+  std::vector<uint8_t> aux(pool_off + pb, 0);
+  std::memcpy(aux.data(), A.fmeta.data(), fb);
+  std::memcpy(aux.data() + fb, A.groups.data(), gb);
+  std::memcpy(aux.data() + pool_off, A.pool.data(), pb);
+  if ((err = cudaMalloc(&m->d_aux, aux.size())) != cudaSuccess) return cuda_fail(err, "cudaMalloc(pttr aux)");
+  m->device_bytes += aux.size();
+  if ((err = cudaMemcpy(m->d_aux, aux.data(), aux.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(err, "cudaMemcpy(pttr aux)");
+  m->aux_groups_off = fb;
+  m->aux_pool_off = pool_off;
+  m->rank_nfc = A.n_fc;
+  m->rank_ngroups = A.n_groups;
+  m->stride = stride;
+  m->nslots = P;
+  m->cfg = cfg;
+  m->ptt_rank = 1;
+  return HB_OK;
+}
+
+// ------------------------------------------------------------------ device
+struct PttrParams {
+  const float *X;
+  int64_t n, ldx;
+  const uint8_t *trees;
+  uint32_t stride;
+  int n_trees_pad, n_trees, tree_begin;
+  const int32_t *leafmap;
+  int nslots;
+  const uint4 *fmeta;     // [n_fc] {orig f, L, offset in group, group}
+  const uint4 *groups;    // [n_groups] {pool byte offset, bytes, fc_begin, fc_end}
+  const uint8_t *pool;
+  int n_fc, n_groups;
+  int F, vec4, x_direct;  // x_direct: all F features used -> stage X into the cells, recode in place
+  const float *scale, *base;
+  int K, w, task, post, kind;
+  void *out;
+  int nw, ns, ch, ntiles;
+  uint32_t stage_bytes;
+};
+
+template <int D, bool LE, int NACC, int G>
+__global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = p.nw, ns = p.ns, ch = p.ch;
+  const size_t xbytes = (size_t)nw * p.n_fc * 128;
+  uint8_t *stages = smem + xbytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(stages + (size_t)ns * p.stage_bytes);
+  uint64_t *empty = full + ns;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], nw);
+    }
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunks = (p.n_trees_pad + ch - 1) / ch;
+  const int items = p.n_groups + nchunks;          // per tile: feature groups, then tree chunks
+  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  if (warp == nw) {
+    if (lane == 0) {
+      const long total = (long)my_tiles * items;
+      for (long it = 0; it < total; ++it) {
+        const int s = (int)(it % ns);
+        dev::mbar_wait(&empty[s], (uint32_t)((it / ns) & 1) ^ 1u);
+        const int q = (int)(it % items);
+        const uint8_t *src;
+        uint32_t bytes;
+        if (q < p.n_groups) {
+          const uint4 g = __ldg(p.groups + q);
+          src = p.pool + g.x;
+          bytes = g.y;
+        } else {
+          const int t0 = (q - p.n_groups) * ch;
+          src = p.trees + (size_t)t0 * p.stride;
+          bytes = (uint32_t)min(ch, p.n_trees_pad - t0) * p.stride;
+        }
+        dev::mbar_arrive_expect_tx(&full[s], bytes);
+        dev::bulk_g2s(stages + (size_t)s * p.stage_bytes, src, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const uint32_t codes = dev::smem_u32(smem) + (uint32_t)(warp * p.n_fc * 128) + 4u * lane;
+  const uint32_t stage0 = dev::smem_u32(stages);
+  const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
+  long it = 0;
+  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
+    const int64_t row = wrow0 + lane;
+    const bool active = wrow0 < p.n;
+    const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
+    if (p.x_direct && active) {
+      // fp32 X slice straight into the code cells (cell(f, lane) = xs[f*32 + lane])
+      dev::load_x_slice(reinterpret_cast<float *>(smem) + (size_t)warp * p.n_fc * 32, p.X, row, p.n,
+                        p.ldx, p.F, lane, p.vec4 != 0);
+    }
+
+    // ---- rank codes of this warp's 32 rows, one feature group per stage
+    for (int gq = 0; gq < p.n_groups; ++gq, ++it) {
+      const int s = (int)(it % ns);
+      dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+      if (active) {
+        const uint4 g = __ldg(p.groups + gq);
+        const uint32_t gb = stage0 + (uint32_t)s * p.stage_bytes;
+        // four independent searches per lane (memory-level parallelism); the
+        // per-feature depth L is warp-uniform, so the guards do not diverge
+        for (int fc = (int)g.z; fc < (int)g.w; fc += 4) {
+          uint32_t i[4], eb[4], L[4];
+          float x[4];
+          uint32_t lmax = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool valid = fc + q < (int)g.w;
+            const uint4 fm = __ldg(p.fmeta + (valid ? fc + q : fc));
+            x[q] = p.x_direct ? dev::lds_f32(codes + (uint32_t)(valid ? fc + q : fc) * 128u)
+                              : __ldg(xr + fm.x);
+            eb[q] = gb + fm.z;
+            L[q] = valid ? fm.y : 0u;
+            i[q] = 1u;
+            lmax = max(lmax, L[q]);
+          }
+          for (uint32_t l = 0; l < lmax; ++l) {
+            // branch-free: finished searches re-read a valid slot and keep i
+            float u[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) u[q] = dev::lds_f32(eb[q] + (l < L[q] ? 4u * i[q] : 4u));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const bool pr = LE ? (u[q] < x[q]) : (u[q] <= x[q]);   // u sorts before x
+              const uint32_t nx = 2u * i[q] + (pr ? 1u : 0u);
+              i[q] = l < L[q] ? nx : i[q];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (fc + q < (int)g.w) {
+              const uint32_t code = (x[q] != x[q]) ? 0xFFFFu : i[q] - (1u << L[q]);
+              dev::sts_u32(codes + (uint32_t)(fc + q) * 128u, code << 16);
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[s]);
+    }
+
+    float acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    uint64_t h = 0;
+    for (int c = 0; c < nchunks; ++c, ++it) {
+      const int s = (int)(it % ns);
+      dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+      if (active) {
+        const uint32_t cb = stage0 + (uint32_t)s * p.stage_bytes;
+        const int nt = min(ch, p.n_trees_pad - c * ch);
+        for (int j = 0; j < nt; j += G) {
+          uint32_t tb[G], off[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            tb[g] = cb + (uint32_t)(j + g) * p.stride;
+            off[g] = 4u;                      // heap node 1, 4-B records
+          }
+#pragma unroll
+          for (int l = 0; l < D; ++l) {
+            uint32_t nd[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(tb[g] + off[g]);
+            uint32_t xc[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) xc[g] = dev::lds_u32(codes + (nd[g] & 0xFFFFu));
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const bool left = nd[g] >= xc[g];           // k >= c(x)  <=>  x < u_k
+              off[g] = 2u * off[g] + (left ? 0u : 4u);
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t slot = (off[g] >> 2) - (1u << D);
+            if (p.w == 1) {
+              const float v = dev::lds_f32(tb[g] + off[g]);   // leaf(slot) == byte offset 4 i
+              if (NACC == 1) {
+                acc[0] += v;
+              } else {
+                const uint32_t k0 = dev::lds_u32(tb[g]);
+#pragma unroll
+                for (int k = 0; k < NACC; ++k)
+                  if (k0 == (uint32_t)k) acc[k] += v;
+              }
+            } else {
+              const uint32_t lb = tb[g] + (4u << D) + 4u * slot * (uint32_t)p.w;
+#pragma unroll
+              for (int k = 0; k < NACC; ++k)
+                if (k < p.K) acc[k] += dev::lds_f32(lb + 4u * k);
+            }
+            if (lm) {
+              const int t = c * ch + j + g;
+              if (t < p.n_trees) {
+                const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + slot);
+                if (lm == 1) {
+                  if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+                } else {
+                  h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[s]);
+    }
+    if (row < p.n) {
+      if (lm == 2) {
+        static_cast<uint64_t *>(p.out)[row] = h;
+      } else if (lm == 0) {
+        dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
+      }
+    }
+  }
+}
+
+using PttrFn = void (*)(const PttrParams);
+
+template <int D, bool LE>
+static PttrFn pick_nacc(int nacc) {
+  switch (nacc) {
+    case 1: return pttr_kernel<D, LE, 1, kTreeGroup>;
+    case 4: return pttr_kernel<D, LE, 4, kTreeGroup>;
+    case 8: return pttr_kernel<D, LE, 8, kTreeGroup>;
+    default: return pttr_kernel<D, LE, 16, kTreeGroup>;
+  }
+}
+
+template <int D>
+static PttrFn pick_le(bool le, int nacc) {
+  return le ? pick_nacc<D, true>(nacc) : pick_nacc<D, false>(nacc);
+}
+
+static PttrFn pick(int D, bool le, int nacc) {
+  switch (D) {
+    case 0: return pick_le<0>(le, nacc);
+    case 1: return pick_le<1>(le, nacc);
+    case 2: return pick_le<2>(le, nacc);
+    case 3: return pick_le<3>(le, nacc);
+    case 4: return pick_le<4>(le, nacc);
+    case 5: return pick_le<5>(le, nacc);
+    case 6: return pick_le<6>(le, nacc);
+    case 7: return pick_le<7>(le, nacc);
+    case 8: return pick_le<8>(le, nacc);
+    case 9: return pick_le<9>(le, nacc);
+    case 10: return pick_le<10>(le, nacc);
+    default: return nullptr;
+  }
+}
+
+int sm_count(int device);
+
+hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
+  PttrFn fn = pick(m.depth, m.cmp == HB_CMP_LE, m.nacc);
+  if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
+  PttrParams p;
+  p.X = a.X;
+  p.n = a.n;
+  p.ldx = a.ldx;
+  p.trees = static_cast<const uint8_t *>(m.d_trees);
+  p.stride = (uint32_t)m.stride;
+  p.n_trees_pad = m.n_trees_pad;
+  p.n_trees = m.n_trees;
+  p.tree_begin = m.tree_begin;
+  p.leafmap = m.d_leafmap;
+  p.nslots = m.nslots;
+  const uint8_t *aux = static_cast<const uint8_t *>(m.d_aux);
+  p.fmeta = reinterpret_cast<const uint4 *>(aux);
+  p.groups = reinterpret_cast<const uint4 *>(aux + m.aux_groups_off);
+  p.pool = aux + m.aux_pool_off;
+  p.n_fc = m.rank_nfc;
+  p.n_groups = m.rank_ngroups;
+  p.F = m.n_features;
+  p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
+  p.x_direct = m.rank_nfc == m.n_features;
+  p.scale = m.d_scale;
+  p.base = m.d_base;
+  p.K = m.n_outputs;
+  p.w = m.leaf_width;
+  p.task = m.task;
+  p.post = m.post;
+  p.kind = a.kind;
+  p.out = a.out;
+  p.nw = m.cfg.nw;
+  p.ns = m.cfg.ns;
+  p.ch = m.cfg.ch;
+  p.stage_bytes = (uint32_t)m.cfg.stage_bytes;
+  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
+  const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
+  if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
+  p.ntiles = (int)ntiles;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       m.cfg.smem_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(pttr)");
+  fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pttr_kernel launch");
+  return HB_OK;
+}
+
+}  // namespace hb

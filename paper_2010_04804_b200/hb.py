@@ -46,7 +46,7 @@ class _Info(C.Structure):
                 ("n_features", C.c_int32), ("n_outputs", C.c_int32),
                 ("leaf_width", C.c_int32), ("device", C.c_int32), ("x_in_smem", C.c_int32),
                 ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64),
-                ("tensor_cores", C.c_int32), ("reserved", C.c_int32)]
+                ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32)]
 
 
 def _load():

@@ -118,16 +118,40 @@ for strat, D in (("ptt", 8), ("ptt", 5), ("tt", 8), ("tt", 11), ("gemm", 3), ("g
 
 
 @pytest.mark.parametrize("strat,D,kind,cmp", CASES)
-def test_strategy_parity(strat, D, kind, cmp):
+def test_strategy_parity(strat, D, kind, cmp, monkeypatch):
     seed = zlib.crc32(f"{strat}{D}{kind}{cmp}".encode()) & 0xFFFF
     family = FAMILIES[seed % 3]
     F = [3, 17, 28, 54][seed % 4]
     T = 37 if strat != "gemm" else 23    # odd: exercises tree-group padding
     e = _forest(kind, T, D, F, seed, family, cmp)
-    m = hb.Model(e, strategy=strat, device=0)
-    assert m.info["strategy_name"] == strat
     n = 1500 + seed % 97                 # several 512-row tiles + ragged tail
     Xd, Xh = X_pair(seed, n, F, special_q24=SPECIAL_Q24)
+    # PTT has two node layouts: rank-coded 4-B records (default) and fp32 8-B
+    for rank in (("1", "0") if strat == "ptt" else ("1",)):
+        monkeypatch.setenv("HB_PTT_RANK", rank)
+        m = hb.Model(e, strategy=strat, device=0)
+        assert m.info["strategy_name"] == strat
+        if strat == "ptt":
+            assert m.info["node_record_bytes"] == (4 if rank == "1" else 8)
+        check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("cmp", [0, 1])
+@pytest.mark.parametrize("rank", ["1", "0"])
+def test_ptt_special_thresholds(cmp, rank, monkeypatch):
+    """Thresholds at +-Inf and -0/+0 (mixed on one feature) against X holding
+    NaN, +-Inf, +-0 and exact ties: the rank code must reproduce every fp32
+    decision (reading R3), for both PTT node layouts."""
+    monkeypatch.setenv("HB_PTT_RANK", rank)
+    e = _forest("binary", 33, 6, 5, 17, "mixed", cmp, grid=synth.GRID_COARSE)
+    rng = np.random.default_rng(3)
+    internal = np.nonzero(e.left != -1)[0]
+    pick = rng.choice(internal, size=len(internal) // 3, replace=False)
+    specials = np.array([np.inf, -np.inf, 0.0, -0.0], np.float32)
+    e.threshold[pick] = specials[rng.integers(0, 4, pick.size)]
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["node_record_bytes"] == (4 if rank == "1" else 8)
+    Xd, Xh = X_pair(8, 4000, 5, grid=synth.GRID_COARSE, special_q24=1 << 22)
     check_all(e, m, Xd, Xh)
 
 
@@ -275,14 +299,26 @@ def test_gemm_tc_vs_cuda_core_many_trees(tc, monkeypatch):
     check_all(e, m, Xd, Xh)
 
 
-def test_auto_strategy_selection():
+def test_auto_strategy_selection(monkeypatch):
     """Sec. 5.1 heuristic (reading R24): GEMM D <= 3, PTT D <= 10, TT beyond;
     PTT falls back to TT when rows are too wide for the SMEM X tile."""
     for D, want in ((2, "gemm"), (3, "gemm"), (4, "ptt"), (8, "ptt"), (10, "ptt"), (11, "tt"),
                     (12, "tt")):
         e = synth.gen_forest(4, D, 8, seed=D, family="skinny")
         assert hb.Model(e, device=0).info["strategy_name"] == want, D
-    wide = synth.gen_forest(4, 6, 2000, seed=1, family="balanced")
+    # a wide row whose few used features fit the rank-coded PTT code tile can
+    # be forced onto PTT (rank layout = feature compaction); AUTO keeps TT
+    # there because the per-tile rank transform would dominate 4 trees
+    sparse = synth.gen_forest(2, 5, 2000, seed=1, family="balanced")
+    assert hb.Model(sparse, device=0).info["strategy_name"] == "tt"
+    monkeypatch.setenv("HB_PTT_RANK", "1")
+    m = hb.Model(sparse, strategy="ptt", device=0)
+    assert m.info["strategy_name"] == "ptt" and m.info["node_record_bytes"] == 4
+    Xd, Xh = X_pair(4, 700, 2000)
+    check_all(e=sparse, m=m, Xd=Xd, Xh=Xh, kinds=("raw", "leaf"))
+    monkeypatch.delenv("HB_PTT_RANK")
+    # many used features: neither PTT layout fits SMEM -> AUTO falls back to TT
+    wide = synth.gen_forest(300, 6, 2000, seed=1, family="balanced")
     assert hb.Model(wide, device=0).info["strategy_name"] == "tt"
     with pytest.raises(hb.HBError) as ei:
         hb.Model(wide, strategy="ptt", device=0)
