@@ -84,6 +84,21 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Position in an NS-stage mbarrier ring (stage index + phase parity),
+// advanced incrementally: no 64-bit division in the hot loops.
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  int ns;
+  __device__ __forceinline__ explicit Ring(int n) : ns(n) {}
+  __device__ __forceinline__ void next() {
+    if (++s == ns) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
 // Per-lane X row staging: lane `lane` of a warp owns row `row`; the warp's
 // slice is feature-major xs[f * 32 + lane] so that every later data-dependent
 // read X[row, f] hits bank `lane` (conflict-free whatever f each lane needs).

@@ -65,11 +65,11 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
     // ---------------- producer warp: stream tree chunks through the ring
     if (lane == 0) {
       const long total = (long)my_tiles * nchunks;
-      for (long it = 0; it < total; ++it) {
-        const int s = (int)(it % ns);
-        const uint32_t ph = (uint32_t)((it / ns) & 1);
-        dev::mbar_wait(&empty[s], ph ^ 1u);
-        const int c = (int)(it % nchunks);
+      dev::Ring r(ns);
+      int c = 0;
+      for (long it = 0; it < total; ++it, r.next(), c = (c + 1 == nchunks) ? 0 : c + 1) {
+        const int s = r.s;
+        dev::mbar_wait(&empty[s], r.ph ^ 1u);
         const int t0 = c * ch;
         const int nt = min(ch, p.n_trees_pad - t0);
         const uint32_t bytes = (uint32_t)nt * p.stride;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
   const uint32_t stage0 = dev::smem_u32(stages);
   const uint32_t leaf_off = 4u << D;                      // leaf(i) at tree + leaf_off + 4 i ... (w = 1)
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
-  long it = 0;
+  dev::Ring ring(ns);
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
     const int64_t row = wrow0 + lane;
@@ -98,25 +98,29 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
     uint64_t h = 0;
 
-    for (int c = 0; c < nchunks; ++c, ++it) {
-      const int s = (int)(it % ns);
-      dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+    for (int c = 0; c < nchunks; ++c, ring.next()) {
+      const int s = ring.s;
+      dev::mbar_wait(&full[s], ring.ph);
       if (active) {
         const uint32_t cb = stage0 + (uint32_t)(s * ch) * p.stride;
         const int nt = min(ch, p.n_trees_pad - c * ch);
         for (int j = 0; j < nt; j += G) {
-          uint32_t tb[G], off[G];
+          // a = absolute address of heap node i (tree + 8 i); next level:
+          // a' = tree + 16 i + (pr ? 0 : 8) = 2 a + (pr ? -tree : 8 - tree)
+          uint32_t tb[G], a[G], m0[G], m8[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             tb[g] = cb + (uint32_t)(j + g) * p.stride;
-            off[g] = 8u;                    // heap node 1 (the root), 8-B records
+            a[g] = tb[g] + 8u;              // heap node 1 (the root), 8-B records
+            m0[g] = 0u - tb[g];
+            m8[g] = 8u - tb[g];
           }
           // Alg. 3: T_I <- 2 T_I + (X[r, N'_F[T_I]] < N'_T[T_I] ? 0 : 1), D times
 #pragma unroll
           for (int l = 0; l < D; ++l) {
             uint2 nd[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) nd[g] = dev::lds_v2(tb[g] + off[g]);
+            for (int g = 0; g < G; ++g) nd[g] = dev::lds_v2(a[g]);
             float x[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) x[g] = dev::lds_f32(xlane + (nd[g].x << 7));
@@ -124,9 +128,12 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
             for (int g = 0; g < G; ++g) {
               const float t = __uint_as_float(nd[g].y);
               const bool pr = LE ? (x[g] <= t) : (x[g] < t);
-              off[g] = 2u * off[g] + (pr ? 0u : 8u);
+              a[g] = 2u * a[g] + (pr ? m0[g] : m8[g]);
             }
           }
+          uint32_t off[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) off[g] = a[g] - tb[g];
           // R <- N'_C[T_I - 2^D]
 #pragma unroll
           for (int g = 0; g < G; ++g) {

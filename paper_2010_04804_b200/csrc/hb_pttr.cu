@@ -22,11 +22,12 @@
 // wavefronts per warp-tree for this layout, plus ~7% for the per-tile code
 // transform.
 //
-// Node record: u32 = (k << 16) | (fc * 128). The per-warp code tile holds
-// cell[fc][lane] = c(x) << 16 as u32, so lane l always reads bank l
-// (conflict-free whatever feature it needs), and "go left" is the single
-// unsigned compare  node >= cell  (k >= c  <=>  (k << 16 | off) >= c << 16);
-// fc * 128 is the byte offset of the feature's row of cells (n_fc <= 511).
+// Node record: u32 = (fc * 128) << 16 | k. The per-warp code tile holds
+// cell[fc][lane] = (fc * 128) << 16 | c(x) as u32, so lane l always reads bank l
+// (conflict-free whatever feature it needs), the cell address is one LEA.HI
+// (tile + (node >> 16)), and since node and cell share the high half, "go
+// left" is the single unsigned compare  node >= cell  <=>  k >= c(x)
+// (n_fc <= 511 so that fc * 128 fits 16 bits).
 // Leaf layout makes the leaf address equal to the final heap byte offset: tree
 // record = node[2^D] (node[0] = tree_output) then leaf[2^D] (w = 1), so after D
 // levels off = 4 i with i in [2^D, 2^(D+1)) and leaf(i - 2^D) sits at off.
@@ -106,7 +107,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   std::vector<uint8_t> buf((size_t)Tpad * stride, 0);
   std::vector<int32_t> leafmap((size_t)Tpad * P, -1);
   std::vector<int> orig(2 * P);
-  const uint32_t kPad = 0xFFFF0000u;  // k = 0xFFFF: always left; any column
+  const uint32_t kPad = 0x0000FFFFu;  // column 0, k = 0xFFFF >= any code: always left
   for (int lt = 0; lt < Tpad; ++lt) {
     uint8_t *rec = buf.data() + (size_t)lt * stride;
     uint32_t *node = reinterpret_cast<uint32_t *>(rec);
@@ -125,7 +126,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
         if (v == 0.f) v = 0.f;
         const std::vector<float> &u = sorted[fc_of[f]];
         const uint32_t k = (uint32_t)(std::lower_bound(u.begin(), u.end(), v) - u.begin());
-        node[p] = (k << 16) | (uint32_t)(fc_of[f] * 128);
+        node[p] = ((uint32_t)(fc_of[f] * 128) << 16) | k;
         orig[2 * p] = e->left[a + o];
         orig[2 * p + 1] = e->right[a + o];
       } else {
@@ -188,7 +189,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   if (ok && force != 1) {
     double lsum = 0;
     for (int c = 0; c < A.n_fc; ++c) lsum += Ls[c];
-    if (lsum > 0.1 * (double)Tpad * (double)std::max(D, 1)) ok = false;
+    if (lsum > 0.2 * (double)Tpad * (double)std::max(D, 1)) ok = false;
   }
   if (!ok) return HB_E_UNSUPPORTED;
   // 5. group features into stage-sized bulk copies
@@ -292,10 +293,11 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
   if (warp == nw) {
     if (lane == 0) {
       const long total = (long)my_tiles * items;
-      for (long it = 0; it < total; ++it) {
-        const int s = (int)(it % ns);
-        dev::mbar_wait(&empty[s], (uint32_t)((it / ns) & 1) ^ 1u);
-        const int q = (int)(it % items);
+      dev::Ring r(ns);
+      int q = 0;
+      for (long it = 0; it < total; ++it, r.next(), q = (q + 1 == items) ? 0 : q + 1) {
+        const int s = r.s;
+        dev::mbar_wait(&empty[s], r.ph ^ 1u);
         const uint8_t *src;
         uint32_t bytes;
         if (q < p.n_groups) {
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
   const uint32_t codes = dev::smem_u32(smem) + (uint32_t)(warp * p.n_fc * 128) + 4u * lane;
   const uint32_t stage0 = dev::smem_u32(stages);
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
-  long it = 0;
+  dev::Ring ring(ns);
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
     const int64_t row = wrow0 + lane;
@@ -330,9 +332,9 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
     }
 
     // ---- rank codes of this warp's 32 rows, one feature group per stage
-    for (int gq = 0; gq < p.n_groups; ++gq, ++it) {
-      const int s = (int)(it % ns);
-      dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+    for (int gq = 0; gq < p.n_groups; ++gq, ring.next()) {
+      const int s = ring.s;
+      dev::mbar_wait(&full[s], ring.ph);
       if (active) {
         const uint4 g = __ldg(p.groups + gq);
         const uint32_t gb = stage0 + (uint32_t)s * p.stage_bytes;
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
           for (int q = 0; q < 4; ++q)
             if (fc + q < (int)g.w) {
               const uint32_t code = (x[q] != x[q]) ? 0xFFFFu : i[q] - (1u << L[q]);
-              dev::sts_u32(codes + (uint32_t)(fc + q) * 128u, code << 16);
+              dev::sts_u32(codes + (uint32_t)(fc + q) * 128u, ((uint32_t)(fc + q) << 23) | code);
             }
         }
       }
@@ -381,33 +383,40 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
     uint64_t h = 0;
-    for (int c = 0; c < nchunks; ++c, ++it) {
-      const int s = (int)(it % ns);
-      dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+    for (int c = 0; c < nchunks; ++c, ring.next()) {
+      const int s = ring.s;
+      dev::mbar_wait(&full[s], ring.ph);
       if (active) {
         const uint32_t cb = stage0 + (uint32_t)s * p.stage_bytes;
         const int nt = min(ch, p.n_trees_pad - c * ch);
         for (int j = 0; j < nt; j += G) {
-          uint32_t tb[G], off[G];
+          // a = absolute address of heap node i (tree + 4 i); next level:
+          // a' = tree + 8 i + (left ? 0 : 4) = 2 a + (left ? -tree : 4 - tree)
+          uint32_t tb[G], a[G], m0[G], m4[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             tb[g] = cb + (uint32_t)(j + g) * p.stride;
-            off[g] = 4u;                      // heap node 1, 4-B records
+            a[g] = tb[g] + 4u;                 // heap node 1 (root), 4-B records
+            m0[g] = 0u - tb[g];
+            m4[g] = 4u - tb[g];
           }
 #pragma unroll
           for (int l = 0; l < D; ++l) {
             uint32_t nd[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(tb[g] + off[g]);
+            for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(a[g]);
             uint32_t xc[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) xc[g] = dev::lds_u32(codes + (nd[g] & 0xFFFFu));
+            for (int g = 0; g < G; ++g) xc[g] = dev::lds_u32(codes + (nd[g] >> 16));
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               const bool left = nd[g] >= xc[g];           // k >= c(x)  <=>  x < u_k
-              off[g] = 2u * off[g] + (left ? 0u : 4u);
+              a[g] = 2u * a[g] + (left ? m0[g] : m4[g]);
             }
           }
+          uint32_t off[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) off[g] = a[g] - tb[g];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const uint32_t slot = (off[g] >> 2) - (1u << D);

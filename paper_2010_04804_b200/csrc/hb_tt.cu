@@ -75,10 +75,12 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
   if (warp == nw) {
     if (p.t_smem && lane == 0) {
       const long total = (long)my_tiles * nchunks;
-      for (long it = 0; it < total; ++it) {
-        const int s = (int)(it % ns);
-        dev::mbar_wait(&empty[s], (uint32_t)((it / ns) & 1) ^ 1u);
-        const int t0 = (int)(it % nchunks) * ch;
+      dev::Ring r(ns);
+      int c = 0;
+      for (long it = 0; it < total; ++it, r.next(), c = (c + 1 == nchunks) ? 0 : c + 1) {
+        const int s = r.s;
+        dev::mbar_wait(&empty[s], r.ph ^ 1u);
+        const int t0 = c * ch;
         const int nt = min(ch, p.n_trees_pad - t0);
         const uint32_t bytes = (uint32_t)nt * p.stride;
         dev::mbar_arrive_expect_tx(&full[s], bytes);
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 
   float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
-  long it = 0;
+  dev::Ring ring(ns);
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row = (int64_t)tile * (nw * 32) + warp * 32 + lane;
     const float *xrow;
@@ -112,8 +114,8 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
       const uint8_t *cb;
       int s = 0;
       if (p.t_smem) {
-        s = (int)(it % ns);
-        dev::mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+        s = ring.s;
+        dev::mbar_wait(&full[s], ring.ph);
         cb = stages + (size_t)s * ch * p.stride;
       } else {
         cb = p.trees + (size_t)c * ch * p.stride;
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
       if (p.t_smem) {
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&empty[s]);
-        ++it;
+        ring.next();
       }
     }
     if (row < p.n) {
