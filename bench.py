@@ -281,7 +281,10 @@ def run_ours(args):
         except Exception as ex:  # pragma: no cover
             peaks = {"error": str(ex)}
     smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
-    prof = load_profile(args.config, info["strategy_name"])
+    layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "")
+    prof = load_profile(args.config, layout)
+    kname = {"ptt": "ptt_kernel", "ptt-rank": "pttr_kernel", "gemm": "gemm_tc_kernel" if info.get("tensor_cores") else "gemm_kernel",
+             "tt": "tt_wide_kernel" if info.get("x_in_smem") and cfg.n_features > 1000 else "tt_kernel"}.get(layout, layout)
     hbm_bytes = n * (cfg.n_features * 4 + (8 if (cls and e.n_outputs == 1) else 4 * e.n_outputs))
     measured = {}
     try:
@@ -295,7 +298,7 @@ def run_ours(args):
         "traffic": prof.get("smem_ld_bytes_per_launch") if prof.get("rows") == n else None,
         "traffic_dram": prof.get("dram_bytes_per_launch") if prof.get("rows") == n else None,
         "traffic_source": prof.get("source"),
-        "kernel": f"{info['strategy_name']}_kernel", "kernel_ms": kern_ms,
+        "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
         "algorithmic_bytes_per_row": per_row,
         "peak_source": "measured LDS.128 microbenchmark (tools/peaks.cu), this run" if peaks.get("smem_gbs")
         else "spec 148 SM x 128 B/clk x 1.965 GHz",
@@ -318,9 +321,9 @@ def run_ours(args):
             dist.barrier()
         ts = []
         for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
+            w0 = time.perf_counter()
             m.predict_host(Xh, kind, out=oh)
-            ts.append(time.perf_counter() - t0)
+            ts.append(time.perf_counter() - w0)
         t_e2e = float(np.mean(ts))
         if dist:
             t_e2e = max_over_ranks(t_e2e, device=X.device)
