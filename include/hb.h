@@ -61,8 +61,11 @@ typedef enum { HB_POST_IDENTITY = 0, HB_POST_SIGMOID = 1, HB_POST_SOFTMAX = 2 } 
 typedef enum { HB_TASK_REGRESSION = 0, HB_TASK_CLASSIFICATION = 1 } hb_task;
 
 /* Compilation strategy (Sec. 4.1). AUTO applies the depth heuristic of
- * Sec. 5.1: GEMM if D_max <= 3, PTT if D_max <= 10, else TT
- * (reading R24; env HB_GEMM_MAX_DEPTH / HB_PTT_MAX_DEPTH override). */
+ * Sec. 5.1 with thresholds recalibrated on B200 (DESIGN.md §6.1,
+ * reading R24): PTT if D_max <= 10, else TT; GEMM only when forced or when
+ * env HB_GEMM_MAX_DEPTH is set (3 restores the paper's CPU rule). Independently
+ * of the strategy, calls with n_rows <= 4096 (env HB_SMALL_BATCH) use the
+ * trees-across-threads small-batch kernel. */
 typedef enum {
   HB_STRATEGY_AUTO = 0,
   HB_STRATEGY_GEMM = 1,

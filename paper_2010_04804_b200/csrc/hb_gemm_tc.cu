@@ -178,7 +178,8 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
   m->cfg.x_smem = xb <= 64 * 1024 ? 1 : 0;
   m->cfg.t_smem = 1;
   m->cfg.smem_bytes = (int)((m->cfg.x_smem ? xb : 0) + 2 * g.stride + kTcRows * 16 * 2 * kTcPairs + 64);
-  m->cfg.ctas_per_sm = m->cfg.smem_bytes <= 100 * 1024 ? 2 : 1;
+  // 4 warps per CTA: fill the SM with up to 4 CTAs (TMEM: 4 x 128 columns = 512)
+  m->cfg.ctas_per_sm = std::max(1, std::min(4, (int)(kSmemBudget / std::max(1, m->cfg.smem_bytes))));
   m->gemm_tc = 1;
   return HB_OK;
 }

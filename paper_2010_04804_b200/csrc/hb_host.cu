@@ -339,10 +339,15 @@ static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool
 }
 
 
-// Sec. 5.1: GEMM for shallow trees, PTT up to D = 10, TT beyond
-// (reading R24 for the GPU thresholds).
+// Sec. 5.1: GEMM for shallow trees, PTT up to D = 10, TT beyond,
+// with the crossover "determined by ... the underlying hardware". Recalibrated
+// on B200 by tools/crossover.py (profiles/r01_crossover.json):
+// PTT beats TT up to D = 10 at large batches, TT wins beyond; the tcgen05 GEMM
+// never beats PTT (large batches) or the small-batch kernel (small batches),
+// so AUTO does not pick GEMM unless HB_GEMM_MAX_DEPTH is set (3 = the paper's
+// CPU rule).
 static int select_strategy(int D) {
-  const int gemm_max = env_int("HB_GEMM_MAX_DEPTH", 3);
+  const int gemm_max = env_int("HB_GEMM_MAX_DEPTH", -1);
   const int ptt_max = std::min(env_int("HB_PTT_MAX_DEPTH", kPttMaxDepth), kPttMaxDepth);
   if (D <= gemm_max && gemm_supported(D)) return HB_STRATEGY_GEMM;
   if (D <= ptt_max) return HB_STRATEGY_PTT;
@@ -358,6 +363,8 @@ static void free_model(Model *m) {
   cudaFree(m->d_base);
   cudaFree(m->d_gemm);
   cudaFree(m->d_aux);
+  cudaFree(m->sb_own_trees);
+  cudaFree(m->sb_own_leafmap);
   delete m;
 }
 
@@ -481,6 +488,36 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   }
   m->strategy = strat;
 
+  // small-batch path: reuse the PTT fp32 / TT records, else build PTT fp32 ones
+  if (strat == HB_STRATEGY_TT) {
+    m->sb_trees = m->d_trees;
+    m->sb_leafmap = m->d_leafmap;
+    m->sb_stride = m->stride;
+    m->sb_nslots = m->nslots;
+    m->sb_tt = 1;
+    m->sb_depth = D;
+  } else if (strat == HB_STRATEGY_PTT && !m->ptt_rank) {
+    m->sb_trees = m->d_trees;
+    m->sb_leafmap = m->d_leafmap;
+    m->sb_stride = m->stride;
+    m->sb_nslots = m->nslots;
+    m->sb_depth = D;
+  } else if (D <= kPttMaxDepth) {
+    HostLayout S;
+    build_ptt(e, t0, t1, D, m->n_trees_pad, &S);
+    uint8_t *dt = nullptr;
+    st = upload(S.trees, &dt, &m->device_bytes);
+    if (st != HB_OK) return st;
+    m->sb_own_trees = dt;
+    st = upload(S.leafmap, &m->sb_own_leafmap, &m->device_bytes);
+    if (st != HB_OK) return st;
+    m->sb_trees = dt;
+    m->sb_leafmap = m->sb_own_leafmap;
+    m->sb_stride = S.stride;
+    m->sb_nslots = S.nslots;
+    m->sb_depth = D;
+  }
+
   // global per-output tree counts (MEAN divisor) and base score
   std::vector<float> div(K, 1.f), base(K, 0.f);
   if (e->agg == HB_AGG_MEAN) {
@@ -565,6 +602,10 @@ static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int
     if (st != HB_OK) return st;
   }
   RunArgs a{X, n, ldx, kind, out, static_cast<cudaStream_t>(stream), nullptr};
+  // request/response sizes: trees-across-threads kernel (f2); threshold from
+  // the crossover sweep (tools/crossover.py)
+  const int small_max = env_int("HB_SMALL_BATCH", 4096);
+  if (n <= small_max && m.sb_trees) return launch_small_batch(m, a);
   return run(m, a);
 }
 

@@ -63,6 +63,15 @@ struct Model {
   size_t aux_groups_off = 0, aux_pool_off = 0;
   int rank_nfc = 0, rank_ngroups = 0;
 
+  // small-batch path (hb_small.cu): PTT fp32 or TT records walked by
+  // trees-across-threads; may alias d_trees / d_leafmap
+  const void *sb_trees = nullptr;
+  const int32_t *sb_leafmap = nullptr;
+  void *sb_own_trees = nullptr;
+  int32_t *sb_own_leafmap = nullptr;
+  size_t sb_stride = 0;
+  int sb_nslots = 0, sb_tt = 0, sb_depth = 0;
+
   size_t device_bytes = 0;
   LaunchCfg cfg;
 };
@@ -94,5 +103,6 @@ hb_status launch_ptt(const Model &m, const RunArgs &a);
 hb_status launch_tt(const Model &m, const RunArgs &a);
 hb_status launch_gemm(const Model &m, const RunArgs &a);
 hb_status launch_finalize(const Model &m, const RunArgs &a);
+hb_status launch_small_batch(const Model &m, const RunArgs &a);
 
 }  // namespace hb

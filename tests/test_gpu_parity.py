@@ -24,6 +24,13 @@ import paper_2010_04804_b200 as hb  # noqa: E402
 import synth.dev  # noqa: E402
 
 
+@pytest.fixture(autouse=True)
+def _large_batch_kernels(monkeypatch):
+    """Parity tests exercise the row-tile scorers by default; the small-batch
+    (trees-across-threads) path is tested explicitly below."""
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")
+
+
 def tol_ok(got, ref):
     got = np.asarray(got, np.float64)
     return np.abs(got - ref) <= 1e-5 + 1e-5 * np.abs(ref)
@@ -299,13 +306,50 @@ def test_gemm_tc_vs_cuda_core_many_trees(tc, monkeypatch):
     check_all(e, m, Xd, Xh)
 
 
+SMALL_CASES = [(strat, D, kind, cmp) for strat, D in (("ptt", 8), ("tt", 11), ("gemm", 3))
+               for kind in ("reg", "binary", "multiclass", "rf") for cmp in (0, 1)]
+
+
+@pytest.mark.parametrize("strat,D,kind,cmp", SMALL_CASES)
+def test_small_batch_path_parity(strat, D, kind, cmp, monkeypatch):
+    """Request/response sizes (n = 1..300) go through the trees-across-threads
+    kernel (hb_small.cu) for every strategy; all outputs against the oracle."""
+    monkeypatch.setenv("HB_SMALL_BATCH", "4096")
+    seed = zlib.crc32(f"small{strat}{D}{kind}{cmp}".encode()) & 0xFFFF
+    e = _forest(kind, 41, D, 19, seed, FAMILIES[seed % 3], cmp)
+    m = hb.Model(e, strategy=strat, device=0)
+    for n in (1, 7, 300):
+        Xd, Xh = X_pair(seed + n, n, 19, special_q24=SPECIAL_Q24)
+        check_all(e, m, Xd, Xh)
+
+
+def test_small_and_large_paths_agree(monkeypatch):
+    e = _forest("binary", 500, 8, 28, 1, "balanced", 0)
+    m = hb.Model(e, device=0)
+    Xd, Xh = X_pair(2, 1000, 28)
+    monkeypatch.setenv("HB_SMALL_BATCH", "4096")
+    small = m.predict_proba(Xd).cpu().numpy().astype(np.float64)
+    hs = m.predict_leaf_hash(Xd).cpu().numpy()
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")
+    large = m.predict_proba(Xd).cpu().numpy().astype(np.float64)
+    assert np.array_equal(hs, m.predict_leaf_hash(Xd).cpu().numpy())
+    assert np.abs(small - large).max() < 1e-5
+
+
 def test_auto_strategy_selection(monkeypatch):
-    """Sec. 5.1 heuristic (reading R24): GEMM D <= 3, PTT D <= 10, TT beyond;
+    """Sec. 5.1 heuristic recalibrated on B200 (reading R24): PTT D <= 10, TT
+    beyond, GEMM on request (HB_GEMM_MAX_DEPTH);
     PTT falls back to TT when rows are too wide for the SMEM X tile."""
-    for D, want in ((2, "gemm"), (3, "gemm"), (4, "ptt"), (8, "ptt"), (10, "ptt"), (11, "tt"),
+    for D, want in ((2, "ptt"), (3, "ptt"), (4, "ptt"), (8, "ptt"), (10, "ptt"), (11, "tt"),
                     (12, "tt")):
         e = synth.gen_forest(4, D, 8, seed=D, family="skinny")
         assert hb.Model(e, device=0).info["strategy_name"] == want, D
+    # the paper's CPU rule (GEMM for D <= 3) on request
+    monkeypatch.setenv("HB_GEMM_MAX_DEPTH", "3")
+    for D, want in ((2, "gemm"), (3, "gemm"), (4, "ptt")):
+        e = synth.gen_forest(4, D, 8, seed=D, family="skinny")
+        assert hb.Model(e, device=0).info["strategy_name"] == want, D
+    monkeypatch.delenv("HB_GEMM_MAX_DEPTH")
     # a wide row whose few used features fit the rank-coded PTT code tile can
     # be forced onto PTT (rank layout = feature compaction); AUTO keeps TT
     # there because the per-tile rank transform would dominate 4 trees
