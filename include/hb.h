@@ -55,8 +55,16 @@ typedef enum { HB_CMP_LT = 0, HB_CMP_LE = 1 } hb_cmp;
  * by the number of trees feeding it in the WHOLE ensemble. */
 typedef enum { HB_AGG_SUM = 0, HB_AGG_MEAN = 1 } hb_agg;
 
-/* Post transform of the margin (Table 2: sigmoid, exp, logsumexp). */
-typedef enum { HB_POST_IDENTITY = 0, HB_POST_SIGMOID = 1, HB_POST_SOFTMAX = 2 } hb_post;
+/* Post transform of the margin (Table 2: sigmoid, exp, logsumexp).
+ * ISOLATION (IsolationForest, Table 1): with leaf
+ * values = path length h (depth + c(leaf size) - 1) and agg = MEAN, the
+ * anomaly score is 2^(-margin / post_param), post_param = c(psi) > 0. */
+typedef enum {
+  HB_POST_IDENTITY = 0,
+  HB_POST_SIGMOID = 1,
+  HB_POST_SOFTMAX = 2,
+  HB_POST_ISOLATION = 3
+} hb_post;
 
 typedef enum { HB_TASK_REGRESSION = 0, HB_TASK_CLASSIFICATION = 1 } hb_task;
 
@@ -115,6 +123,7 @@ typedef struct {
   int32_t agg;                  /* hb_agg      */
   int32_t post;                 /* hb_post     */
   int32_t task;                 /* hb_task     */
+  float post_param;             /* ISOLATION: c(psi) > 0; ignored otherwise */
 } hb_ensemble;
 
 typedef struct hb_model hb_model;
@@ -142,6 +151,7 @@ typedef struct {
  * binary tree (one parent per non-root node, no cycles, all nodes reachable,
  * left == -1 <=> right == -1); feature in range; threshold not NaN; leaf values
  * finite; tree_output in [0, K); SIGMOID => K == 1; SOFTMAX => K >= 2;
+ * ISOLATION => K == 1, REGRESSION and a finite post_param > 0;
  * CLASSIFICATION => (K == 1 and SIGMOID) or K >= 2. */
 hb_status hb_validate(const hb_ensemble *e);
 

@@ -37,7 +37,8 @@ class _Ens(C.Structure):
                 ("threshold", C.c_void_p), ("left", C.c_void_p), ("right", C.c_void_p),
                 ("leaf_value", C.c_void_p), ("leaf_width", C.c_int32),
                 ("tree_output", C.c_void_p), ("base_score", C.c_void_p),
-                ("cmp", C.c_int32), ("agg", C.c_int32), ("post", C.c_int32)]
+                ("cmp", C.c_int32), ("agg", C.c_int32), ("post", C.c_int32),
+                ("post_param", C.c_double)]
 
 
 _lib = None
@@ -81,7 +82,7 @@ class _Handle:
                       arr(e.right, np.int32), arr(e.leaf_value, np.float32),
                       int(e.leaf_width), arr(e.tree_output, np.int32),
                       arr(e.base_score, np.float32), int(e.cmp), int(e.agg),
-                      int(e.post))
+                      int(e.post), float(getattr(e, "post_param", 0.0)))
         self.K = int(e.n_outputs)
         self.T = int(e.n_trees)
 

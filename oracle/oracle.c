@@ -109,6 +109,9 @@ void oracle_post(const oracle_ensemble *e, const double *margin, int64_t n, doub
       for (int32_t k = 0; k < K; ++k) o[k] = m[k];
     } else if (e->post == 1) {
       for (int32_t k = 0; k < K; ++k) o[k] = 1.0 / (1.0 + exp(-m[k]));
+    } else if (e->post == 3) {
+      /* IsolationForest anomaly score: 2^(-E[h(x)] / c(psi)) */
+      for (int32_t k = 0; k < K; ++k) o[k] = pow(2.0, -m[k] / e->post_param);
     } else {
       double mx = m[0];
       for (int32_t k = 1; k < K; ++k) if (m[k] > mx) mx = m[k];

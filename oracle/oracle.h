@@ -12,7 +12,8 @@
  *   the reached leaf is leaf[r][t] (its tree-local ORIGINAL node id).
  *   raw[r][k]    = sum over trees feeding k, in tree order, fp64.
  *   margin[r][k] = (agg == MEAN ? raw / ntrees_k : raw) + base[k].
- *   post: identity | sigmoid | softmax (max-subtracted), fp64.
+ *   post: identity | sigmoid | softmax (max-subtracted) | isolation
+ *   2^(-margin / c(psi)) (IsolationForest, Liu et al.; sklearn score_samples), fp64.
  *   label: K == 1 -> margin > 0 ; K >= 2 -> argmax, lowest index on ties.
  *
  * The GEMM / TreeTraversal / PerfectTreeTraversal strategies reach exactly
@@ -39,7 +40,8 @@ typedef struct {
   const float   *base_score;    /* [n_outputs] or NULL => 0 */
   int32_t cmp;                  /* 0 = LT, 1 = LE */
   int32_t agg;                  /* 0 = SUM, 1 = MEAN */
-  int32_t post;                 /* 0 = identity, 1 = sigmoid, 2 = softmax */
+  int32_t post;                 /* 0 = identity, 1 = sigmoid, 2 = softmax, 3 = isolation */
+  double post_param;            /* isolation: c(psi) */
 } oracle_ensemble;
 
 /* leaf ids: out[r * (t1 - t0) + (t - t0)] for trees t in [t0, t1). */

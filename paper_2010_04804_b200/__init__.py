@@ -9,4 +9,4 @@ There is no CPU fallback: if libhb.so is missing, importing the binding raises.
 """
 from .hb import (HBError, Model, validate, lib, lib_path, exported_symbols,  # noqa: F401
                  STRATEGY, OUT, CMP_LT, CMP_LE, AGG_SUM, AGG_MEAN, POST_IDENTITY,
-                 POST_SIGMOID, POST_SOFTMAX, TASK_REGRESSION, TASK_CLASSIFICATION)
+                 POST_SIGMOID, POST_SOFTMAX, POST_ISOLATION, TASK_REGRESSION, TASK_CLASSIFICATION)

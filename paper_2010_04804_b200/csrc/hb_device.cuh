@@ -122,6 +122,15 @@ __device__ __forceinline__ void load_x_slice(float *xs, const float *__restrict_
   }
 }
 
+// Same, for a compacted feature set (feature-selection injection):
+// slice column c holds X[row, fmap[c]] for the model's used features only.
+__device__ __forceinline__ void load_x_slice_map(float *xs, const float *__restrict__ X, int64_t row,
+                                                 int64_t n, int64_t ldx,
+                                                 const int32_t *__restrict__ fmap, int nx, int lane) {
+  const float *xr = X + (row < n ? row : 0) * ldx;
+  for (int c = 0; c < nx; ++c) xs[c * 32 + lane] = row < n ? __ldg(xr + __ldg(fmap + c)) : 0.f;
+}
+
 // Fused epilogue for one row (a10/a11 of SURVEY §8): margin = acc / div +
 // base, post transform, proba / label, coalesced-enough row-major stores.
 template <int NACC>
@@ -176,6 +185,11 @@ __device__ __forceinline__ void write_row(int kind, const float (&acc)[NACC], in
     }
 #pragma unroll
     for (int k = 0; k < NACC; ++k) p[k] = p[k] / s;
+  } else if (post == HB_POST_ISOLATION) {
+    // 2^(-mean path length / c(psi)); c(psi) is stored after the K base scores
+    const float c = __ldg(base + K);
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) p[k] = exp2f(-m[k] / c);
   } else {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) p[k] = m[k];

@@ -76,7 +76,10 @@ static hb_status validate_impl(const hb_ensemble *e, std::vector<TreeInfo> *info
   if (e->cmp != HB_CMP_LT && e->cmp != HB_CMP_LE)
     return fail(HB_E_UNSUPPORTED, "cmp must be HB_CMP_LT or HB_CMP_LE (GT/GE would change NaN routing)");
   if (e->agg != HB_AGG_SUM && e->agg != HB_AGG_MEAN) return fail(HB_E_TREE, "bad agg");
-  if (e->post < HB_POST_IDENTITY || e->post > HB_POST_SOFTMAX) return fail(HB_E_TREE, "bad post");
+  if (e->post < HB_POST_IDENTITY || e->post > HB_POST_ISOLATION) return fail(HB_E_TREE, "bad post");
+  if (e->post == HB_POST_ISOLATION &&
+      (K != 1 || e->task != HB_TASK_REGRESSION || !(e->post_param > 0.f) || !std::isfinite(e->post_param)))
+    return fail(HB_E_TREE, "ISOLATION requires n_outputs == 1, REGRESSION and post_param > 0");
   if (e->task != HB_TASK_REGRESSION && e->task != HB_TASK_CLASSIFICATION)
     return fail(HB_E_TREE, "bad task");
   if (e->post == HB_POST_SIGMOID && K != 1) return fail(HB_E_TREE, "SIGMOID requires n_outputs == 1");
@@ -163,6 +166,34 @@ static inline uint32_t f2u(float f) {
 
 static size_t round16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Feature-selection injection (Sec. 5.2): "for tree models,
+// we update the indices of the decision variables" — used features get
+// compact ids in first-use-independent (ascending) order.
+struct FeatureMap {
+  std::vector<int32_t> remap;    // original -> compact (-1 unused)
+  std::vector<int32_t> used;     // compact -> original
+  bool identity = true;
+};
+
+static FeatureMap feature_map(const hb_ensemble *e, int t0, int t1) {
+  FeatureMap fm;
+  std::vector<char> u(e->n_features, 0);
+  for (int t = t0; t < t1; ++t)
+    for (int64_t i = e->node_offset[t]; i < e->node_offset[t + 1]; ++i)
+      if (e->left[i] != -1) u[e->feature[i]] = 1;
+  fm.remap.assign(e->n_features, -1);
+  for (int f = 0; f < e->n_features; ++f)
+    if (u[f]) {
+      fm.remap[f] = (int32_t)fm.used.size();
+      fm.used.push_back(f);
+    }
+  if (fm.used.empty()) fm.used.push_back(0), fm.remap[0] = 0;
+  fm.identity = (int)fm.used.size() == e->n_features;
+  if (fm.identity)
+    for (int f = 0; f < e->n_features; ++f) fm.remap[f] = f;
+  return fm;
+}
+
 struct HostLayout {
   std::vector<uint8_t> trees;
   std::vector<int32_t> leafmap;
@@ -176,7 +207,8 @@ struct HostLayout {
 // A leaf at depth D_k < D becomes a perfect subtree whose decision nodes
 // compare feature 0 against +Inf ("free to perform arbitrary comparisons")
 // and whose 2^(D-D_k) leaves copy the leaf; leafmap keeps the original id.
-static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, HostLayout *L) {
+static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, HostLayout *L,
+                      const FeatureMap *fm = nullptr) {
   const int w = e->leaf_width;
   const int P = 1 << D;
   L->nslots = P;
@@ -200,7 +232,7 @@ static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, Hos
     for (int p = 1; p < P; ++p) {
       const int o = orig[p];
       if (e->left[a + o] != -1) {
-        node[2 * p] = (uint32_t)e->feature[a + o];
+        node[2 * p] = (uint32_t)(fm ? fm->remap[e->feature[a + o]] : e->feature[a + o]);
         node[2 * p + 1] = f2u(e->threshold[a + o]);
         orig[2 * p] = e->left[a + o];
         orig[2 * p + 1] = e->right[a + o];
@@ -228,7 +260,8 @@ static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, Hos
 // node[nslots] = {N_F | N_R << 16, N_T}, float leaf[nslots][w] = N_C. Leaves
 // self-loop (N_R = self, N_T = NaN => predicate false for LT and LE). Padded
 // to the max node count over trees.
-static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLayout *L) {
+static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLayout *L,
+                          const FeatureMap *fm = nullptr) {
   const int w = e->leaf_width;
   int maxn = 1;
   for (int t = t0; t < t1; ++t)
@@ -268,7 +301,7 @@ static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLa
       L->leafmap[(size_t)lt * maxn + j] = o;
       if (e->left[a + o] != -1) {
         const int r = newid[e->right[a + o]];
-        node[2 * j] = (uint32_t)e->feature[a + o] | ((uint32_t)r << 16);
+        node[2 * j] = (uint32_t)(fm ? fm->remap[e->feature[a + o]] : e->feature[a + o]) | ((uint32_t)r << 16);
         node[2 * j + 1] = f2u(e->threshold[a + o]);
       } else {
         for (int k = 0; k < w; ++k) leaf[(size_t)j * w + k] = e->leaf_value[(a + o) * w + k];
@@ -365,6 +398,7 @@ static void free_model(Model *m) {
   cudaFree(m->d_aux);
   cudaFree(m->sb_own_trees);
   cudaFree(m->sb_own_leafmap);
+  cudaFree(m->d_fmap);
   delete m;
 }
 
@@ -427,16 +461,26 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     if (st != HB_OK) return st;
   } else {
     bool done = false;
+    const FeatureMap fmap = feature_map(e, t0, t1);
+    m->n_xf = (int)fmap.used.size();
+    if (!fmap.identity) {
+      st = upload(fmap.used, &m->d_fmap, &m->device_bytes);
+      if (st != HB_OK) return st;
+    }
     if (strat == HB_STRATEGY_PTT && D <= kPttMaxDepth) {
-      st = compile_ptt_rank(e, t0, t1, D, m.get());   // 4-B rank-coded nodes when eligible
+      // warps the fp32-node layout would get (the rank layout must match it)
+      LaunchCfg fcfg;
+      const size_t fstride = round16((size_t)8 * (1 << D) + (size_t)4 * e->leaf_width * (1 << D));
+      const int nw_fp32 = choose_cfg(m->n_xf, fstride, m->n_trees_pad, false, false, 24, &fcfg) ? fcfg.nw : 0;
+      st = compile_ptt_rank(e, t0, t1, D, m.get(), nw_fp32);   // 4-B rank-coded nodes when eligible
       if (st == HB_OK) done = true;
       else if (st != HB_E_UNSUPPORTED) return st;
     }
     if (!done && strat == HB_STRATEGY_PTT) {
       bool ok = D <= kPttMaxDepth;
       if (ok) {
-        build_ptt(e, t0, t1, D, m->n_trees_pad, &L);
-        ok = choose_cfg(e->n_features, L.stride, m->n_trees_pad, false, false, 24, &m->cfg);
+        build_ptt(e, t0, t1, D, m->n_trees_pad, &L, &fmap);
+        ok = choose_cfg((int)fmap.used.size(), L.stride, m->n_trees_pad, false, false, 24, &m->cfg);
       }
       if (!ok) {
         if (strategy == HB_STRATEGY_PTT)
@@ -449,11 +493,11 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
       }
     }
     if (!done && strat == HB_STRATEGY_TT) {
-      st = build_tt(e, t0, t1, m->n_trees_pad, &L);
+      st = build_tt(e, t0, t1, m->n_trees_pad, &L, &fmap);
       if (st != HB_OK) return st;
       // rows that fit a 32-row-per-warp SMEM slice with room for a tree ring
       // use tt_kernel; wider rows or trees too big for SMEM use tt_wide_kernel
-      const bool narrow = choose_cfg(e->n_features, L.stride, m->n_trees_pad, false, false, 16, &m->cfg);
+      const bool narrow = choose_cfg((int)fmap.used.size(), L.stride, m->n_trees_pad, false, false, 16, &m->cfg);
       const int force_wide = env_int("HB_TT_WIDE", -1);
       if (!narrow || force_wide == 1) {
         if (force_wide == 0) return fail(HB_E_UNSUPPORTED, "TT: no narrow configuration fits");
@@ -463,7 +507,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.nw = 32;
         c.wide_rows = 0;
         for (int R : {32, 16, 8}) {
-          const long bytes = (long)e->n_features * R * 4 + (long)c.nw * R * (4L * nacc + 8);
+          const long bytes = (long)fmap.used.size() * R * 4 + (long)c.nw * R * (4L * nacc + 8);
           if (bytes <= kSmemBudget) {
             c.wide_rows = R;
             c.smem_bytes = (int)bytes;
@@ -489,6 +533,11 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   m->strategy = strat;
 
   // small-batch path: reuse the PTT fp32 / TT records, else build PTT fp32 ones
+  m->sb_nxf = m->n_features;
+  if (strat == HB_STRATEGY_TT || (strat == HB_STRATEGY_PTT && !m->ptt_rank)) {
+    m->sb_fmap = m->d_fmap;     // those records index the compacted tile
+    m->sb_nxf = m->n_xf;
+  }
   if (strat == HB_STRATEGY_TT) {
     m->sb_trees = m->d_trees;
     m->sb_leafmap = m->d_leafmap;
@@ -519,7 +568,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   }
 
   // global per-output tree counts (MEAN divisor) and base score
-  std::vector<float> div(K, 1.f), base(K, 0.f);
+  std::vector<float> div(K, 1.f), base(K + 1, 0.f);   // base[K] = post_param
   if (e->agg == HB_AGG_MEAN) {
     std::vector<double> cnt(K, 0.0);
     for (int t = 0; t < e->n_trees; ++t) {
@@ -530,6 +579,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   }
   if (e->base_score)
     for (int k = 0; k < K; ++k) base[k] = e->base_score[k];
+  base[K] = e->post == HB_POST_ISOLATION ? e->post_param : 1.f;
   st = upload(div, &m->d_scale, &m->device_bytes);
   if (st != HB_OK) return st;
   st = upload(base, &m->d_base, &m->device_bytes);

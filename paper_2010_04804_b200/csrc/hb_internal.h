@@ -71,6 +71,13 @@ struct Model {
   int32_t *sb_own_leafmap = nullptr;
   size_t sb_stride = 0;
   int sb_nslots = 0, sb_tt = 0, sb_depth = 0;
+  const int32_t *sb_fmap = nullptr;   // feature map of the small-batch records
+  int sb_nxf = 0;
+
+  // feature-selection injection: fp32 PTT / TT records index a
+  // compacted X tile holding only the model's used features
+  int32_t *d_fmap = nullptr;   // [n_xf] compact column -> original feature (null: identity)
+  int n_xf = 0;
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
@@ -96,7 +103,7 @@ hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);
 bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1);
 hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m);
 hb_status launch_gemm_tc(const Model &m, const RunArgs &a);
-hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m);
+hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m, int nw_fp32);
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);

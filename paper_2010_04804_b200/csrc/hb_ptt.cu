@@ -26,7 +26,8 @@ namespace hb {
 struct PttParams {
   const float *X;
   int64_t n, ldx;
-  int F;
+  int F;                  // columns of the X slice (used features when fmap != null)
+  const int32_t *fmap;    // compact column -> original feature, or null (identity)
   int vec4;
   const uint8_t *trees;
   uint32_t stride;
@@ -92,7 +93,10 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
     const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
     const int64_t row = wrow0 + lane;
     const bool active = wrow0 < p.n;        // whole warp beyond n: only keep the ring in step
-    if (active) dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+    if (active) {
+      if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
+      else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+    }
     float acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
@@ -224,7 +228,8 @@ hb_status launch_ptt(const Model &m, const RunArgs &a) {
   p.X = a.X;
   p.n = a.n;
   p.ldx = a.ldx;
-  p.F = m.n_features;
+  p.F = m.n_xf;
+  p.fmap = m.d_fmap;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   p.trees = static_cast<const uint8_t *>(m.d_trees);
   p.stride = (uint32_t)m.stride;

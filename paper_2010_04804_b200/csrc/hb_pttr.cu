@@ -75,7 +75,7 @@ static int env_int2(const char *name, int dflt) {
 
 // Builds the rank-coded layout; returns HB_E_UNSUPPORTED (and leaves m intact)
 // when the model does not qualify (caller then uses the fp32 PTT layout).
-hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m) {
+hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m, int nw_fp32) {
   if (env_int2("HB_PTT_RANK", -1) == 0) return HB_E_UNSUPPORTED;
   const int F = e->n_features, w = e->leaf_width;
   const int Tpad = m->n_trees_pad;
@@ -152,19 +152,17 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     eytz_fill(sorted[c], ey[c], L, 1, next);
     A.max_feat_bytes = std::max(A.max_feat_bytes, ey[c].size() * 4);
   }
-  // 4. launch configuration: X codes NW*n_fc*128 B + a 2-stage ring of large
-  //    items. Every consumer warp waits for every ring item, so items must be
-  //    big (>= 32 trees) for the per-item sync and bulk-copy latency to hide;
-  //    measured on B200: C3 24 warps x 2 stages x 32 trees =
-  //    636M rows/s vs 520M with 16-tree chunks.
+  // 4. launch configuration: X codes NW*n_fc*128 B + a 2-stage ring. Every
+  //    consumer warp waits for every ring item, so items should be large:
+  //    the largest tree chunk that fits (<= 64 trees) for the most warps.
+  //    Measured on B200: C3 24 warps x 2 stages x 32 trees =
+  //    700M rows/s vs 520M with 16-tree chunks.
   const int force = env_int2("HB_PTT_RANK", -1);
   LaunchCfg cfg;
   bool ok = false;
   const int force_nw = env_int2("HB_NW", 0);
-  const int min_ch = force == 1 ? kTreeGroup : std::min(32, Tpad);
   for (int nw : {24, 16, 12, 8, 4}) {
     if (force_nw && nw != force_nw) continue;
-    if (force != 1 && nw < 24) break;               // auto: only the full-occupancy shape
     const long xb = (long)nw * A.n_fc * 128;
     const long rem = (long)kSmemBudget - xb;
     const int ns = env_int2("HB_NS", 2);
@@ -172,7 +170,6 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     if (per < (long)A.max_feat_bytes || per < (long)kTreeGroup * (long)stride) continue;
     int ch = (int)std::min<long>(env_int2("HB_CH", 64), per / (long)stride) & ~(kTreeGroup - 1);
     ch = std::min(ch, Tpad);
-    if (ch < min_ch) continue;
     const long stage = std::max<long>((long)ch * stride, (long)A.max_feat_bytes);
     cfg.nw = nw;
     cfg.ns = ns;
@@ -184,12 +181,15 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     ok = cfg.smem_bytes <= kSmemBudget;
     if (ok) break;
   }
-  // auto: the per-tile rank transform (n_fc searches of depth L per row) must
-  // stay small next to the walk it shortens (T * D levels per row)
+  // auto: rank-coded nodes only when (a) the per-tile rank
+  // transform (sum_f L_f searches per row) stays small next to the walk it
+  // shortens (T * D levels per row) and (b) the layout runs at least as many
+  // warps as the fp32-node layout would (occupancy decides at equal bytes).
   if (ok && force != 1) {
     double lsum = 0;
     for (int c = 0; c < A.n_fc; ++c) lsum += Ls[c];
     if (lsum > 0.2 * (double)Tpad * (double)std::max(D, 1)) ok = false;
+    if (cfg.nw < nw_fp32) ok = false;
   }
   if (!ok) return HB_E_UNSUPPORTED;
   // 5. group features into stage-sized bulk copies

@@ -19,6 +19,7 @@ namespace hb {
 struct SbParams {
   const float *X;
   int64_t n, ldx;
+  const int32_t *fmap;       // compact column -> original feature, or null
   int F, depth, tt;          // tt: 1 = TT records (16-B header, self-loops), 0 = PTT fp32 records
   const uint8_t *trees;
   uint32_t stride;
@@ -66,7 +67,8 @@ __global__ void __launch_bounds__(256) small_batch_kernel(const SbParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
-    for (int f = threadIdx.x; f < p.F; f += blockDim.x) xs[f] = __ldg(p.X + row * p.ldx + f);
+    for (int f = threadIdx.x; f < p.F; f += blockDim.x)
+      xs[f] = __ldg(p.X + row * p.ldx + (p.fmap ? __ldg(p.fmap + f) : f));
     __syncthreads();
     float acc[NACC];
 #pragma unroll
@@ -151,7 +153,8 @@ hb_status launch_small_batch(const Model &m, const RunArgs &a) {
   p.X = a.X;
   p.n = a.n;
   p.ldx = a.ldx;
-  p.F = m.n_features;
+  p.F = m.sb_nxf;
+  p.fmap = m.sb_fmap;
   p.depth = m.sb_tt ? m.depth : m.sb_depth;
   p.tt = m.sb_tt;
   p.trees = static_cast<const uint8_t *>(m.sb_trees);
@@ -170,7 +173,7 @@ hb_status launch_small_batch(const Model &m, const RunArgs &a) {
   p.kind = a.kind;
   p.out = a.out;
   const int threads = 256;
-  const size_t smem = (size_t)((m.n_features + 3) & ~3) * 4 + 8 * 16 * 4 + 8 * 8;
+  const size_t smem = (size_t)((m.sb_nxf + 3) & ~3) * 4 + 8 * 16 * 4 + 8 * 8;
   if (smem > (size_t)kSmemBudget) return fail(HB_E_UNSUPPORTED, "small-batch path: row too wide");
   const int64_t grid = std::min<int64_t>(a.n, (int64_t)sm_count(m.device) * 16);
   SbFn fn = m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc);

@@ -23,7 +23,8 @@ namespace hb {
 struct TtParams {
   const float *X;
   int64_t n, ldx;
-  int F, vec4, depth;
+  int F, vec4, depth;     // F: columns of the X tile (used features when fmap != null)
+  const int32_t *fmap;    // compact column -> original feature, or null
   const uint8_t *trees;
   uint32_t stride;
   int n_trees_pad, n_trees, tree_begin;
@@ -99,7 +100,8 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
     const float *xrow;
     int xstride;
     if (p.x_smem) {
-      dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+      if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
+      else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
       xrow = xs + lane;
       xstride = 32;
     } else {
@@ -211,7 +213,8 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
     for (int idx = threadIdx.x; idx < R * p.F; idx += blockDim.x) {
       const int rr = idx / p.F, f = idx - rr * p.F;
       const int64_t gr = row0 + rr;
-      xs[f * R + rr] = gr < p.n ? __ldg(p.X + gr * p.ldx + f) : 0.f;
+      const int fo = p.fmap ? __ldg(p.fmap + f) : f;
+      xs[f * R + rr] = gr < p.n ? __ldg(p.X + gr * p.ldx + fo) : 0.f;
     }
     __syncthreads();
     const int64_t row = row0 + r;
@@ -354,7 +357,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.X = a.X;
   p.n = a.n;
   p.ldx = a.ldx;
-  p.F = m.n_features;
+  p.F = m.n_xf;
+  p.fmap = m.d_fmap;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   p.depth = m.depth;
   p.trees = static_cast<const uint8_t *>(m.d_trees);

@@ -11,7 +11,7 @@ lib_path = os.path.join(_PKG, "libhb.so")
 
 CMP_LT, CMP_LE = 0, 1
 AGG_SUM, AGG_MEAN = 0, 1
-POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX = 0, 1, 2
+POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX, POST_ISOLATION = 0, 1, 2, 3
 TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
 STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
@@ -37,7 +37,7 @@ class _Ens(C.Structure):
                 ("leaf_value", C.c_void_p), ("leaf_width", C.c_int32),
                 ("tree_output", C.c_void_p), ("base_score", C.c_void_p),
                 ("cmp", C.c_int32), ("agg", C.c_int32), ("post", C.c_int32),
-                ("task", C.c_int32)]
+                ("task", C.c_int32), ("post_param", C.c_float)]
 
 
 class _Info(C.Structure):
@@ -104,7 +104,8 @@ class _EnsHandle:
                       arr(e.right, np.int32), arr(e.leaf_value, np.float32),
                       int(e.leaf_width), arr(e.tree_output, np.int32),
                       arr(e.base_score, np.float32), int(e.cmp), int(e.agg),
-                      int(e.post), int(getattr(e, "task", 0)))
+                      int(e.post), int(getattr(e, "task", 0)),
+                      float(getattr(e, "post_param", 0.0)))
 
 
 def validate(e) -> None:

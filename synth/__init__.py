@@ -19,6 +19,6 @@ Recipes:
 from .xgen import gen_X, GRID_FINE, GRID_COARSE, mix64, counter_hash  # noqa: F401
 from .forest import (Ensemble, gen_forest, from_trees, tree_depths,  # noqa: F401
                      CMP_LT, CMP_LE, AGG_SUM, AGG_MEAN, POST_IDENTITY,
-                     POST_SIGMOID, POST_SOFTMAX, TASK_REGRESSION,
+                     POST_SIGMOID, POST_SOFTMAX, POST_ISOLATION, TASK_REGRESSION,
                      TASK_CLASSIFICATION)
 from .configs import CONFIGS, Config, make_config  # noqa: F401

@@ -17,7 +17,7 @@ from .xgen import GRID_FINE, GRID_COARSE
 
 CMP_LT, CMP_LE = 0, 1
 AGG_SUM, AGG_MEAN = 0, 1
-POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX = 0, 1, 2
+POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX, POST_ISOLATION = 0, 1, 2, 3
 TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 
 _NCODES = {GRID_FINE: 65536, GRID_COARSE: 64}
@@ -43,6 +43,7 @@ class Ensemble:
     agg: int = AGG_SUM
     post: int = POST_IDENTITY
     task: int = TASK_REGRESSION
+    post_param: float = 0.0          # ISOLATION: c(psi)
 
     @property
     def n_nodes(self) -> int:
@@ -68,7 +69,7 @@ class Ensemble:
                         self.left[a:b].copy(), self.right[a:b].copy(),
                         self.leaf_value[a * w:b * w].copy(), w, to,
                         None if self.base_score is None else self.base_score.copy(),
-                        self.cmp, self.agg, self.post, self.task)
+                        self.cmp, self.agg, self.post, self.task, self.post_param)
 
 
 def from_trees(trees, n_features, n_outputs=1, leaf_width=1, **kw) -> Ensemble:
@@ -102,7 +103,7 @@ def gen_forest(n_trees: int, depth: int, n_features: int, *, seed: int = 0,
                tree_output: Optional[np.ndarray] = None,
                base_score=None, cmp: int = CMP_LT, agg: int = AGG_SUM,
                post: int = POST_IDENTITY, task: int = TASK_REGRESSION,
-               permute: bool = True, features=None) -> Ensemble:
+               permute: bool = True, features=None, post_param: float = 0.0) -> Ensemble:
     """Draw ``n_trees`` random trees of maximum depth ``depth``.
 
     family: "balanced" (XGBoost-like, every node splits down to ``depth``),
@@ -249,7 +250,7 @@ def gen_forest(n_trees: int, depth: int, n_features: int, *, seed: int = 0,
         base_score = np.asarray(base_score, np.float32).reshape(n_outputs)
     return Ensemble(n_trees, n_features, n_outputs, off, feature, threshold,
                     left, right, leaf_value.reshape(G * w), w, tree_output,
-                    base_score, cmp, agg, post, task)
+                    base_score, cmp, agg, post, task, post_param)
 
 
 def tree_depths(e: Ensemble) -> np.ndarray:

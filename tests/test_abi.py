@@ -68,6 +68,9 @@ def test_validate_accepts_generated_and_configs():
     ("sigmoid with K=2", lambda e: (setattr(e, "n_outputs", 2), setattr(e, "post", 1)), 2),
     ("GT cmp", lambda e: setattr(e, "cmp", 2), 3),
     ("classification identity K=1", lambda e: setattr(e, "task", 1), 2),
+    ("isolation without c(psi)", lambda e: (setattr(e, "post", 3), setattr(e, "agg", 1)), 2),
+    ("isolation K=2", lambda e: (setattr(e, "post", 3), setattr(e, "post_param", 8.0),
+                                 setattr(e, "n_outputs", 2)), 2),
 ])
 def test_validate_rejects(what, mut, status):
     from paper_2010_04804_b200.hb import validate, HBError

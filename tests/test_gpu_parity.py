@@ -350,11 +350,11 @@ def test_auto_strategy_selection(monkeypatch):
         e = synth.gen_forest(4, D, 8, seed=D, family="skinny")
         assert hb.Model(e, device=0).info["strategy_name"] == want, D
     monkeypatch.delenv("HB_GEMM_MAX_DEPTH")
-    # a wide row whose few used features fit the rank-coded PTT code tile can
-    # be forced onto PTT (rank layout = feature compaction); AUTO keeps TT
-    # there because the per-tile rank transform would dominate 4 trees
+    # a wide row with few used features: feature-selection injection
+    # shrinks the X tile to the used columns, so PTT fits (fp32 nodes under
+    # AUTO, rank-coded when forced)
     sparse = synth.gen_forest(2, 5, 2000, seed=1, family="balanced")
-    assert hb.Model(sparse, device=0).info["strategy_name"] == "tt"
+    assert hb.Model(sparse, device=0).info["strategy_name"] == "ptt"
     monkeypatch.setenv("HB_PTT_RANK", "1")
     m = hb.Model(sparse, strategy="ptt", device=0)
     assert m.info["strategy_name"] == "ptt" and m.info["node_record_bytes"] == 4
@@ -491,3 +491,37 @@ def test_c5_shard_sampled():
         assert np.array_equal(hsh[r0:r0 + 500], oracle.leaf_hash(e, Xh, *r))
     del X
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("strat", ["ptt", "tt"])
+def test_isolation_forest_parity(strat):
+    """f4: IsolationForest (Table 1) — sklearn-trained forest exported as
+    path-length leaves + MEAN + ISOLATION post; GPU against the oracle (which
+    tests/test_oracle_sklearn.py pins to sklearn's score_samples)."""
+    sk = pytest.importorskip("sklearn.ensemble")
+    from tests.test_oracle_sklearn import export_isolation_forest
+    X = synth.gen_X(9, 4000, 6)
+    iso = sk.IsolationForest(n_estimators=50, max_samples=256, random_state=1).fit(X)
+    e = export_isolation_forest(iso, 6)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd, Xh = X_pair(11, 5000, 6)
+    check_all(e, m, Xd, Xh, kinds=("predict", "raw", "margin", "leaf"))
+    got = m.predict(Xd).cpu().numpy()[:, 0]
+    assert np.allclose(got, -iso.score_samples(Xh), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("strat,rank", [("ptt", "0"), ("ptt", "1"), ("tt", "0")])
+@pytest.mark.parametrize("small", ["0", "4096"])
+def test_feature_selection_injection(strat, rank, small, monkeypatch):
+    """f3: a model using 40 of 3000 features; node ids are remapped to
+    the used set and X tiles hold only those columns — on every scorer,
+    including the small-batch kernel, with an unaligned ldx."""
+    monkeypatch.setenv("HB_PTT_RANK", rank)
+    monkeypatch.setenv("HB_SMALL_BATCH", small)
+    used = np.sort(np.random.default_rng(5).choice(3000, 40, replace=False))
+    e = synth.gen_forest(30, 6, 3000, seed=8, family="mixed", features=used,
+                         post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
+    m = hb.Model(e, strategy=strat, device=0)
+    assert m.info["strategy_name"] == strat
+    Xd, Xh = X_pair(6, 1500, 3000, ldx=3001, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)

@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 sk = pytest.importorskip("sklearn")
-from sklearn.ensemble import GradientBoostingRegressor, RandomForestClassifier  # noqa: E402
+from sklearn.ensemble import (GradientBoostingRegressor, IsolationForest,  # noqa: E402
+                              RandomForestClassifier)
 from sklearn.tree import DecisionTreeClassifier, DecisionTreeRegressor  # noqa: E402
 
 import oracle  # noqa: E402
@@ -89,3 +90,28 @@ def test_regression_tree_apply_with_ties():
     e = export([dt], 3, [lambda tr: tr.value[:, 0, :]])
     Xt = synth.gen_X(8, 3000, 3, grid=synth.GRID_COARSE)
     assert np.array_equal(oracle.leaf(e, Xt)[:, 0], dt.apply(Xt))
+
+
+def export_isolation_forest(iso, n_features):
+    """IsolationForest -> ABI ensemble: leaf value = path
+    length h = node depth + c(n_leaf) - 1 (sklearn _compute_score_samples),
+    agg MEAN, post ISOLATION with post_param = c(max_samples)."""
+    from sklearn.ensemble._iforest import _average_path_length
+    vals = []
+    for est in iso.estimators_:
+        tr = est.tree_
+        h = tr.compute_node_depths() + _average_path_length(tr.n_node_samples) - 1.0
+        vals.append(lambda tr, h=h: h[:, None])
+    c = float(_average_path_length([iso._max_samples])[0])
+    return export(iso.estimators_, n_features, vals, agg=synth.AGG_MEAN,
+                  post=synth.POST_ISOLATION, post_param=c)
+
+
+def test_isolation_forest_score_samples():
+    X = synth.gen_X(9, 2000, 5)
+    iso = IsolationForest(n_estimators=25, max_samples=256, random_state=0).fit(X)
+    e = export_isolation_forest(iso, 5)
+    Xt = synth.gen_X(10, 3000, 5)
+    Xt[:50] *= 40.0                                   # some clear outliers
+    s = oracle.scores(e, Xt)
+    assert np.allclose(s["post"][:, 0], -iso.score_samples(Xt), rtol=1e-6, atol=1e-6)
