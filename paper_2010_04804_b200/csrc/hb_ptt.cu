@@ -172,8 +172,7 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);
+      dev::release_stage(&empty[s], lane);
     }
     if (row < p.n) {
       if (lm == 2) {

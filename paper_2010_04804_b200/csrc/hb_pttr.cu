@@ -375,8 +375,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
             }
         }
       }
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);
+      dev::release_stage(&empty[s], lane);
     }
 
     float acc[NACC];
@@ -450,8 +449,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[s]);
+      dev::release_stage(&empty[s], lane);
     }
     if (row < p.n) {
       if (lm == 2) {

@@ -171,8 +171,7 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
         }
       }
       if (p.t_smem) {
-        __syncwarp();
-        if (lane == 0) dev::mbar_arrive(&empty[s]);
+        dev::release_stage(&empty[s], lane);
         ring.next();
       }
     }

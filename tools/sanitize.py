@@ -1,0 +1,40 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck /
+racecheck / synccheck / initcheck):
+
+    compute-sanitizer --tool racecheck python tools/sanitize.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import synth.dev  # noqa: E402
+import paper_2010_04804_b200 as hb  # noqa: E402
+
+cases = [
+    ("ptt-rank", synth.gen_forest(40, 6, 12, seed=1), {"HB_PTT_RANK": "1"}, "ptt"),
+    ("ptt-fp32", synth.gen_forest(40, 6, 12, seed=1), {"HB_PTT_RANK": "0"}, "ptt"),
+    ("tt", synth.gen_forest(24, 11, 12, seed=2, family="mixed"), {}, "tt"),
+    ("tt-wide", synth.gen_forest(24, 11, 12, seed=2, family="mixed"), {"HB_TT_WIDE": "1"}, "tt"),
+    ("ptt-rank-wrap", synth.gen_forest(300, 8, 12, seed=4), {"HB_PTT_RANK": "1", "HB_CH": "8"}, "ptt"),
+    ("ptt-fp32-wrap", synth.gen_forest(300, 8, 12, seed=4), {"HB_PTT_RANK": "0", "HB_CH": "8"}, "ptt"),
+    ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
+    ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
+]
+for name, e, env, strat in cases:
+    os.environ.update(env)
+    for n, small in ((3000, "0"), (40, "4096")):
+        os.environ["HB_SMALL_BATCH"] = small
+        m = hb.Model(e, strategy=strat, device=0)
+        X = synth.dev.gen_X_device(7, n, 12)
+        for kind in ("predict", "raw", "leaf", "leaf_hash"):
+            m.run(X, kind)
+        torch.cuda.synchronize()
+        m.free()
+    for k in env:
+        os.environ.pop(k)
+    print("ok", name, flush=True)
