@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--shard", default=None, choices=["rows", "trees"],
                     help="default: trees for C5, rows otherwise")
+    ap.add_argument("--emulate-gpus", type=int, default=0,
+                    help="trees mode on 1 GPU: score only rank 0's tree shard of an "
+                         "N-GPU run (the per-GPU piece of C5 on 8 GPUs)")
     return ap.parse_args()
 
 
@@ -209,7 +212,8 @@ def run_ours(args):
     else:
         # trees sharded, all rows on every rank; one NCCL reduce of fp32
         # partials to rank 0, which finalizes (strong scaling)
-        t0, t1 = tree_shard(e.n_trees, rank, world, e.n_outputs, e.leaf_width)
+        t0, t1 = tree_shard(e.n_trees, rank, max(world, args.emulate_gpus), e.n_outputs,
+                            e.leaf_width)
         m = hb.Model(e, strategy=args.strategy, device=local, tree_range=(t0, t1))
         X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, device=local)
         raw = torch.empty((n, e.n_outputs), dtype=torch.float32, device=X.device)

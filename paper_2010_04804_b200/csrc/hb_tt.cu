@@ -194,71 +194,88 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // parallelism) and the walk stops early once every lane of the warp sits on a
 // leaf (the self-loop makes further iterations no-ops). Per-row sums
 // are combined with warp shuffles and one SMEM pass in a fixed order.
+// X tile swizzle: row rr of feature f sits at f*R + (rr ^ h(f)), h(f) =
+// (f >> log2(32/R)) & (R-1), so a warp storing 32 consecutive features of one
+// row hits 32 distinct banks (the plain f*R + rr layout is R-way conflicted).
+template <int R>
+__device__ __forceinline__ int xw_swz(int f) {
+  constexpr int S = R == 32 ? 0 : (R == 16 ? 1 : 2);
+  return (f >> S) & (R - 1);
+}
+
+template <bool LE, int R>
+__device__ __forceinline__ void wide_step(const uint2 *n, uint32_t &i, const float *xs, int r,
+                                          bool &done) {
+  const uint2 d = __ldg(n + i);
+  const int f = (int)(d.x & 0xFFFFu);
+  const float x = xs[f * R + (r ^ xw_swz<R>(f))];
+  const float t = __uint_as_float(d.y);
+  const bool pr = LE ? (x <= t) : (x < t);
+  const uint32_t nx = (d.x >> 16) - (pr ? 1u : 0u);
+  done = done && (nx == i);
+  i = nx;
+}
+
 template <bool LE, int NACC, int R>
 __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int L = 32 / R;                       // tree slots per warp
+  constexpr int G = 4;                            // trees walked at once per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int sub = lane / R, r = lane % R;
-  float *xs = reinterpret_cast<float *>(smem);                       // [F][R]
+  float *xs = reinterpret_cast<float *>(smem);                       // [F][R] swizzled
   float *red = xs + (size_t)p.F * R;                                 // [nwarps][R][NACC]
   uint64_t *hred = reinterpret_cast<uint64_t *>(red + (size_t)nwarps * R * NACC);  // [nwarps][R]
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   const int slots = nwarps * L;
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row0 = (int64_t)tile * R;
-    // cooperative, coalesced X tile load (row-major global -> feature-major SMEM)
+    // coalesced X tile load: consecutive threads -> consecutive features of a row
     for (int idx = threadIdx.x; idx < R * p.F; idx += blockDim.x) {
       const int rr = idx / p.F, f = idx - rr * p.F;
       const int64_t gr = row0 + rr;
       const int fo = p.fmap ? __ldg(p.fmap + f) : f;
-      xs[f * R + rr] = gr < p.n ? __ldg(p.X + gr * p.ldx + fo) : 0.f;
+      xs[f * R + (rr ^ xw_swz<R>(f))] = gr < p.n ? __ldg(p.X + gr * p.ldx + fo) : 0.f;
     }
     __syncthreads();
     const int64_t row = row0 + r;
-    const float *xr = xs + r;
     float acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
     uint64_t h = 0;
-    for (int t0 = warp * L + sub; t0 < p.n_trees_pad; t0 += 2 * slots) {
-      const int t1 = t0 + slots;
-      const bool two = t1 < p.n_trees_pad;
-      const uint8_t *ra = p.trees + (size_t)t0 * p.stride;
-      const uint8_t *rb = p.trees + (size_t)(two ? t1 : t0) * p.stride;
-      const uint2 *na = reinterpret_cast<const uint2 *>(ra + 16);
-      const uint2 *nb = reinterpret_cast<const uint2 *>(rb + 16);
-      uint32_t ia = 0, ib = 0;
-      for (int l = 0; l < p.depth; ++l) {
-        const uint2 da = __ldg(na + ia);
-        const uint2 db = __ldg(nb + ib);
-        const float xa = xr[(da.x & 0xFFFFu) * R];
-        const float xb = xr[(db.x & 0xFFFFu) * R];
-        const float ta = __uint_as_float(da.y), tb = __uint_as_float(db.y);
-        const bool pa = LE ? (xa <= ta) : (xa < ta);
-        const bool pb = LE ? (xb <= tb) : (xb < tb);
-        const uint32_t na_i = (da.x >> 16) - (pa ? 1u : 0u);
-        const uint32_t nb_i = (db.x >> 16) - (pb ? 1u : 0u);
-        const bool done = (na_i == ia) && (nb_i == ib);   // both on a self-looping leaf
-        ia = na_i;
-        ib = nb_i;
-        if (__all_sync(0xFFFFFFFFu, done)) break;
-      }
-      const float *la = reinterpret_cast<const float *>(na + p.nslots);
-      const float *lb = reinterpret_cast<const float *>(nb + p.nslots);
+    // warp-uniform loop over groups of G tree slots (t = base + sub + g*slots)
+    for (int base = warp * L; base < p.n_trees_pad; base += G * slots) {
+      const uint8_t *rec[G];
+      const uint2 *nd[G];
+      uint32_t idx[G];
+      bool valid[G];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (q == 1 && !two) break;
-        const uint8_t *rec = q ? rb : ra;
-        const float *lv = q ? lb : la;
-        const uint32_t leaf = q ? ib : ia;
+      for (int g = 0; g < G; ++g) {
+        const int t = base + sub + g * slots;
+        valid[g] = t < p.n_trees_pad;               // uniform across the warp
+        rec[g] = p.trees + (size_t)(valid[g] ? t : base + sub) * p.stride;
+        nd[g] = reinterpret_cast<const uint2 *>(rec[g] + 16);
+        idx[g] = 0;
+      }
+      for (int l = 0; l < p.depth; ++l) {
+        bool done = true;
+#pragma unroll
+        for (int g = 0; g < G; ++g) wide_step<LE, R>(nd[g], idx[g], xs, r, done);
+        if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (!valid[g]) continue;
+        const int t = base + sub + g * slots;
+        const float *lv = reinterpret_cast<const float *>(nd[g] + p.nslots);
+        const uint32_t leaf = idx[g];
         if (p.w == 1) {
           const float v = __ldg(lv + leaf);
           if (NACC == 1) {
             acc[0] += v;
           } else {
-            const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rec));
+            const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rec[g]));
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
               if (k0 == (uint32_t)k) acc[k] += v;
@@ -268,15 +285,12 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
           for (int k = 0; k < NACC; ++k)
             if (k < p.K) acc[k] += __ldg(lv + leaf * p.w + k);
         }
-        if (lm) {
-          const int t = q ? t1 : t0;
-          if (t < p.n_trees) {
-            const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
-            if (lm == 1) {
-              if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
-            } else {
-              h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
-            }
+        if (lm && t < p.n_trees) {
+          const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
+          if (lm == 1) {
+            if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+          } else {
+            h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
           }
         }
       }
