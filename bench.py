@@ -60,6 +60,9 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run every rank on one device (multi-rank code path on a 1-GPU box)
+    if os.environ.get("HB_BENCH_ONE_DEVICE"):
+        local = 0
     return rank, world, local
 
 
@@ -184,7 +187,11 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HB_BENCH_BACKEND", "nccl")   # gloo: 1-GPU multi-rank test
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2010_04804_b200 as hb
     import synth

@@ -40,6 +40,11 @@ def reduce_partials(partial, dst: int = 0, group=None):
     """Sum the [n, K] raw partials of all ranks into `partial` on rank `dst`
     (one torch.distributed.reduce; NCCL for CUDA tensors, gloo for CPU)."""
     import torch.distributed as dist
+    if partial.is_cuda and dist.get_backend(group) == "gloo":   # 1-GPU multi-rank tests
+        host = partial.cpu()
+        dist.reduce(host, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        partial.copy_(host)
+        return partial
     dist.reduce(partial, dst=dst, op=dist.ReduceOp.SUM, group=group)
     return partial
 
@@ -48,6 +53,8 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     """Max of a per-rank scalar (the timing rule: max over ranks)."""
     import torch
     import torch.distributed as dist
+    if dist.get_backend(group) == "gloo":
+        device = None
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
