@@ -525,3 +525,90 @@ def test_feature_selection_injection(strat, rank, small, monkeypatch):
     assert m.info["strategy_name"] == strat
     Xd, Xh = X_pair(6, 1500, 3000, ldx=3001, special_q24=SPECIAL_Q24)
     check_all(e, m, Xd, Xh)
+
+
+def _chain_tree(depth, F, seed, left_chain=True):
+    """A degenerate 'chain' tree of the given depth (worst case for perfect
+    padding): every internal node has one leaf child."""
+    rng = np.random.default_rng(seed)
+    feat, thr, L, R, val = [], [], [], [], []
+    nid = 0
+    for d in range(depth):
+        i = nid
+        feat.append(int(rng.integers(0, F)))
+        thr.append(np.float32(rng.integers(-32, 32) / 4.0))
+        L.append(-2); R.append(-2); val.append(np.nan)
+        nid += 1
+        leaf = nid
+        feat.append(-1); thr.append(np.nan); L.append(-1); R.append(-1)
+        val.append(np.float32(rng.normal()))
+        nid += 1
+        nxt = nid
+        if left_chain:
+            L[i], R[i] = nxt, leaf
+        else:
+            L[i], R[i] = leaf, nxt
+    feat.append(-1); thr.append(np.nan); L.append(-1); R.append(-1); val.append(np.float32(rng.normal()))
+    return dict(feature=feat, threshold=thr, left=L, right=R, leaf_value=val)
+
+
+@pytest.mark.parametrize("strat,depth", [("ptt", 10), ("tt", 10), ("tt", 24), ("tt", 40)])
+@pytest.mark.parametrize("small", ["0", "4096"])
+def test_chain_trees(strat, depth, small, monkeypatch):
+    """Chain trees: PTT pads a depth-10 chain to a perfect tree (1023 nodes);
+    TT walks depth-40 chains with its self-loop; mixed with bushy trees."""
+    monkeypatch.setenv("HB_SMALL_BATCH", small)
+    F = 6
+    trees = [_chain_tree(depth, F, s, left_chain=s % 2 == 0) for s in range(7)]
+    bushy = synth.gen_forest(5, min(depth, 8), F, seed=2, family="balanced", grid=synth.GRID_COARSE)
+    trees += [dict(feature=t["feature"], threshold=t["threshold"], left=t["left"], right=t["right"],
+                   leaf_value=t["leaf_value"]) for t in (bushy.tree(i) for i in range(5))]
+    e = synth.from_trees(trees, F, cmp=1)
+    m = hb.Model(e, strategy=strat, device=0)
+    assert m.info["max_depth"] == depth
+    Xd, Xh = X_pair(3, 2500, F, grid=synth.GRID_COARSE, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh, kinds=("predict", "raw", "leaf", "leaf_hash"))
+
+
+@pytest.mark.parametrize("strat", ["ptt", "tt", "gemm"])
+@pytest.mark.parametrize("small", ["0", "4096"])
+def test_sixteen_outputs_vector_leaves(strat, small, monkeypatch):
+    """K = 16 (the NACC = 16 kernels) with vector leaves and MEAN."""
+    monkeypatch.setenv("HB_SMALL_BATCH", small)
+    e = synth.gen_forest(21, 3 if strat == "gemm" else 7, 9, seed=4, family="mixed",
+                         n_outputs=16, leaf_width=16, leaf_kind="dirichlet",
+                         agg=synth.AGG_MEAN, task=synth.TASK_CLASSIFICATION)
+    m = hb.Model(e, strategy=strat, device=0)
+    Xd, Xh = X_pair(5, 1200, 9)
+    check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("D", [1, 2, 9, 10])
+@pytest.mark.parametrize("rank", ["0", "1"])
+def test_ptt_depth_range(D, rank, monkeypatch):
+    monkeypatch.setenv("HB_PTT_RANK", rank)
+    e = synth.gen_forest(13, D, 10, seed=D, family="skinny", post=synth.POST_SIGMOID,
+                         task=synth.TASK_CLASSIFICATION, base_score=[0.125])
+    m = hb.Model(e, strategy="ptt", device=0)
+    Xd, Xh = X_pair(D, 3000, 10, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+
+
+def test_single_tree_models_every_strategy():
+    e = synth.gen_forest(1, 3, 4, seed=1, family="balanced")
+    Xd, Xh = X_pair(1, 2000, 4)
+    for strat in ("ptt", "tt", "gemm"):
+        check_all(e, hb.Model(e, strategy=strat, device=0), Xd, Xh, kinds=("raw", "leaf"))
+
+
+def test_leaf_values_extreme_magnitudes():
+    """fp32 accumulation against fp64 within the R23 tolerance when leaf values
+    span large magnitudes with cancellation (GBDT-like margins)."""
+    e = synth.gen_forest(200, 6, 8, seed=9, family="balanced", leaf_sigma=50.0)
+    m = hb.Model(e, device=0)
+    Xd, Xh = X_pair(9, 3000, 8)
+    s = oracle.scores(e, Xh)
+    got = m.predict_raw(Xd).cpu().numpy().astype(np.float64)
+    # fp32 sum of 200 terms |v| ~ 50: error bound ~ 200 * 2^-24 * sum|v|
+    bound = 200 * 2.0 ** -24 * np.abs(s["raw"]).max() * 200
+    assert np.abs(got - s["raw"]).max() <= max(bound, 1e-3)
