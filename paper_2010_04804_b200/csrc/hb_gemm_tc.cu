@@ -89,6 +89,23 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
   const TcGeom g = tc_geom(w);
   const int T = t1 - t0;
   const int ngroups = (T + kTcTrees - 1) / kTcTrees;
+  // feature-selection injection: the X tile holds used features only
+  std::vector<int32_t> remap(e->n_features, -1), used;
+  for (int t = t0; t < t1; ++t)
+    for (int64_t i = e->node_offset[t]; i < e->node_offset[t + 1]; ++i)
+      if (e->left[i] != -1) remap[e->feature[i]] = 1;
+  for (int f = 0; f < e->n_features; ++f)
+    if (remap[f] == 1) {
+      remap[f] = (int32_t)used.size();
+      used.push_back(f);
+    }
+  if (used.empty()) used.push_back(0), remap[0] = 0;
+  // X slices of 4 warps in SMEM when the used columns fit (else X is read
+  // from global with original feature ids)
+  const bool fits = 4L * (long)used.size() * 128 <= 160L * 1024;
+  const bool compact = fits && (int)used.size() < e->n_features;
+  if (!compact)
+    for (int f = 0; f < e->n_features; ++f) remap[f] = f;
   std::vector<uint8_t> buf((size_t)ngroups * g.stride, 0);
   std::vector<int32_t> leafmap((size_t)ngroups * kTcTrees * 8, -1);
   std::vector<int> ipos, lpos, stack;
@@ -123,7 +140,7 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
       }
       for (int i = 0; i < n; ++i) {
         if (ipos[i] >= 0) {
-          feat[q * 8 + ipos[i]] = (uint32_t)e->feature[a + i];
+          feat[q * 8 + ipos[i]] = (uint32_t)remap[e->feature[a + i]];
           thr[q * 8 + ipos[i]] = e->threshold[a + i];
         } else {
           for (int k = 0; k < w; ++k)
@@ -172,10 +189,17 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
   m->device_bytes += leafmap.size() * 4;
   err = cudaMemcpy(m->d_leafmap, leafmap.data(), leafmap.size() * 4, cudaMemcpyHostToDevice);
   if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm_tc leafmap)");
-  const long xb = 4L * e->n_features * 128;
+  if (compact) {
+    if ((err = cudaMalloc(&m->d_fmap, used.size() * 4)) != cudaSuccess) return cuda_fail(err, "cudaMalloc(fmap)");
+    m->device_bytes += used.size() * 4;
+    if ((err = cudaMemcpy(m->d_fmap, used.data(), used.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(err, "cudaMemcpy(fmap)");
+  }
+  m->n_xf = compact ? (int)used.size() : e->n_features;
+  const long xb = 4L * m->n_xf * 128;
   m->cfg = LaunchCfg();
   m->cfg.nw = 4;
-  m->cfg.x_smem = xb <= 64 * 1024 ? 1 : 0;
+  m->cfg.x_smem = fits ? 1 : 0;
   m->cfg.t_smem = 1;
   m->cfg.smem_bytes = (int)((m->cfg.x_smem ? xb : 0) + 2 * g.stride + kTcRows * 16 * 2 * kTcPairs + 64);
   // 4 warps per CTA: fill the SM with up to 4 CTAs (TMEM: 4 x 128 columns = 512)
@@ -233,6 +257,7 @@ struct TcParams {
   const float *X;
   int64_t n, ldx;
   int F, vec4, x_smem;
+  const int32_t *fmap;   // compact X column -> original feature, or null
   const uint8_t *groups;
   uint32_t stride, off_feat, off_thr, off_d, off_tout, off_e;
   int ngroups, n_trees, tree_begin;
@@ -290,7 +315,8 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
     const float *xrow;
     int xstride;
     if (p.x_smem) {
-      dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+      if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
+      else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
       xrow = xs + lane;
       xstride = 32;
     } else {
@@ -433,9 +459,10 @@ hb_status launch_gemm_tc(const Model &m, const RunArgs &a) {
   p.X = a.X;
   p.n = a.n;
   p.ldx = a.ldx;
-  p.F = m.n_features;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   p.x_smem = m.cfg.x_smem;
+  p.F = m.n_xf;
+  p.fmap = m.d_fmap;
   p.groups = static_cast<const uint8_t *>(m.d_trees);
   p.stride = (uint32_t)g.stride;
   p.off_feat = (uint32_t)g.off_feat;
