@@ -142,9 +142,10 @@ def run_reference(args):
                 break
     except OSError:
         pass
-    # size each step for ~4 s of CPU work
-    rate0, used, _, _ = time_oracle(e, cfg, budget_s=1.0)
-    rows = int(min(cfg.n_rows, max(1000, rate0 * 4.0)))
+    # size each step for ~4 s of CPU work (HB_REF_STEP_S overrides)
+    step_s = float(os.environ.get("HB_REF_STEP_S", "4.0"))
+    rate0, used, _, _ = time_oracle(e, cfg, budget_s=min(1.0, step_s))
+    rows = int(min(cfg.n_rows, max(100, rate0 * step_s)))
     import oracle
     X = synth.gen_X(cfg.seed_x, rows, cfg.n_features)
     for _ in range(args.warmup):
