@@ -91,6 +91,23 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
+// Warm L2 with the X rows of a CTA's next row tile (TMA bulk prefetch, no
+// SMEM, no completion tracking); [first, first + rows) rows of stride ldx.
+__device__ __forceinline__ void prefetch_rows_l2(const float *X, int64_t first, int64_t rows,
+                                                 int64_t n, int64_t ldx) {
+  if (first >= n) return;
+  rows = min(rows, n - first);
+  const char *a = reinterpret_cast<const char *>(X + first * ldx);
+  const char *b = reinterpret_cast<const char *>(X + (first + rows) * ldx);
+  const char *p = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15));
+  while (p < b) {
+    const int64_t left = ((int64_t)(b - p) + 15) & ~int64_t(15);
+    const uint32_t bytes = (uint32_t)(left < 65536 ? left : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+    p += bytes;
+  }
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;

@@ -531,6 +531,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     }
   }
   m->strategy = strat;
+  m->cfg.prefetch = env_int("HB_PREFETCH", 1);
 
   // small-batch path: reuse the PTT fp32 / TT records, else build PTT fp32 ones
   m->sb_nxf = m->n_features;

@@ -29,6 +29,7 @@ struct LaunchCfg {
   int ctas_per_sm = 1;
   int wide_rows = 0;    // TT only: >0 selects tt_wide_kernel with this many rows per CTA
   int stage_bytes = 0;  // PTT rank layout: bytes per ring stage
+  int prefetch = 1;     // producer warms L2 with the next tile's X rows
 };
 
 struct Model {

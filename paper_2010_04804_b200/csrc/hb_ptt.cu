@@ -38,6 +38,7 @@ struct PttParams {
   int K, w, task, post, kind;
   void *out;
   int nw, ns, ch, ntiles;
+  int prefetch;           // L2 prefetch of the next tile's X rows
 };
 
 template <int D, bool LE, int NACC, int G>
@@ -71,6 +72,12 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
       for (long it = 0; it < total; ++it, r.next(), c = (c + 1 == nchunks) ? 0 : c + 1) {
         const int s = r.s;
         dev::mbar_wait(&empty[s], r.ph ^ 1u);
+        if (c == 0 && p.prefetch) {
+          // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
+          const long tile_i = it / nchunks;
+          const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32);
+          dev::prefetch_rows_l2(p.X, next, (int64_t)nw * 32, p.n, p.ldx);
+        }
         const int t0 = c * ch;
         const int nt = min(ch, p.n_trees_pad - t0);
         const uint32_t bytes = (uint32_t)nt * p.stride;
@@ -245,6 +252,7 @@ hb_status launch_ptt(const Model &m, const RunArgs &a) {
   p.post = m.post;
   p.kind = a.kind;
   p.out = a.out;
+  p.prefetch = m.cfg.prefetch;
   p.nw = m.cfg.nw;
   p.ns = m.cfg.ns;
   p.ch = m.cfg.ch;

@@ -266,6 +266,7 @@ struct PttrParams {
   int K, w, task, post, kind;
   void *out;
   int nw, ns, ch, ntiles;
+  int prefetch;           // L2 prefetch of the next tile's X rows
   uint32_t stage_bytes;
 };
 
@@ -298,6 +299,12 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
       for (long it = 0; it < total; ++it, r.next(), q = (q + 1 == items) ? 0 : q + 1) {
         const int s = r.s;
         dev::mbar_wait(&empty[s], r.ph ^ 1u);
+        if (q == 0 && p.prefetch) {
+          // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
+          const long tile_i = it / items;
+          const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32);
+          dev::prefetch_rows_l2(p.X, next, (int64_t)nw * 32, p.n, p.ldx);
+        }
         const uint8_t *src;
         uint32_t bytes;
         if (q < p.n_groups) {
@@ -528,6 +535,7 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   p.post = m.post;
   p.kind = a.kind;
   p.out = a.out;
+  p.prefetch = m.cfg.prefetch;
   p.nw = m.cfg.nw;
   p.ns = m.cfg.ns;
   p.ch = m.cfg.ch;
