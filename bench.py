@@ -281,8 +281,13 @@ def run_ours(args):
     D = info["max_depth"]
     w = info["leaf_width"]
     # per (row, tree) and level one 8-B node record + one 4-B X
-    # value; per tree one leaf of 4w B (PTT: D levels by construction).
-    per_row = (t1 - t0) * (D * 12 + 4 * w)
+    # value; per tree one leaf of 4w B. PTT walks D levels by construction; TT
+    # is credited only the levels it actually traverses (mean root->leaf path
+    # length of the reached leaves, measured on a sample of rows).
+    levels = float(D)
+    if info["strategy_name"] == "tt":
+        levels = mean_path_length(m, e, X[: min(n, 2048)], t0, t1)
+    per_row = (t1 - t0) * (levels * 12 + 4 * w)
     achieved = per_row * n / (kern_ms * 1e-3) / 1e9
     peaks = {}
     if rank == 0:
@@ -295,8 +300,7 @@ def run_ours(args):
     smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
     layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "")
     prof = load_profile(args.config, layout)
-    kname = {"ptt": "ptt_kernel", "ptt-rank": "pttr_kernel", "gemm": "gemm_tc_kernel" if info.get("tensor_cores") else "gemm_kernel",
-             "tt": "tt_wide_kernel" if info.get("x_in_smem") and cfg.n_features > 1000 else "tt_kernel"}.get(layout, layout)
+    kname = info["kernel_name"]
     hbm_bytes = n * (cfg.n_features * 4 + (8 if (cls and e.n_outputs == 1) else 4 * e.n_outputs))
     measured = {}
     try:
@@ -304,15 +308,21 @@ def run_ours(args):
     except OSError:
         pass
     hbm_peak = measured.get("hbm_gbs", 6650.0)
+    # nodes staged in SMEM (PTT, narrow TT) -> SMEM roof; tt_wide_kernel reads
+    # node records through L1/L2 -> the measured L2 read roof
+    l2_wide = info["strategy_name"] == "tt" and kname == "tt_wide_kernel"
+    bound, peak = ("l2", peaks.get("l2_gbs") or 12000.0) if l2_wide else ("smem", smem_peak)
     roofline = {
-        "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-        "frac": achieved / smem_peak,
+        "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "mean_levels_per_tree": levels,
         "traffic": prof.get("smem_ld_bytes_per_launch") if prof.get("rows") == n else None,
         "traffic_dram": prof.get("dram_bytes_per_launch") if prof.get("rows") == n else None,
         "traffic_source": prof.get("source"),
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
         "algorithmic_bytes_per_row": per_row,
-        "peak_source": "measured LDS.128 microbenchmark (tools/peaks.cu), this run" if peaks.get("smem_gbs")
+        "peak_source": ("measured L2 read microbenchmark (tools/peaks.cu), this run" if l2_wide else
+                        "measured LDS.128 microbenchmark (tools/peaks.cu), this run")
+        if (peaks.get("l2_gbs") if l2_wide else peaks.get("smem_gbs"))
         else "spec 148 SM x 128 B/clk x 1.965 GHz",
         "smem_peak_spec_gbs": 148 * 128 * 1.965,
         "l2_peak_gbs": peaks.get("l2_gbs"),
@@ -367,6 +377,25 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def mean_path_length(m, e, X, t0, t1):
+    """Mean number of levels the walk traverses per (row, tree): leaf depth of
+    the reached leaf (leaf ids from the device, depths from the tree arrays)."""
+    import numpy as np
+    leaf = m.predict_leaf(X).cpu().numpy()
+    tot = 0.0
+    for j, t in enumerate(range(t0, t1)):
+        a, b = int(e.node_offset[t]), int(e.node_offset[t + 1])
+        L, R = e.left[a:b], e.right[a:b]
+        depth = np.zeros(b - a, np.int32)
+        order = [0]
+        for i in order:
+            if L[i] >= 0:
+                depth[L[i]] = depth[R[i]] = depth[i] + 1
+                order += [int(L[i]), int(R[i])]
+        tot += depth[leaf[:, j]].mean()
+    return tot / max(1, t1 - t0)
 
 
 def load_profile(config, strat):

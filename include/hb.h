@@ -143,6 +143,9 @@ typedef struct {
   int64_t tree_stride_bytes;    /* bytes per tree in the compiled layout       */
   int32_t tensor_cores;         /* 1 if the scorer runs tcgen05 MMAs (GEMM)    */
   int32_t node_record_bytes;    /* PTT/TT node record size (4 = rank-coded PTT) */
+  int32_t kernel;               /* row-tile scorer: 0 ptt, 1 ptt rank-coded, 2 tt, 3 tt wide-row,
+                                   4 gemm tcgen05, 5 gemm CUDA-core (small batches: hb_small) */
+  int32_t rows_per_cta;         /* rows one CTA owns per tile                   */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the

@@ -821,6 +821,11 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->tree_stride_bytes = (int64_t)m.stride;
   info->tensor_cores = m.gemm_tc;
   info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : (m.ptt_rank ? 4 : 8);
+  if (m.strategy == HB_STRATEGY_PTT) info->kernel = m.ptt_rank ? 1 : 0;
+  else if (m.strategy == HB_STRATEGY_TT) info->kernel = m.cfg.wide_rows ? 3 : 2;
+  else info->kernel = m.gemm_tc ? 4 : 5;
+  info->rows_per_cta = m.strategy == HB_STRATEGY_GEMM ? (m.gemm_tc ? 128 : 128)
+                       : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);
   return HB_OK;
 }
 

@@ -15,6 +15,8 @@ POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX, POST_ISOLATION = 0, 1, 2, 3
 TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
 STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
+KERNEL_NAME = {0: "ptt_kernel", 1: "pttr_kernel", 2: "tt_kernel", 3: "tt_wide_kernel",
+               4: "gemm_tc_kernel", 5: "gemm_kernel"}
 OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5}
 
 # every symbol include/hb.h declares (checked by tests/test_abi.py)
@@ -46,7 +48,8 @@ class _Info(C.Structure):
                 ("n_features", C.c_int32), ("n_outputs", C.c_int32),
                 ("leaf_width", C.c_int32), ("device", C.c_int32), ("x_in_smem", C.c_int32),
                 ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64),
-                ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32)]
+                ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32),
+                ("kernel", C.c_int32), ("rows_per_cta", C.c_int32)]
 
 
 def _load():
@@ -136,6 +139,7 @@ class Model:
         _check(lib.hb_model_get_info(self._p, C.byref(i)))
         d = {k: getattr(i, k) for k, _ in _Info._fields_}
         d["strategy_name"] = STRATEGY_NAME[d["strategy"]]
+        d["kernel_name"] = KERNEL_NAME.get(d["kernel"], "?")
         return d
 
     def free(self):
