@@ -826,6 +826,8 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   else info->kernel = m.gemm_tc ? 4 : 5;
   info->rows_per_cta = m.strategy == HB_STRATEGY_GEMM ? (m.gemm_tc ? 128 : 128)
                        : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);
+  info->code_cell_bits = m.ptt_rank ? m.rank_cw : 0;
+  info->reserved = 0;
   return HB_OK;
 }
 

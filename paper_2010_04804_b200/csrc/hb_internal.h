@@ -60,6 +60,7 @@ struct Model {
   int gemm_tc = 0;          // 1: tensor-core (tcgen05) GEMM kernel
   // PTT with rank-coded thresholds (hb_pttr.cu)
   int ptt_rank = 0;
+  int rank_cw = 32;          // code cell width (32 or 16 bits)
   void *d_aux = nullptr;    // [fmeta | groups | eytzinger pool]
   size_t aux_groups_off = 0, aux_pool_off = 0;
   int rank_nfc = 0, rank_ngroups = 0;

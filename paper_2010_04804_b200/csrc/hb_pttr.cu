@@ -38,8 +38,8 @@
 #include <cstring>
 #include <vector>
 
-#include "hb_device.cuh"
 #include "hb_internal.h"
+#include "hb_pttr_kernel.cuh"
 
 namespace hb {
 
@@ -100,10 +100,77 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     fc_of[f] = A.n_fc++;
     sorted.push_back(v);
   }
-  if (A.n_fc > 511) return HB_E_UNSUPPORTED;    // fc * 128 must fit 16 bits
-  // 2. tree records
+  if (A.n_fc > 1023) return HB_E_UNSUPPORTED;   // node offsets must fit 16 bits
   const int P = 1 << D;
   const size_t stride = (4 * (size_t)P + 4 * (size_t)w * P + 15) & ~size_t(15);
+  // Eytzinger search arrays (grouped later by stage size)
+  std::vector<std::vector<float>> ey(A.n_fc);
+  std::vector<int> Ls(A.n_fc);
+  for (int c = 0; c < A.n_fc; ++c) {
+    const int L = bit_length((uint32_t)sorted[c].size());
+    Ls[c] = L;
+    ey[c].assign(std::max(4, 1 << L), NAN);   // >= 16 B, slot 0 unused
+    size_t next = 0;
+    eytz_fill(sorted[c], ey[c], L, 1, next);
+    A.max_feat_bytes = std::max(A.max_feat_bytes, ey[c].size() * 4);
+  }
+  // launch configuration: X code tile NW * tile_bytes + a 2-stage ring. Every
+  // consumer warp waits for every ring item, so items should be large: the
+  // largest tree chunk that fits (<= 64 trees) for the most warps. Measured on
+  // B200: C3 24 warps x 2 stages x 32 trees = 700M rows/s vs
+  // 520M with 16-tree chunks. 32-bit cells first; 16-bit cells (half the
+  // tile, one more instruction per level) when they buy more warps.
+  const int force = env_int2("HB_PTT_RANK", -1);
+  const int force_cw = env_int2("HB_RANK_CW", 0);
+  const int force_nw = env_int2("HB_NW", 0);
+  auto try_cfg = [&](int cw, LaunchCfg &cfg) {
+    if (cw == 32 && A.n_fc > 511) return false;
+    const long tile = cw == 32 ? (long)A.n_fc * 128 : (long)((A.n_fc + 1) / 2) * 128;
+    for (int nw : {24, 16, 12, 8, 4}) {
+      if (force_nw && nw != force_nw) continue;
+      const long xb = (long)nw * tile;
+      const long rem = (long)kSmemBudget - xb;
+      const int ns = env_int2("HB_NS", 2);
+      const long per = rem / ns - 16;
+      if (per < (long)A.max_feat_bytes || per < (long)kTreeGroup * (long)stride) continue;
+      int ch = (int)std::min<long>(env_int2("HB_CH", 64), per / (long)stride) & ~(kTreeGroup - 1);
+      ch = std::min(ch, Tpad);
+      const long stage = std::max<long>((long)ch * stride, (long)A.max_feat_bytes);
+      cfg.nw = nw;
+      cfg.ns = ns;
+      cfg.ch = ch;
+      cfg.x_smem = 1;
+      cfg.t_smem = 1;
+      cfg.stage_bytes = (int)((stage + 127) & ~127L);
+      cfg.smem_bytes = (int)(xb + (long)ns * cfg.stage_bytes + 16 * ns);
+      if (cfg.smem_bytes <= kSmemBudget) return true;
+    }
+    return false;
+  };
+  LaunchCfg cfg, cfg16;
+  int cw = 32;
+  bool ok = force_cw != 16 && try_cfg(32, cfg);
+  const bool ok16 = force_cw != 32 && try_cfg(16, cfg16);
+  if (ok16 && (!ok || force_cw == 16 || cfg16.nw > cfg.nw)) {
+    cfg = cfg16;
+    cw = 16;
+    ok = true;
+  }
+  // auto (DESIGN.md §4.6): rank-coded nodes only when (a) the per-tile rank
+  // transform (sum_f L_f searches per row) stays small next to the walk it
+  // shortens (T * D levels per row) and (b) the layout runs at least as many
+  // warps as the fp32-node layout would (occupancy decides at equal bytes).
+  if (ok && force != 1) {
+    double lsum = 0;
+    for (int c = 0; c < A.n_fc; ++c) lsum += Ls[c];
+    if (lsum > 0.2 * (double)Tpad * (double)std::max(D, 1)) ok = false;
+    if (cfg.nw < nw_fp32) ok = false;
+  }
+  if (!ok) return HB_E_UNSUPPORTED;
+  // tree records: node = (cell offset) << 16 | k
+  auto cell_off = [&](int fc) -> uint32_t {
+    return cw == 32 ? (uint32_t)fc * 128u : (uint32_t)(fc >> 1) * 128u + (uint32_t)(fc & 1) * 2u;
+  };
   std::vector<uint8_t> buf((size_t)Tpad * stride, 0);
   std::vector<int32_t> leafmap((size_t)Tpad * P, -1);
   std::vector<int> orig(2 * P);
@@ -126,14 +193,13 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
         if (v == 0.f) v = 0.f;
         const std::vector<float> &u = sorted[fc_of[f]];
         const uint32_t k = (uint32_t)(std::lower_bound(u.begin(), u.end(), v) - u.begin());
-        node[p] = ((uint32_t)(fc_of[f] * 128) << 16) | k;
+        node[p] = (cell_off(fc_of[f]) << 16) | k;
         orig[2 * p] = e->left[a + o];
         orig[2 * p + 1] = e->right[a + o];
       } else {
         orig[2 * p] = orig[2 * p + 1] = o;
       }
     }
-    if (D == 0) orig[1] = 0;
     for (int p = P; p < 2 * P; ++p) {
       const int o = D == 0 ? 0 : orig[p];
       const int slot = p - P;
@@ -141,57 +207,6 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
       leafmap[(size_t)lt * P + slot] = o;
     }
   }
-  // 3. Eytzinger arrays, grouped later by stage size
-  std::vector<std::vector<float>> ey(A.n_fc);
-  std::vector<int> Ls(A.n_fc);
-  for (int c = 0; c < A.n_fc; ++c) {
-    const int L = bit_length((uint32_t)sorted[c].size());
-    Ls[c] = L;
-    ey[c].assign(std::max(4, 1 << L), NAN);   // >= 16 B, slot 0 unused
-    size_t next = 0;
-    eytz_fill(sorted[c], ey[c], L, 1, next);
-    A.max_feat_bytes = std::max(A.max_feat_bytes, ey[c].size() * 4);
-  }
-  // 4. launch configuration: X codes NW*n_fc*128 B + a 2-stage ring. Every
-  //    consumer warp waits for every ring item, so items should be large:
-  //    the largest tree chunk that fits (<= 64 trees) for the most warps.
-  //    Measured on B200: C3 24 warps x 2 stages x 32 trees =
-  //    700M rows/s vs 520M with 16-tree chunks.
-  const int force = env_int2("HB_PTT_RANK", -1);
-  LaunchCfg cfg;
-  bool ok = false;
-  const int force_nw = env_int2("HB_NW", 0);
-  for (int nw : {24, 16, 12, 8, 4}) {
-    if (force_nw && nw != force_nw) continue;
-    const long xb = (long)nw * A.n_fc * 128;
-    const long rem = (long)kSmemBudget - xb;
-    const int ns = env_int2("HB_NS", 2);
-    const long per = rem / ns - 16;
-    if (per < (long)A.max_feat_bytes || per < (long)kTreeGroup * (long)stride) continue;
-    int ch = (int)std::min<long>(env_int2("HB_CH", 64), per / (long)stride) & ~(kTreeGroup - 1);
-    ch = std::min(ch, Tpad);
-    const long stage = std::max<long>((long)ch * stride, (long)A.max_feat_bytes);
-    cfg.nw = nw;
-    cfg.ns = ns;
-    cfg.ch = ch;
-    cfg.x_smem = 1;
-    cfg.t_smem = 1;
-    cfg.stage_bytes = (int)((stage + 127) & ~127L);
-    cfg.smem_bytes = (int)(xb + (long)ns * cfg.stage_bytes + 16 * ns);
-    ok = cfg.smem_bytes <= kSmemBudget;
-    if (ok) break;
-  }
-  // auto (DESIGN.md §4.6): rank-coded nodes only when (a) the per-tile rank
-  // transform (sum_f L_f searches per row) stays small next to the walk it
-  // shortens (T * D levels per row) and (b) the layout runs at least as many
-  // warps as the fp32-node layout would (occupancy decides at equal bytes).
-  if (ok && force != 1) {
-    double lsum = 0;
-    for (int c = 0; c < A.n_fc; ++c) lsum += Ls[c];
-    if (lsum > 0.2 * (double)Tpad * (double)std::max(D, 1)) ok = false;
-    if (cfg.nw < nw_fp32) ok = false;
-  }
-  if (!ok) return HB_E_UNSUPPORTED;
   // 5. group features into stage-sized bulk copies
   {
     size_t goff = 0, gbytes = 0;
@@ -245,267 +260,15 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   m->nslots = P;
   m->cfg = cfg;
   m->ptt_rank = 1;
+  m->rank_cw = cw;
   return HB_OK;
-}
-
-// ------------------------------------------------------------------ device
-struct PttrParams {
-  const float *X;
-  int64_t n, ldx;
-  const uint8_t *trees;
-  uint32_t stride;
-  int n_trees_pad, n_trees, tree_begin;
-  const int32_t *leafmap;
-  int nslots;
-  const uint4 *fmeta;     // [n_fc] {orig f, L, offset in group, group}
-  const uint4 *groups;    // [n_groups] {pool byte offset, bytes, fc_begin, fc_end}
-  const uint8_t *pool;
-  int n_fc, n_groups;
-  int F, vec4, x_direct;  // x_direct: all F features used -> stage X into the cells, recode in place
-  const float *scale, *base;
-  int K, w, task, post, kind;
-  void *out;
-  int nw, ns, ch, ntiles;
-  int prefetch;           // L2 prefetch of the next tile's X rows
-  uint32_t stage_bytes;
-};
-
-template <int D, bool LE, int NACC, int G>
-__global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = p.nw, ns = p.ns, ch = p.ch;
-  const size_t xbytes = (size_t)nw * p.n_fc * 128;
-  uint8_t *stages = smem + xbytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(stages + (size_t)ns * p.stage_bytes);
-  uint64_t *empty = full + ns;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ns; ++s) {
-      dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], nw);
-    }
-    dev::fence_mbar_init();
-  }
-  __syncthreads();
-  const int nchunks = (p.n_trees_pad + ch - 1) / ch;
-  const int items = p.n_groups + nchunks;          // per tile: feature groups, then tree chunks
-  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-
-  if (warp == nw) {
-    if (lane == 0) {
-      const long total = (long)my_tiles * items;
-      dev::Ring r(ns);
-      int q = 0;
-      for (long it = 0; it < total; ++it, r.next(), q = (q + 1 == items) ? 0 : q + 1) {
-        const int s = r.s;
-        dev::mbar_wait(&empty[s], r.ph ^ 1u);
-        if (q == 0 && p.prefetch) {
-          // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
-          const long tile_i = it / items;
-          const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32);
-          dev::prefetch_rows_l2(p.X, next, (int64_t)nw * 32, p.n, p.ldx);
-        }
-        const uint8_t *src;
-        uint32_t bytes;
-        if (q < p.n_groups) {
-          const uint4 g = __ldg(p.groups + q);
-          src = p.pool + g.x;
-          bytes = g.y;
-        } else {
-          const int t0 = (q - p.n_groups) * ch;
-          src = p.trees + (size_t)t0 * p.stride;
-          bytes = (uint32_t)min(ch, p.n_trees_pad - t0) * p.stride;
-        }
-        dev::mbar_arrive_expect_tx(&full[s], bytes);
-        dev::bulk_g2s(stages + (size_t)s * p.stage_bytes, src, bytes, &full[s]);
-      }
-    }
-    return;
-  }
-
-  const uint32_t codes = dev::smem_u32(smem) + (uint32_t)(warp * p.n_fc * 128) + 4u * lane;
-  const uint32_t stage0 = dev::smem_u32(stages);
-  const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
-  dev::Ring ring(ns);
-  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
-    const int64_t row = wrow0 + lane;
-    const bool active = wrow0 < p.n;
-    const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
-    if (p.x_direct && active) {
-      // fp32 X slice straight into the code cells (cell(f, lane) = xs[f*32 + lane])
-      dev::load_x_slice(reinterpret_cast<float *>(smem) + (size_t)warp * p.n_fc * 32, p.X, row, p.n,
-                        p.ldx, p.F, lane, p.vec4 != 0);
-    }
-
-    // ---- rank codes of this warp's 32 rows, one feature group per stage
-    for (int gq = 0; gq < p.n_groups; ++gq, ring.next()) {
-      const int s = ring.s;
-      dev::mbar_wait(&full[s], ring.ph);
-      if (active) {
-        const uint4 g = __ldg(p.groups + gq);
-        const uint32_t gb = stage0 + (uint32_t)s * p.stage_bytes;
-        // four independent searches per lane (memory-level parallelism); the
-        // per-feature depth L is warp-uniform, so the guards do not diverge
-        for (int fc = (int)g.z; fc < (int)g.w; fc += 4) {
-          uint32_t i[4], eb[4], L[4];
-          float x[4];
-          uint32_t lmax = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const bool valid = fc + q < (int)g.w;
-            const uint4 fm = __ldg(p.fmeta + (valid ? fc + q : fc));
-            x[q] = p.x_direct ? dev::lds_f32(codes + (uint32_t)(valid ? fc + q : fc) * 128u)
-                              : __ldg(xr + fm.x);
-            eb[q] = gb + fm.z;
-            L[q] = valid ? fm.y : 0u;
-            i[q] = 1u;
-            lmax = max(lmax, L[q]);
-          }
-          for (uint32_t l = 0; l < lmax; ++l) {
-            // branch-free: finished searches re-read a valid slot and keep i
-            float u[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) u[q] = dev::lds_f32(eb[q] + (l < L[q] ? 4u * i[q] : 4u));
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const bool pr = LE ? (u[q] < x[q]) : (u[q] <= x[q]);   // u sorts before x
-              const uint32_t nx = 2u * i[q] + (pr ? 1u : 0u);
-              i[q] = l < L[q] ? nx : i[q];
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (fc + q < (int)g.w) {
-              const uint32_t code = (x[q] != x[q]) ? 0xFFFFu : i[q] - (1u << L[q]);
-              dev::sts_u32(codes + (uint32_t)(fc + q) * 128u, ((uint32_t)(fc + q) << 23) | code);
-            }
-        }
-      }
-      dev::release_stage(&empty[s], lane);
-    }
-
-    float acc[NACC];
-#pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
-    uint64_t h = 0;
-    for (int c = 0; c < nchunks; ++c, ring.next()) {
-      const int s = ring.s;
-      dev::mbar_wait(&full[s], ring.ph);
-      if (active) {
-        const uint32_t cb = stage0 + (uint32_t)s * p.stage_bytes;
-        const int nt = min(ch, p.n_trees_pad - c * ch);
-        for (int j = 0; j < nt; j += G) {
-          // a = absolute address of heap node i (tree + 4 i); next level:
-          // a' = tree + 8 i + (left ? 0 : 4) = 2 a + (left ? -tree : 4 - tree)
-          uint32_t tb[G], a[G], m0[G], m4[G];
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            tb[g] = cb + (uint32_t)(j + g) * p.stride;
-            a[g] = tb[g] + 4u;                 // heap node 1 (root), 4-B records
-            m0[g] = 0u - tb[g];
-            m4[g] = 4u - tb[g];
-          }
-#pragma unroll
-          for (int l = 0; l < D; ++l) {
-            uint32_t nd[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(a[g]);
-            uint32_t xc[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) xc[g] = dev::lds_u32(codes + (nd[g] >> 16));
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-              const bool left = nd[g] >= xc[g];           // k >= c(x)  <=>  x < u_k
-              a[g] = 2u * a[g] + (left ? m0[g] : m4[g]);
-            }
-          }
-          uint32_t off[G];
-#pragma unroll
-          for (int g = 0; g < G; ++g) off[g] = a[g] - tb[g];
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t slot = (off[g] >> 2) - (1u << D);
-            if (p.w == 1) {
-              const float v = dev::lds_f32(tb[g] + off[g]);   // leaf(slot) == byte offset 4 i
-              if (NACC == 1) {
-                acc[0] += v;
-              } else {
-                const uint32_t k0 = dev::lds_u32(tb[g]);
-#pragma unroll
-                for (int k = 0; k < NACC; ++k)
-                  if (k0 == (uint32_t)k) acc[k] += v;
-              }
-            } else {
-              const uint32_t lb = tb[g] + (4u << D) + 4u * slot * (uint32_t)p.w;
-#pragma unroll
-              for (int k = 0; k < NACC; ++k)
-                if (k < p.K) acc[k] += dev::lds_f32(lb + 4u * k);
-            }
-            if (lm) {
-              const int t = c * ch + j + g;
-              if (t < p.n_trees) {
-                const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + slot);
-                if (lm == 1) {
-                  if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
-                } else {
-                  h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
-                }
-              }
-            }
-          }
-        }
-      }
-      dev::release_stage(&empty[s], lane);
-    }
-    if (row < p.n) {
-      if (lm == 2) {
-        static_cast<uint64_t *>(p.out)[row] = h;
-      } else if (lm == 0) {
-        dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
-      }
-    }
-  }
-}
-
-using PttrFn = void (*)(const PttrParams);
-
-template <int D, bool LE>
-static PttrFn pick_nacc(int nacc) {
-  switch (nacc) {
-    case 1: return pttr_kernel<D, LE, 1, kTreeGroup>;
-    case 4: return pttr_kernel<D, LE, 4, kTreeGroup>;
-    case 8: return pttr_kernel<D, LE, 8, kTreeGroup>;
-    default: return pttr_kernel<D, LE, 16, kTreeGroup>;
-  }
-}
-
-template <int D>
-static PttrFn pick_le(bool le, int nacc) {
-  return le ? pick_nacc<D, true>(nacc) : pick_nacc<D, false>(nacc);
-}
-
-static PttrFn pick(int D, bool le, int nacc) {
-  switch (D) {
-    case 0: return pick_le<0>(le, nacc);
-    case 1: return pick_le<1>(le, nacc);
-    case 2: return pick_le<2>(le, nacc);
-    case 3: return pick_le<3>(le, nacc);
-    case 4: return pick_le<4>(le, nacc);
-    case 5: return pick_le<5>(le, nacc);
-    case 6: return pick_le<6>(le, nacc);
-    case 7: return pick_le<7>(le, nacc);
-    case 8: return pick_le<8>(le, nacc);
-    case 9: return pick_le<9>(le, nacc);
-    case 10: return pick_le<10>(le, nacc);
-    default: return nullptr;
-  }
 }
 
 int sm_count(int device);
 
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
-  PttrFn fn = pick(m.depth, m.cmp == HB_CMP_LE, m.nacc);
+  PttrFn fn = m.rank_cw == 16 ? pttr_fn16(m.depth, m.cmp == HB_CMP_LE, m.nacc)
+                              : pttr_fn32(m.depth, m.cmp == HB_CMP_LE, m.nacc);
   if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
   PttrParams p;
   p.X = a.X;
@@ -526,7 +289,7 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   p.n_groups = m.rank_ngroups;
   p.F = m.n_features;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
-  p.x_direct = m.rank_nfc == m.n_features;
+  p.x_direct = m.rank_cw == 32 && m.rank_nfc == m.n_features;
   p.scale = m.d_scale;
   p.base = m.d_base;
   p.K = m.n_outputs;

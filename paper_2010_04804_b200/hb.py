@@ -49,7 +49,8 @@ class _Info(C.Structure):
                 ("leaf_width", C.c_int32), ("device", C.c_int32), ("x_in_smem", C.c_int32),
                 ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64),
                 ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32),
-                ("kernel", C.c_int32), ("rows_per_cta", C.c_int32)]
+                ("kernel", C.c_int32), ("rows_per_cta", C.c_int32),
+                ("code_cell_bits", C.c_int32), ("reserved", C.c_int32)]
 
 
 def _load():

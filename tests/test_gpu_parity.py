@@ -133,23 +133,27 @@ def test_strategy_parity(strat, D, kind, cmp, monkeypatch):
     e = _forest(kind, T, D, F, seed, family, cmp)
     n = 1500 + seed % 97                 # several 512-row tiles + ragged tail
     Xd, Xh = X_pair(seed, n, F, special_q24=SPECIAL_Q24)
-    # PTT has two node layouts: rank-coded 4-B records (default) and fp32 8-B
-    for rank in (("1", "0") if strat == "ptt" else ("1",)):
+    # PTT has three node layouts: rank-coded 4-B records with 32- or 16-bit
+    # code cells, and fp32 8-B records
+    for rank, cw in ((("1", "32"), ("1", "16"), ("0", "0")) if strat == "ptt" else (("1", "0"),)):
         monkeypatch.setenv("HB_PTT_RANK", rank)
+        monkeypatch.setenv("HB_RANK_CW", cw)
         m = hb.Model(e, strategy=strat, device=0)
         assert m.info["strategy_name"] == strat
         if strat == "ptt":
             assert m.info["node_record_bytes"] == (4 if rank == "1" else 8)
+            assert m.info["code_cell_bits"] == int(cw)
         check_all(e, m, Xd, Xh)
 
 
 @pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("rank", ["1", "0"])
+@pytest.mark.parametrize("rank", ["1", "0", "16"])
 def test_ptt_special_thresholds(cmp, rank, monkeypatch):
     """Thresholds at +-Inf and -0/+0 (mixed on one feature) against X holding
     NaN, +-Inf, +-0 and exact ties: the rank code must reproduce every fp32
     decision (reading R3), for both PTT node layouts."""
-    monkeypatch.setenv("HB_PTT_RANK", rank)
+    monkeypatch.setenv("HB_PTT_RANK", "0" if rank == "0" else "1")
+    monkeypatch.setenv("HB_RANK_CW", "16" if rank == "16" else "0")
     e = _forest("binary", 33, 6, 5, 17, "mixed", cmp, grid=synth.GRID_COARSE)
     rng = np.random.default_rng(3)
     internal = np.nonzero(e.left != -1)[0]
@@ -157,7 +161,7 @@ def test_ptt_special_thresholds(cmp, rank, monkeypatch):
     specials = np.array([np.inf, -np.inf, 0.0, -0.0], np.float32)
     e.threshold[pick] = specials[rng.integers(0, 4, pick.size)]
     m = hb.Model(e, strategy="ptt", device=0)
-    assert m.info["node_record_bytes"] == (4 if rank == "1" else 8)
+    assert m.info["node_record_bytes"] == (8 if rank == "0" else 4)
     Xd, Xh = X_pair(8, 4000, 5, grid=synth.GRID_COARSE, special_q24=1 << 22)
     check_all(e, m, Xd, Xh)
 
@@ -584,9 +588,10 @@ def test_sixteen_outputs_vector_leaves(strat, small, monkeypatch):
 
 
 @pytest.mark.parametrize("D", [1, 2, 9, 10])
-@pytest.mark.parametrize("rank", ["0", "1"])
+@pytest.mark.parametrize("rank", ["0", "1", "16"])
 def test_ptt_depth_range(D, rank, monkeypatch):
-    monkeypatch.setenv("HB_PTT_RANK", rank)
+    monkeypatch.setenv("HB_PTT_RANK", "0" if rank == "0" else "1")
+    monkeypatch.setenv("HB_RANK_CW", "16" if rank == "16" else "0")
     e = synth.gen_forest(13, D, 10, seed=D, family="skinny", post=synth.POST_SIGMOID,
                          task=synth.TASK_CLASSIFICATION, base_score=[0.125])
     m = hb.Model(e, strategy="ptt", device=0)
