@@ -158,6 +158,32 @@ static inline int tree_out(const hb_ensemble *e, int t) {
   return e->tree_output ? e->tree_output[t] : t % e->n_outputs;
 }
 
+// Record order of the PTT layouts. For per-class scalar trees (leaf_width 1,
+// K > 1) records are sorted by output class (stable) and every class is padded
+// with zero trees to a multiple of the kernel's tree group, so a whole ILP
+// group shares one class and the kernel selects the accumulator once per group
+// (DESIGN.md §4.1). Each record header carries class | (local id + 1) << 8.
+TreeOrder ptt_order(const hb_ensemble *e, int t0, int t1, bool by_class) {
+  TreeOrder o;
+  const int K = e->n_outputs;
+  if (by_class && e->leaf_width == 1 && K > 1) {
+    for (int k = 0; k < K; ++k) {
+      for (int t = t0; t < t1; ++t)
+        if (tree_out(e, t) == k) o.local.push_back(t - t0), o.cls.push_back(k);
+      while (o.local.size() % kTreeGroup) o.local.push_back(-1), o.cls.push_back(k);
+    }
+  } else {
+    for (int t = t0; t < t1; ++t)
+      o.local.push_back(t - t0), o.cls.push_back(e->leaf_width == 1 ? tree_out(e, t) : 0);
+    while (o.local.size() % kTreeGroup) o.local.push_back(-1), o.cls.push_back(0);
+  }
+  return o;
+}
+
+uint32_t ptt_header(const TreeOrder &o, size_t r) {
+  return (uint32_t)o.cls[r] | ((uint32_t)(o.local[r] + 1) << 8);
+}
+
 static inline uint32_t f2u(float f) {
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -207,10 +233,11 @@ struct HostLayout {
 // A leaf at depth D_k < D becomes a perfect subtree whose decision nodes
 // compare feature 0 against +Inf ("free to perform arbitrary comparisons")
 // and whose 2^(D-D_k) leaves copy the leaf; leafmap keeps the original id.
-static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, HostLayout *L,
+static void build_ptt(const hb_ensemble *e, int t0, int D, const TreeOrder &order, HostLayout *L,
                       const FeatureMap *fm = nullptr) {
   const int w = e->leaf_width;
   const int P = 1 << D;
+  const int Tpad = (int)order.local.size();
   L->nslots = P;
   L->stride = round16((size_t)8 * P + (size_t)4 * w * P);
   L->trees.assign((size_t)Tpad * L->stride, 0);
@@ -221,13 +248,13 @@ static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, Hos
     uint8_t *rec = L->trees.data() + (size_t)lt * L->stride;
     uint32_t *node = reinterpret_cast<uint32_t *>(rec);
     float *leaf = reinterpret_cast<float *>(rec + (size_t)8 * P);
-    if (lt >= t1 - t0) {  // zero tree (padding to the tree group)
+    node[0] = ptt_header(order, lt);
+    if (order.local[lt] < 0) {  // zero tree (padding of a class / the tree group)
       for (int p = 1; p < P; ++p) node[2 * p] = 0, node[2 * p + 1] = f2u(pinf);
       continue;
     }
-    const int t = t0 + lt;
+    const int t = t0 + order.local[lt];
     const int64_t a = e->node_offset[t];
-    node[0] = (uint32_t)(w == 1 ? tree_out(e, t) : 0);
     orig[1] = 0;
     for (int p = 1; p < P; ++p) {
       const int o = orig[p];
@@ -243,14 +270,10 @@ static void build_ptt(const hb_ensemble *e, int t0, int t1, int D, int Tpad, Hos
       }
     }
     for (int p = P; p < 2 * P; ++p) {
-      const int o = orig[p];
+      const int o = D == 0 ? 0 : orig[p];
       const int slot = p - P;
       for (int k = 0; k < w; ++k) leaf[(size_t)slot * w + k] = e->leaf_value[(a + o) * w + k];
       L->leafmap[(size_t)lt * P + slot] = o;
-    }
-    if (D == 0) {  // single-leaf tree: root is the only slot
-      for (int k = 0; k < w; ++k) leaf[k] = e->leaf_value[a * w + k];
-      L->leafmap[(size_t)lt * P] = 0;
     }
   }
 }
@@ -479,7 +502,9 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     if (!done && strat == HB_STRATEGY_PTT) {
       bool ok = D <= kPttMaxDepth;
       if (ok) {
-        build_ptt(e, t0, t1, D, m->n_trees_pad, &L, &fmap);
+        const TreeOrder order = ptt_order(e, t0, t1, true);
+        m->n_trees_pad = (int)order.local.size();
+        build_ptt(e, t0, D, order, &L, &fmap);
         ok = choose_cfg((int)fmap.used.size(), L.stride, m->n_trees_pad, false, false, 24, &m->cfg);
       }
       if (!ok) {
@@ -540,6 +565,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     m->sb_nxf = m->n_xf;
   }
   if (strat == HB_STRATEGY_TT) {
+    m->sb_nrec = m->n_trees;
     m->sb_trees = m->d_trees;
     m->sb_leafmap = m->d_leafmap;
     m->sb_stride = m->stride;
@@ -547,6 +573,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     m->sb_tt = 1;
     m->sb_depth = D;
   } else if (strat == HB_STRATEGY_PTT && !m->ptt_rank) {
+    m->sb_nrec = m->n_trees_pad;
     m->sb_trees = m->d_trees;
     m->sb_leafmap = m->d_leafmap;
     m->sb_stride = m->stride;
@@ -554,7 +581,9 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     m->sb_depth = D;
   } else if (D <= kPttMaxDepth) {
     HostLayout S;
-    build_ptt(e, t0, t1, D, m->n_trees_pad, &S);
+    const TreeOrder order = ptt_order(e, t0, t1, true);
+    build_ptt(e, t0, D, order, &S);
+    m->sb_nrec = (int)order.local.size();
     uint8_t *dt = nullptr;
     st = upload(S.trees, &dt, &m->device_bytes);
     if (st != HB_OK) return st;

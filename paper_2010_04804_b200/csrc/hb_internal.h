@@ -73,6 +73,7 @@ struct Model {
   int32_t *sb_own_leafmap = nullptr;
   size_t sb_stride = 0;
   int sb_nslots = 0, sb_tt = 0, sb_depth = 0;
+  int sb_nrec = 0;                    // records in sb_trees (PTT: class-ordered, padded)
   const int32_t *sb_fmap = nullptr;   // feature map of the small-batch records
   int sb_nxf = 0;
 
@@ -105,6 +106,13 @@ hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);
 bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1);
 hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m);
 hb_status launch_gemm_tc(const Model &m, const RunArgs &a);
+// record order of the PTT layouts (hb_host.cu ptt_order)
+struct TreeOrder {
+  std::vector<int> local;   // per record: local tree id (t - t0), -1 = zero tree
+  std::vector<int> cls;     // per record: output class
+};
+TreeOrder ptt_order(const hb_ensemble *e, int t0, int t1, bool by_class);
+uint32_t ptt_header(const TreeOrder &o, size_t r);
 hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m, int nw_fp32);
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a);
 

@@ -78,7 +78,8 @@ static int env_int2(const char *name, int dflt) {
 hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m, int nw_fp32) {
   if (env_int2("HB_PTT_RANK", -1) == 0) return HB_E_UNSUPPORTED;
   const int F = e->n_features, w = e->leaf_width;
-  const int Tpad = m->n_trees_pad;
+  const TreeOrder order = ptt_order(e, t0, t1, true);
+  const int Tpad = (int)order.local.size();
   // 1. distinct thresholds per feature
   std::vector<std::vector<float>> th(F);
   for (int t = t0; t < t1; ++t)
@@ -180,10 +181,10 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     uint32_t *node = reinterpret_cast<uint32_t *>(rec);
     float *leaf = reinterpret_cast<float *>(rec + 4 * (size_t)P);
     for (int p = 1; p < P; ++p) node[p] = kPad;
-    if (lt >= t1 - t0) continue;   // zero tree
-    const int t = t0 + lt;
+    node[0] = ptt_header(order, lt);
+    if (order.local[lt] < 0) continue;   // zero tree (padding)
+    const int t = t0 + order.local[lt];
     const int64_t a = e->node_offset[t];
-    node[0] = (uint32_t)(w == 1 ? (e->tree_output ? e->tree_output[t] : t % e->n_outputs) : 0);
     orig[1] = 0;
     for (int p = 1; p < P; ++p) {
       const int o = orig[p];
@@ -260,6 +261,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   m->nslots = P;
   m->cfg = cfg;
   m->ptt_rank = 1;
+  m->n_trees_pad = Tpad;
   m->rank_cw = cw;
   return HB_OK;
 }

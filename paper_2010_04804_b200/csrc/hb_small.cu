@@ -23,7 +23,7 @@ struct SbParams {
   int F, depth, tt;          // tt: 1 = TT records (16-B header, self-loops), 0 = PTT fp32 records
   const uint8_t *trees;
   uint32_t stride;
-  int n_trees_pad, n_trees, tree_begin, nslots;
+  int n_rec, n_trees, tree_begin, nslots;   // n_rec: records (PTT: class-ordered + padding)
   const int32_t *leafmap;
   const float *scale, *base;
   int K, w, task, post, kind;
@@ -74,19 +74,25 @@ __global__ void __launch_bounds__(256) small_batch_kernel(const SbParams p) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
     uint64_t h = 0;
-    for (int t = threadIdx.x; t < p.n_trees; t += blockDim.x) {
+    for (int t = threadIdx.x; t < p.n_rec; t += blockDim.x) {
       const uint8_t *rec = p.trees + (size_t)t * p.stride;
       uint32_t slot;
       const float *leaf;
+      const uint32_t hdr = __ldg(reinterpret_cast<const uint32_t *>(rec));
       uint32_t kout;
+      int orig;
       if (p.tt) {
         slot = sb_walk_tt<LE>(reinterpret_cast<const uint2 *>(rec + 16), xs, p.depth);
         leaf = reinterpret_cast<const float *>(rec + 16 + 8 * (size_t)p.nslots);
-        kout = __ldg(reinterpret_cast<const uint32_t *>(rec));
+        kout = hdr;
+        orig = t;
       } else {
+        // PTT header: class | (local tree id + 1) << 8, 0 = padding record
+        orig = (int)(hdr >> 8) - 1;
+        if (orig < 0) continue;
         slot = sb_walk_ptt<LE>(reinterpret_cast<const uint2 *>(rec), xs, p.depth);
         leaf = reinterpret_cast<const float *>(rec + (8u << p.depth));
-        kout = __ldg(reinterpret_cast<const uint32_t *>(rec));
+        kout = hdr & 0xFFu;
       }
       if (p.w == 1) {
         const float v = __ldg(leaf + slot);
@@ -100,8 +106,8 @@ __global__ void __launch_bounds__(256) small_batch_kernel(const SbParams p) {
       }
       if (lm) {
         const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + slot);
-        if (lm == 1) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
-        else h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+        if (lm == 1) static_cast<int32_t *>(p.out)[row * p.n_trees + orig] = id;
+        else h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + orig) << 32) | (uint32_t)id);
       }
     }
     // fixed-order block reduction: warp shuffles, then warp 0 over 8 warps
@@ -159,7 +165,7 @@ hb_status launch_small_batch(const Model &m, const RunArgs &a) {
   p.tt = m.sb_tt;
   p.trees = static_cast<const uint8_t *>(m.sb_trees);
   p.stride = (uint32_t)m.sb_stride;
-  p.n_trees_pad = m.n_trees_pad;
+  p.n_rec = m.sb_nrec;
   p.n_trees = m.n_trees;
   p.tree_begin = m.tree_begin;
   p.nslots = m.sb_nslots;
