@@ -203,16 +203,12 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
           uint32_t off[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) off[g] = a[g] - tb[g];
-          // record header: tree_output | (local tree id + 1) << 8 (0: padding)
-          uint32_t hdr[G];
-#pragma unroll
-          for (int g = 0; g < G; ++g) hdr[g] = (NACC > 1 || lm) ? dev::lds_u32(tb[g]) : 0u;
           float vsum = 0.f;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const uint32_t slot = (off[g] >> 2) - (1u << D);
             if (p.w == 1) {
-              const float v = dev::lds_f32(tb[g] + off[g]);   // leaf(slot) == byte offset 4 i
+              const float v = dev::lds_f32(tb[g] + off[g]);
               if (NACC == 1) acc[0] += v;
               else vsum += v;
             } else {
@@ -221,25 +217,29 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
               for (int k = 0; k < NACC; ++k)
                 if (k < p.K) acc[k] += dev::lds_f32(lb + 4u * k);
             }
-            if (lm) {
-              const int orig = (int)(hdr[g] >> 8) - 1;     // local tree id, -1 = padding
-              if (orig >= 0) {
-                const int32_t id = __ldg(p.leafmap + (size_t)(c * ch + j + g) * p.nslots + slot);
-                if (lm == 1) {
-                  if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + orig] = id;
-                } else {
-                  h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + orig) << 32) | (uint32_t)id);
-                }
-              }
-            }
           }
           if (NACC > 1 && p.w == 1) {
             // per-class records are ordered by class in groups of G (hb_host.cu
             // ptt_order): one output selection per group instead of per tree
-            const uint32_t k0 = hdr[0] & 0xFFu;
+            const uint32_t k0 = dev::lds_u32(tb[0]) & 0xFFu;
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
               if (k0 == (uint32_t)k) acc[k] += vsum;
+          }
+          if (lm) {
+            // record header: tree_output | (local tree id + 1) << 8 (0: padding)
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const int orig = (int)(dev::lds_u32(tb[g]) >> 8) - 1;
+              if (orig < 0) continue;
+              const uint32_t slot = (off[g] >> 2) - (1u << D);
+              const int32_t id = __ldg(p.leafmap + (size_t)(c * ch + j + g) * p.nslots + slot);
+              if (lm == 1) {
+                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + orig] = id;
+              } else {
+                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + orig) << 32) | (uint32_t)id);
+              }
+            }
           }
         }
       }
