@@ -99,3 +99,18 @@ def test_compile_without_gpu_fails_cleanly():
     with pytest.raises(hb.HBError) as ei:
         hb.Model(_ok_forest(), device=0)
     assert ei.value.status == 1   # HB_E_INVALID: not a CUDA device
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: a copy of the package without libhb.so imports (so the
+    build module works on a clean tree) but any API use raises ImportError."""
+    import shutil
+    pkg = os.path.join(ROOT, "paper_2010_04804_b200")
+    dst = tmp_path / "paper_2010_04804_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "build", "csrc"))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2010_04804_b200 as hb\n"
+            "import paper_2010_04804_b200.build\n"
+            "try:\n    hb.Model\nexcept ImportError as e:\n    print('IMPORTERROR', e)\n") % str(tmp_path)
+    out = subprocess.run([__import__("sys").executable, "-c", code], capture_output=True, text=True)
+    assert "IMPORTERROR" in out.stdout and "libhb.so is missing" in out.stdout, out.stdout + out.stderr
