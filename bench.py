@@ -301,6 +301,8 @@ def run_ours(args):
     layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "")
     prof = load_profile(args.config, layout)
     kname = info["kernel_name"]
+    if n <= int(os.environ.get("HB_SMALL_BATCH", "4096")):
+        kname = "small_batch_kernel"      # request/response sizes (hb_small.cu)
     hbm_bytes = n * (cfg.n_features * 4 + (8 if (cls and e.n_outputs == 1) else 4 * e.n_outputs))
     measured = {}
     try:
