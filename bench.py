@@ -310,6 +310,7 @@ def run_ours(args):
     except OSError:
         pass
     hbm_peak = measured.get("hbm_gbs", 6650.0)
+    same_launch = prof.get("rows") == n and prof.get("trees", t1 - t0) == t1 - t0
     # nodes staged in SMEM (PTT, narrow TT) -> SMEM roof; tt_wide_kernel reads
     # node records through L1/L2 -> the measured L2 read roof
     l2_wide = info["strategy_name"] == "tt" and kname == "tt_wide_kernel"
@@ -317,8 +318,8 @@ def run_ours(args):
     roofline = {
         "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "mean_levels_per_tree": levels,
-        "traffic": prof.get("smem_ld_bytes_per_launch") if prof.get("rows") == n else None,
-        "traffic_dram": prof.get("dram_bytes_per_launch") if prof.get("rows") == n else None,
+        "traffic": prof.get("smem_ld_bytes_per_launch") if same_launch else None,
+        "traffic_dram": prof.get("dram_bytes_per_launch") if same_launch else None,
         "traffic_source": prof.get("source"),
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
         "algorithmic_bytes_per_row": per_row,
