@@ -422,6 +422,7 @@ static void free_model(Model *m) {
   cudaFree(m->sb_own_trees);
   cudaFree(m->sb_own_leafmap);
   cudaFree(m->d_fmap);
+  cudaFree(m->d_tops);
   delete m;
 }
 
@@ -544,6 +545,15 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.t_smem = 0;
         c.ch = kTreeGroup;
         m->cfg = c;
+        // large ensembles on wide rows: 4-CTA clusters with SMEM-resident top
+        // levels (hb_tt_cluster.cu) when all features are used and tops fit
+        if (fmap.identity && env_int("HB_TT_CLUSTER", 0)) {
+          m->stride = L.stride;
+          m->nslots = L.nslots;
+          st = compile_tt_cluster(e, t0, t1, m.get(), nullptr, L.trees);
+          if (st == HB_OK) m->tt_cluster = 1;
+          else if (st != HB_E_UNSUPPORTED) return st;
+        }
       }
     }
     if (!done) {
@@ -851,7 +861,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->tensor_cores = m.gemm_tc;
   info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : (m.ptt_rank ? 4 : 8);
   if (m.strategy == HB_STRATEGY_PTT) info->kernel = m.ptt_rank ? 1 : 0;
-  else if (m.strategy == HB_STRATEGY_TT) info->kernel = m.cfg.wide_rows ? 3 : 2;
+  else if (m.strategy == HB_STRATEGY_TT) info->kernel = m.tt_cluster ? 6 : (m.cfg.wide_rows ? 3 : 2);
   else info->kernel = m.gemm_tc ? 4 : 5;
   info->rows_per_cta = m.strategy == HB_STRATEGY_GEMM ? (m.gemm_tc ? 128 : 128)
                        : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);

@@ -82,6 +82,12 @@ struct Model {
   int32_t *d_fmap = nullptr;   // [n_xf] compact column -> original feature (null: identity)
   int n_xf = 0;
 
+  // TT cluster kernel (hb_tt_cluster.cu): SMEM-resident top levels per CTA
+  int tt_cluster = 0;
+  void *d_tops = nullptr;
+  int cl_topd = 0, cl_per_cta = 0, cl_smem = 0;
+  size_t cl_top_bytes = 0;
+
   size_t device_bytes = 0;
   LaunchCfg cfg;
 };
@@ -121,5 +127,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a);
 hb_status launch_gemm(const Model &m, const RunArgs &a);
 hb_status launch_finalize(const Model &m, const RunArgs &a);
 hb_status launch_small_batch(const Model &m, const RunArgs &a);
+hb_status compile_tt_cluster(const hb_ensemble *e, int t0, int t1, Model *m, const int32_t *fremap,
+                             const std::vector<uint8_t> &tt_trees);
+hb_status launch_tt_cluster(const Model &m, const RunArgs &a);
 
 }  // namespace hb

@@ -362,6 +362,10 @@ static TtFn pick_wide(int R, int nacc) {
 }
 
 hb_status launch_tt(const Model &m, const RunArgs &a) {
+  if (m.tt_cluster) {
+    const hb_status st = launch_tt_cluster(m, a);
+    if (st != HB_E_UNSUPPORTED) return st;   // unaligned rows: tt_wide_kernel below
+  }
   const bool wide = m.cfg.wide_rows > 0;
   TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc)
                                       : pick_wide<false>(m.cfg.wide_rows, m.nacc))

@@ -16,7 +16,7 @@ TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
 STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
 KERNEL_NAME = {0: "ptt_kernel", 1: "pttr_kernel", 2: "tt_kernel", 3: "tt_wide_kernel",
-               4: "gemm_tc_kernel", 5: "gemm_kernel"}
+               4: "gemm_tc_kernel", 5: "gemm_kernel", 6: "tt_cluster_kernel"}
 OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5}
 
 # every symbol include/hb.h declares (checked by tests/test_abi.py)

@@ -617,3 +617,25 @@ def test_leaf_values_extreme_magnitudes():
     # fp32 sum of 200 terms |v| ~ 50: error bound ~ 200 * 2^-24 * sum|v|
     bound = 200 * 2.0 ** -24 * np.abs(s["raw"]).max() * 200
     assert np.abs(got - s["raw"]).max() <= max(bound, 1e-3)
+
+
+@pytest.mark.parametrize("kind", ["binary", "multiclass", "rf"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_tt_cluster_kernel_parity(kind, cmp, monkeypatch):
+    """The 4-CTA cluster TT kernel (SMEM-resident top levels, multicast X tile,
+    DSMEM reduction; opt-in via HB_TT_CLUSTER=1): wide rows with every
+    feature used, deep mixed trees, ragged row tiles and tree counts not
+    divisible by the cluster size."""
+    monkeypatch.setenv("HB_TT_CLUSTER", "1")
+    seed = zlib.crc32(f"cluster{kind}{cmp}".encode()) & 0xFFFF
+    F = 1200
+    e = _forest(kind, 61, 12, F, seed, "mixed", cmp)
+    # make every feature used (the cluster kernel reads uncompacted rows)
+    e.feature[e.left != -1] = np.arange(int((e.left != -1).sum())) % F
+    m = hb.Model(e, device=0)
+    assert m.info["kernel_name"] == "tt_cluster_kernel", m.info
+    Xd, Xh = X_pair(seed, 997, F, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
+    # unaligned rows fall back to tt_wide_kernel inside the same model
+    Xd2, Xh2 = X_pair(seed + 1, 301, F, ldx=F + 1)
+    check_all(e, m, Xd2, Xh2, kinds=("raw", "leaf"))
