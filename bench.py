@@ -216,7 +216,8 @@ def run_ours(args):
 
         def step():
             m.run(X, kind, out=out, stream=stream)
-        launches_per_step = 1
+        # rank-code pre-pass models launch rank_code_kernel + pttr_kernel per call
+        launches_per_step = 2 if m.info.get("rank_prepass") else 1
     else:
         # trees sharded, all rows on every rank; one NCCL reduce of fp32
         # partials to rank 0, which finalizes (strong scaling)
@@ -298,7 +299,8 @@ def run_ours(args):
         except Exception as ex:  # pragma: no cover
             peaks = {"error": str(ex)}
     smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
-    layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "")
+    layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "") + \
+        ("-pre" if info.get("rank_prepass") else "")
     prof = load_profile(args.config, layout)
     kname = info["kernel_name"]
     if n <= int(os.environ.get("HB_SMALL_BATCH", "4096")):
@@ -311,9 +313,9 @@ def run_ours(args):
         pass
     hbm_peak = measured.get("hbm_gbs", 6650.0)
     same_launch = prof.get("rows") == n and prof.get("trees", t1 - t0) == t1 - t0
-    # nodes staged in SMEM (PTT, narrow TT) -> SMEM roof; tt_wide_kernel reads
-    # node records through L1/L2 -> the measured L2 read roof
-    l2_wide = info["strategy_name"] == "tt" and kname == "tt_wide_kernel"
+    # nodes staged in SMEM (PTT, narrow TT) -> SMEM roof; tt_wide_kernel and
+    # ttb_kernel read node records through L1/L2 -> the measured L2 read roof
+    l2_wide = info["strategy_name"] == "tt" and kname in ("tt_wide_kernel", "ttb_kernel")
     bound, peak = ("l2", peaks.get("l2_gbs") or 12000.0) if l2_wide else ("smem", smem_peak)
     roofline = {
         "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -322,6 +324,9 @@ def run_ours(args):
         "traffic_dram": prof.get("dram_bytes_per_launch") if same_launch else None,
         "traffic_source": prof.get("source"),
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
+        "kernel_ms_covers": ("rank_code_kernel + pttr_kernel (both launches of one hb_predict call; "
+                             "their split is in the ncu launch list under profiles/)")
+        if info.get("rank_prepass") else kname,
         "algorithmic_bytes_per_row": per_row,
         "peak_source": ("measured L2 read microbenchmark (tools/peaks.cu), this run" if l2_wide else
                         "measured LDS.128 microbenchmark (tools/peaks.cu), this run")

@@ -144,11 +144,13 @@ typedef struct {
   int32_t tensor_cores;         /* 1 if the scorer runs tcgen05 MMAs (GEMM)    */
   int32_t node_record_bytes;    /* PTT/TT node record size (4 = rank-coded PTT) */
   int32_t kernel;               /* row-tile scorer: 0 ptt, 1 ptt rank-coded, 2 tt, 3 tt wide-row,
-                                   4 gemm tcgen05, 5 gemm CUDA-core, 6 tt 4-CTA cluster
+                                   4 gemm tcgen05, 5 gemm CUDA-core, 6 tt 4-CTA cluster,
+                                   7 tt over 2-level node blocks
                                    (small batches: hb_small) */
   int32_t rows_per_cta;         /* rows one CTA owns per tile                   */
   int32_t code_cell_bits;       /* rank-coded PTT: 32 or 16-bit X code cells    */
-  int32_t reserved;
+  int32_t rank_prepass;         /* rank-coded PTT: 1 if a separate launch (rank_code_kernel)
+                                   computes the X codes into stream-ordered scratch */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the

@@ -423,6 +423,9 @@ static void free_model(Model *m) {
   cudaFree(m->sb_own_leafmap);
   cudaFree(m->d_fmap);
   cudaFree(m->d_tops);
+  cudaFree(m->d_rb);
+  cudaFree(m->d_ttb);
+  if (m->mempool) cudaMemPoolDestroy(m->mempool);   // deferred until pending frees complete
   delete m;
 }
 
@@ -545,6 +548,13 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.t_smem = 0;
         c.ch = kTreeGroup;
         m->cfg = c;
+        // opt-in (HB_TT_BLOCK=1): 2-level node blocks walked by per-lane
+        // cursors (hb_ttb.cu); measured slower than
+        // tt_wide_kernel on C5, so AUTO keeps tt_wide_kernel
+        if (env_int("HB_TT_BLOCK", 0) && !env_int("HB_TT_CLUSTER", 0)) {
+          st = compile_tt_blocks(e, t0, t1, fmap.identity ? nullptr : fmap.remap.data(), m.get());
+          if (st != HB_OK) return st;
+        }
         // large ensembles on wide rows: 4-CTA clusters with SMEM-resident top
         // levels (hb_tt_cluster.cu) when all features are used and tops fit
         if (fmap.identity && env_int("HB_TT_CLUSTER", 0)) {
@@ -861,12 +871,13 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->tensor_cores = m.gemm_tc;
   info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : (m.ptt_rank ? 4 : 8);
   if (m.strategy == HB_STRATEGY_PTT) info->kernel = m.ptt_rank ? 1 : 0;
-  else if (m.strategy == HB_STRATEGY_TT) info->kernel = m.tt_cluster ? 6 : (m.cfg.wide_rows ? 3 : 2);
+  else if (m.strategy == HB_STRATEGY_TT)
+    info->kernel = m.tt_cluster ? 6 : (m.tt_blocks ? 7 : (m.cfg.wide_rows ? 3 : 2));
   else info->kernel = m.gemm_tc ? 4 : 5;
   info->rows_per_cta = m.strategy == HB_STRATEGY_GEMM ? (m.gemm_tc ? 128 : 128)
                        : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);
   info->code_cell_bits = m.ptt_rank ? m.rank_cw : 0;
-  info->reserved = 0;
+  info->rank_prepass = m.rank_pre;
   return HB_OK;
 }
 

@@ -64,6 +64,15 @@ struct Model {
   void *d_aux = nullptr;    // [fmeta | groups | eytzinger pool]
   size_t aux_groups_off = 0, aux_pool_off = 0;
   int rank_nfc = 0, rank_ngroups = 0;
+  // rank-code pre-pass (hb_rank_codes.cu): codes computed by a separate launch
+  // into a per-call scratch buffer (stream-ordered pool), scorer ring carries
+  // tree chunks only
+  int rank_pre = 0;
+  int rank_nwords = 0;       // 32-bit code words per row (n_fc or ceil(n_fc / 2))
+  void *d_rb = nullptr;      // [feat | groups | bucket tables]
+  size_t rb_groups_off = 0, rb_pool_off = 0, rb_smem = 0;
+  int rb_ngroups = 0;
+  cudaMemPool_t mempool = nullptr;
 
   // small-batch path (hb_small.cu): PTT fp32 or TT records walked by
   // trees-across-threads; may alias d_trees / d_leafmap
@@ -87,6 +96,13 @@ struct Model {
   void *d_tops = nullptr;
   int cl_topd = 0, cl_per_cta = 0, cl_smem = 0;
   size_t cl_top_bytes = 0;
+
+  // TT over 2-level node blocks (hb_ttb.cu): [blocks | leaves | lorig | cls]
+  int tt_blocks = 0;
+  void *d_ttb = nullptr;
+  size_t ttb_leaf_off = 0, ttb_lorig_off = 0, ttb_cls_off = 0;
+  int64_t ttb_nblocks = 0;
+  int ttb_sync = 1;          // lanes of a warp advance a cursor together
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
@@ -121,6 +137,17 @@ TreeOrder ptt_order(const hb_ensemble *e, int t0, int t1, bool by_class);
 uint32_t ptt_header(const TreeOrder &o, size_t r);
 hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m, int nw_fp32);
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a);
+// rank-code pre-pass tables (hb_rank_codes.cu)
+struct RankBuckets {
+  std::vector<uint32_t> feat;     // [n_fc][8] {f, B, S, start off, lo, hi, s, u off}
+  std::vector<uint32_t> groups;   // [n_groups][4] {pool off, bytes, word_begin, word_end}
+  std::vector<uint8_t> pool;
+  int n_groups = 0, n_words = 0;
+  size_t max_group_bytes = 0;     // largest SMEM-resident group
+};
+hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
+                             int cw, RankBuckets *out);
+hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);
 hb_status launch_tt(const Model &m, const RunArgs &a);
@@ -130,5 +157,7 @@ hb_status launch_small_batch(const Model &m, const RunArgs &a);
 hb_status compile_tt_cluster(const hb_ensemble *e, int t0, int t1, Model *m, const int32_t *fremap,
                              const std::vector<uint8_t> &tt_trees);
 hb_status launch_tt_cluster(const Model &m, const RunArgs &a);
+hb_status compile_tt_blocks(const hb_ensemble *e, int t0, int t1, const int32_t *remap, Model *m);
+hb_status launch_tt_blocks(const Model &m, const RunArgs &a);
 
 }  // namespace hb

@@ -124,7 +124,10 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   const int force = env_int2("HB_PTT_RANK", -1);
   const int force_cw = env_int2("HB_RANK_CW", 0);
   const int force_nw = env_int2("HB_NW", 0);
-  auto try_cfg = [&](int cw, LaunchCfg &cfg) {
+  const int force_pre = env_int2("HB_RANK_PRE", -1);
+  // pre: codes come from the pre-pass (hb_rank_codes.cu), the ring carries
+  // tree chunks only; otherwise the ring also carries the Eytzinger arrays
+  auto try_cfg = [&](int cw, bool pre, LaunchCfg &cfg) {
     if (cw == 32 && A.n_fc > 511) return false;
     const long tile = cw == 32 ? (long)A.n_fc * 128 : (long)((A.n_fc + 1) / 2) * 128;
     for (int nw : {24, 16, 12, 8, 4}) {
@@ -133,10 +136,10 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
       const long rem = (long)kSmemBudget - xb;
       const int ns = env_int2("HB_NS", 2);
       const long per = rem / ns - 16;
-      if (per < (long)A.max_feat_bytes || per < (long)kTreeGroup * (long)stride) continue;
+      if ((!pre && per < (long)A.max_feat_bytes) || per < (long)kTreeGroup * (long)stride) continue;
       int ch = (int)std::min<long>(env_int2("HB_CH", 64), per / (long)stride) & ~(kTreeGroup - 1);
       ch = std::min(ch, Tpad);
-      const long stage = std::max<long>((long)ch * stride, (long)A.max_feat_bytes);
+      const long stage = pre ? (long)ch * stride : std::max<long>((long)ch * stride, (long)A.max_feat_bytes);
       cfg.nw = nw;
       cfg.ns = ns;
       cfg.ch = ch;
@@ -148,24 +151,40 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     }
     return false;
   };
-  LaunchCfg cfg, cfg16;
+  // 32-bit cells first; 16-bit cells (half the tile, one more instruction
+  // per level) when they buy more warps
+  auto pick_cw = [&](bool pre, LaunchCfg &cfg, int &cw) {
+    LaunchCfg c32, c16;
+    const bool ok32 = force_cw != 16 && try_cfg(32, pre, c32);
+    const bool ok16 = force_cw != 32 && try_cfg(16, pre, c16);
+    if (ok16 && (!ok32 || force_cw == 16 || c16.nw > c32.nw)) {
+      cfg = c16;
+      cw = 16;
+      return true;
+    }
+    cfg = c32;
+    cw = 32;
+    return ok32;
+  };
+  LaunchCfg cfg;
   int cw = 32;
-  bool ok = force_cw != 16 && try_cfg(32, cfg);
-  const bool ok16 = force_cw != 32 && try_cfg(16, cfg16);
-  if (ok16 && (!ok || force_cw == 16 || cfg16.nw > cfg.nw)) {
-    cfg = cfg16;
-    cw = 16;
-    ok = true;
-  }
-  // auto: rank-coded nodes only when (a) the per-tile rank
+  bool pre = force_pre == 1;
+  bool ok = !pre && pick_cw(false, cfg, cw);
+  // auto: in-kernel codes only when (a) the per-tile rank
   // transform (sum_f L_f searches per row) stays small next to the walk it
   // shortens (T * D levels per row) and (b) the layout runs at least as many
   // warps as the fp32-node layout would (occupancy decides at equal bytes).
+  // Otherwise the pre-pass computes the codes (cost: one more read of X, and
+  // a write + read of the code words, in HBM).
   if (ok && force != 1) {
     double lsum = 0;
     for (int c = 0; c < A.n_fc; ++c) lsum += Ls[c];
     if (lsum > 0.2 * (double)Tpad * (double)std::max(D, 1)) ok = false;
     if (cfg.nw < nw_fp32) ok = false;
+  }
+  if (!ok && force_pre != 0) {
+    pre = true;
+    ok = pick_cw(true, cfg, cw);
   }
   if (!ok) return HB_E_UNSUPPORTED;
   // tree records: node = (cell offset) << 16 | k
@@ -208,28 +227,30 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
       leafmap[(size_t)lt * P + slot] = o;
     }
   }
-  // 5. group features into stage-sized bulk copies
-  {
-    size_t goff = 0, gbytes = 0;
-    int gbeg = 0;
-    auto close = [&](int end) {
-      A.groups.insert(A.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)gbeg, (uint32_t)end});
-      goff += gbytes;
-      gbytes = 0;
-      gbeg = end;
-      A.n_groups++;
-    };
-    for (int c = 0; c < A.n_fc; ++c) {
-      const size_t b = ey[c].size() * 4;
-      if (gbytes + b > (size_t)cfg.stage_bytes) close(c);
-      A.fmeta.insert(A.fmeta.end(), {0u, (uint32_t)Ls[c], (uint32_t)gbytes, (uint32_t)A.n_groups});
-      gbytes += b;
-      A.pool.insert(A.pool.end(), ey[c].begin(), ey[c].end());
+  if (!pre) {
+    // 5. group features into stage-sized bulk copies
+    {
+      size_t goff = 0, gbytes = 0;
+      int gbeg = 0;
+      auto close = [&](int end) {
+        A.groups.insert(A.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)gbeg, (uint32_t)end});
+        goff += gbytes;
+        gbytes = 0;
+        gbeg = end;
+        A.n_groups++;
+      };
+      for (int c = 0; c < A.n_fc; ++c) {
+        const size_t b = ey[c].size() * 4;
+        if (gbytes + b > (size_t)cfg.stage_bytes) close(c);
+        A.fmeta.insert(A.fmeta.end(), {0u, (uint32_t)Ls[c], (uint32_t)gbytes, (uint32_t)A.n_groups});
+        gbytes += b;
+        A.pool.insert(A.pool.end(), ey[c].begin(), ey[c].end());
+      }
+      if (gbytes) close(A.n_fc);
+      int c = 0;
+      for (int f = 0; f < F; ++f)
+        if (fc_of[f] >= 0) A.fmeta[4 * c++] = (uint32_t)f;
     }
-    if (gbytes) close(A.n_fc);
-    int c = 0;
-    for (int f = 0; f < F; ++f)
-      if (fc_of[f] >= 0) A.fmeta[4 * c++] = (uint32_t)f;
   }
   // 6. upload: trees, leafmap, aux = [fmeta | groups | pool]
   cudaError_t err;
@@ -243,20 +264,57 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   if ((err = cudaMemcpy(m->d_leafmap, leafmap.data(), leafmap.size() * 4, cudaMemcpyHostToDevice)) !=
       cudaSuccess)
     return cuda_fail(err, "cudaMemcpy(pttr leafmap)");
-  const size_t fb = A.fmeta.size() * 4, gb = A.groups.size() * 4, pb = A.pool.size() * 4;
-  const size_t pool_off = (fb + gb + 127) & ~size_t(127);
-  std::vector<uint8_t> aux(pool_off + pb, 0);
-  std::memcpy(aux.data(), A.fmeta.data(), fb);
-  std::memcpy(aux.data() + fb, A.groups.data(), gb);
-  std::memcpy(aux.data() + pool_off, A.pool.data(), pb);
-  if ((err = cudaMalloc(&m->d_aux, aux.size())) != cudaSuccess) return cuda_fail(err, "cudaMalloc(pttr aux)");
-  m->device_bytes += aux.size();
-  if ((err = cudaMemcpy(m->d_aux, aux.data(), aux.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
-    return cuda_fail(err, "cudaMemcpy(pttr aux)");
-  m->aux_groups_off = fb;
-  m->aux_pool_off = pool_off;
+  if (!pre) {
+    const size_t fb = A.fmeta.size() * 4, gb = A.groups.size() * 4, pb = A.pool.size() * 4;
+    const size_t pool_off = (fb + gb + 127) & ~size_t(127);
+    std::vector<uint8_t> aux(pool_off + pb, 0);
+    std::memcpy(aux.data(), A.fmeta.data(), fb);
+    std::memcpy(aux.data() + fb, A.groups.data(), gb);
+    std::memcpy(aux.data() + pool_off, A.pool.data(), pb);
+    if ((err = cudaMalloc(&m->d_aux, aux.size())) != cudaSuccess) return cuda_fail(err, "cudaMalloc(pttr aux)");
+    m->device_bytes += aux.size();
+    if ((err = cudaMemcpy(m->d_aux, aux.data(), aux.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(err, "cudaMemcpy(pttr aux)");
+    m->aux_groups_off = fb;
+    m->aux_pool_off = pool_off;
+    m->rank_ngroups = A.n_groups;
+  } else {
+    // pre-pass bucket tables: [feat | groups | pool]
+    std::vector<int> origf;
+    for (int f = 0; f < F; ++f)
+      if (fc_of[f] >= 0) origf.push_back(f);
+    RankBuckets R;
+    const hb_status st = build_rank_buckets(sorted, origf, cw, &R);
+    if (st != HB_OK) return st;
+    const size_t fb = R.feat.size() * 4, gb = R.groups.size() * 4;
+    const size_t pool_off = (fb + gb + 127) & ~size_t(127);
+    std::vector<uint8_t> aux(pool_off + R.pool.size(), 0);
+    std::memcpy(aux.data(), R.feat.data(), fb);
+    std::memcpy(aux.data() + fb, R.groups.data(), gb);
+    std::memcpy(aux.data() + pool_off, R.pool.data(), R.pool.size());
+    if ((err = cudaMalloc(&m->d_rb, aux.size())) != cudaSuccess) return cuda_fail(err, "cudaMalloc(rank tables)");
+    m->device_bytes += aux.size();
+    if ((err = cudaMemcpy(m->d_rb, aux.data(), aux.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_fail(err, "cudaMemcpy(rank tables)");
+    m->rb_groups_off = fb;
+    m->rb_pool_off = pool_off;
+    m->rb_ngroups = R.n_groups;
+    m->rb_smem = R.max_group_bytes;
+    m->rank_nwords = R.n_words;
+    m->rank_ngroups = 0;
+    // per-call code scratch: stream-ordered allocations from a model-owned
+    // pool that keeps its memory (no cudaMalloc on the scoring path)
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = m->device;
+    if ((err = cudaMemPoolCreate(&m->mempool, &props)) != cudaSuccess) return cuda_fail(err, "cudaMemPoolCreate");
+    uint64_t keep = UINT64_MAX;
+    if ((err = cudaMemPoolSetAttribute(m->mempool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
+      return cuda_fail(err, "cudaMemPoolSetAttribute");
+  }
+  m->rank_pre = pre ? 1 : 0;
   m->rank_nfc = A.n_fc;
-  m->rank_ngroups = A.n_groups;
   m->stride = stride;
   m->nslots = P;
   m->cfg = cfg;
@@ -273,6 +331,23 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
                               : pttr_fn32(m.depth, m.cmp == HB_CMP_LE, m.nacc);
   if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
   PttrParams p;
+  // pre-pass: rank codes of every (row, used feature) into stream-ordered
+  // scratch, in the per-warp tile layout the scorer copies verbatim
+  uint32_t *codes = nullptr;
+  cudaError_t e;
+  if (m.rank_pre) {
+    const int64_t nblocks = (a.n + 31) / 32;
+    const size_t bytes = std::max<size_t>((size_t)nblocks * m.rank_nwords * 128, 128);
+    e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&codes), bytes, m.mempool, a.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync(rank codes)");
+    const hb_status st = launch_rank_codes(m, a, codes, nblocks);
+    if (st != HB_OK) {
+      cudaFreeAsync(codes, a.stream);
+      return st;
+    }
+  }
+  p.codes = codes;
+  p.n_words = m.rank_nwords;
   p.X = a.X;
   p.n = a.n;
   p.ldx = a.ldx;
@@ -307,14 +382,18 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   p.stage_bytes = (uint32_t)m.cfg.stage_bytes;
   const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
-  if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
+  if (ntiles > INT32_MAX) {
+    if (codes) cudaFreeAsync(codes, a.stream);
+    return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
+  }
   p.ntiles = (int)ntiles;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       m.cfg.smem_bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(pttr)");
-  fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
-  e = cudaGetLastError();
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m.cfg.smem_bytes);
+  if (e == cudaSuccess) {
+    fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
+    e = cudaGetLastError();
+  }
+  if (codes) cudaFreeAsync(codes, a.stream);
   if (e != cudaSuccess) return cuda_fail(e, "pttr_kernel launch");
   return HB_OK;
 }

@@ -26,8 +26,10 @@ struct PttrParams {
   int K, w, task, post, kind;
   void *out;
   int nw, ns, ch, ntiles;
-  int prefetch;           // L2 prefetch of the next tile's X rows
+  int prefetch;           // L2 prefetch of the next tile's X rows (code words with the pre-pass)
   uint32_t stage_bytes;
+  const uint32_t *codes;  // pre-pass output [row block][n_words][32] (null: codes computed in-kernel)
+  int n_words;
 };
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
@@ -77,9 +79,17 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
         dev::mbar_wait(&empty[s], r.ph ^ 1u);
         if (q == 0 && p.prefetch) {
           // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
+          // (of code words, which are contiguous per tile, with the pre-pass)
           const long tile_i = it / items;
           const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32);
-          dev::prefetch_rows_l2(p.X, next, (int64_t)nw * 32, p.n, p.ldx);
+          if (p.codes) {
+            const int64_t nb = (p.n + 31) / 32, b0 = next / 32;
+            if (b0 < nb)
+              dev::prefetch_rows_l2(reinterpret_cast<const float *>(p.codes), b0,
+                                    min((int64_t)nw, nb - b0), nb, (int64_t)p.n_words * 32);
+          } else {
+            dev::prefetch_rows_l2(p.X, next, (int64_t)nw * 32, p.n, p.ldx);
+          }
         }
         const uint8_t *src;
         uint32_t bytes;
@@ -108,7 +118,19 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
     const int64_t row = wrow0 + lane;
     const bool active = wrow0 < p.n;
     const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
-    if (CW == 32 && p.x_direct && active) {
+    if (p.codes) {
+      // codes from the pre-pass: this warp's block is already in tile layout
+      if (active) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.codes + (size_t)(wrow0 >> 5) * p.n_words * 32);
+        const uint32_t dst = codes - 4u * lane;
+        for (int i = lane; i < p.n_words * 8; i += 32) {
+          const uint4 v = __ldg(src + i);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * i), "r"(v.x), "r"(v.y),
+                       "r"(v.z), "r"(v.w));
+        }
+        __syncwarp();
+      }
+    } else if (CW == 32 && p.x_direct && active) {
       // fp32 X slice straight into the code cells (cell(f, lane) = xs[f*32 + lane])
       dev::load_x_slice(reinterpret_cast<float *>(smem) + (size_t)warp * p.n_fc * 32, p.X, row, p.n,
                         p.ldx, p.F, lane, p.vec4 != 0);

@@ -1,0 +1,286 @@
+// hb_rank_codes.cu — rank-code pre-pass of the rank-coded PTT scorer (sm_100a).
+//
+// The rank-coded PTT layout (hb_pttr.cu) walks integer codes
+// c(x) = #{j : u_j <= x} (LT; LE: u_j < x) instead of fp32 values, which keeps
+// every branch of PAPER.md Alg. 3 bit-identical to the fp32 walk.
+// For models with many distinct thresholds per feature (C2: ~1,400 over 90
+// features) the in-kernel Eytzinger search costs more than the walk it
+// shortens, and its search arrays crowd the tree ring out of shared memory.
+// This pre-pass computes the codes once per (row, feature) in a separate
+// launch and writes them in exactly the per-warp SMEM tile layout the scorer
+// uses, so the scorer's tile fill is a plain 16-B copy and its ring carries
+// tree chunks only.
+//
+// Search: a bucket index followed by a short binary search.
+//   b(x) = trunc(min((clamp(x, lo, hi) - lo) * s, B - 1))     (fp32, RN, no FMA)
+// is monotone non-decreasing in x for any s > 0, so
+//   u_j in a lower bucket than x  =>  u_j < x,   higher  =>  u_j > x,
+// and c(x) = start[b(x)] + #{u_j in bucket b(x) : u_j <= x}. start[] is
+// computed on the host by applying the same b() to every u_j, so the result is
+// exact whatever rounding b() does — the fp32 compares against u_j decide.
+// NaN -> 0xFFFF (sorts after every threshold: "go right", as x < t is false).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "hb_internal.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int kRcWarps = 8;                 // warps per CTA of the pre-pass
+constexpr uint32_t kRcSmemCap = 48 * 1024;  // per-CTA table budget (4 CTAs / SM)
+constexpr int kRcBatch = 16;                // X loads in flight together per lane
+constexpr int kRcRows = 4;                  // 32-row blocks per warp iteration
+
+struct RankCodeParams {
+  const float *X;
+  int64_t n, ldx;
+  const uint4 *feat;      // [n_fc][2] {f, B, S, start off} {lo, hi, s, u off} (offsets in group)
+  const uint4 *groups;    // [n_groups] {pool byte offset, bytes, word_begin, word_end}
+  const uint8_t *pool;
+  int n_fc, n_words;
+  uint32_t *codes;        // [nblocks][n_words][32]
+  int64_t nblocks;
+};
+
+template <bool LE>
+__device__ __forceinline__ uint32_t rank_code(float x, const uint4 m0, const uint4 m1, const uint8_t *tb) {
+  if (x != x) return 0xFFFFu;
+  const float lo = __uint_as_float(m1.x), hi = __uint_as_float(m1.y), s = __uint_as_float(m1.z);
+  const float xc = fminf(fmaxf(x, lo), hi);
+  float y = __fmul_rn(__fsub_rn(xc, lo), s);
+  y = fminf(y, (float)(m0.y - 1u));
+  const uint32_t b = __float2uint_rz(y);
+  const uint16_t *start = reinterpret_cast<const uint16_t *>(tb + m0.w);
+  const float *u = reinterpret_cast<const float *>(tb + m1.w);
+  uint32_t base = start[b];
+  uint32_t cnt = (uint32_t)start[b + 1] - base;
+  for (uint32_t k = 0; k < m0.z; ++k) {
+    const uint32_t half = cnt >> 1;
+    const float v = u[base + half];              // u has one pad slot: in range when cnt == 0
+    const bool go = cnt != 0 && (LE ? v < x : v <= x);
+    base = go ? base + half + 1u : base;
+    cnt = go ? cnt - half - 1u : half;
+  }
+  return base;
+}
+
+template <bool LE, int CW>
+__global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankCodeParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint4 g = __ldg(p.groups + blockIdx.y);
+  const uint8_t *tb = p.pool + g.x;
+  if (g.y <= kRcSmemCap) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(tb);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem);
+    for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+    tb = smem;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // one warp = kRcRows 32-row blocks, all words of this group: lane = row, so
+  // the strided X reads of consecutive features hit the sectors the first one
+  // brought into L1, and each word store is one coalesced 128-B line. X loads
+  // of kRcRows blocks x NB words are issued before the first search, so the
+  // HBM latency is paid once per batch, not once per feature.
+  constexpr int PW = CW == 32 ? 1 : 2;                   // features per word
+  constexpr int NB = kRcBatch / (kRcRows * PW) > 0 ? kRcBatch / (kRcRows * PW) : 1;   // words per batch
+  for (int64_t rb0 = ((int64_t)blockIdx.x * kRcWarps + warp) * kRcRows; rb0 < p.nblocks;
+       rb0 += (int64_t)gridDim.x * kRcWarps * kRcRows) {
+    for (int w0 = (int)g.z; w0 < (int)g.w; w0 += NB) {
+      float xv[kRcRows][NB][PW];
+#pragma unroll
+      for (int i = 0; i < kRcRows; ++i) {
+        const int64_t row = (rb0 + i) * 32 + lane;
+        const bool in = row < p.n;
+        const float *xr = p.X + (in ? row : 0) * p.ldx;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+#pragma unroll
+          for (int q = 0; q < PW; ++q) {
+            const int fc = min((w0 + j) * PW + q, p.n_fc - 1);
+            const uint32_t f = __ldg(reinterpret_cast<const uint32_t *>(p.feat + 2 * fc));
+            xv[i][j][q] = (in && w0 + j < (int)g.w) ? __ldg(xr + f) : 0.f;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int wd = w0 + j;
+        if (wd >= (int)g.w) break;
+        const int f0 = PW * wd, f1 = PW * wd + 1;
+        const uint4 a0 = __ldg(p.feat + 2 * f0), a1 = __ldg(p.feat + 2 * f0 + 1);
+        const bool has1 = PW == 2 && f1 < p.n_fc;
+        const uint4 b0 = __ldg(p.feat + 2 * (has1 ? f1 : f0)), b1 = __ldg(p.feat + 2 * (has1 ? f1 : f0) + 1);
+#pragma unroll
+        for (int i = 0; i < kRcRows; ++i) {
+          if (rb0 + i >= p.nblocks) break;
+          uint32_t word;
+          if (CW == 32) {
+            word = ((uint32_t)wd << 23) | rank_code<LE>(xv[i][j][0], a0, a1, tb);
+          } else {
+            const uint32_t c0 = rank_code<LE>(xv[i][j][0], a0, a1, tb);
+            const uint32_t c1 = has1 ? rank_code<LE>(xv[i][j][PW - 1], b0, b1, tb) : 0u;
+            word = c0 | (c1 << 16);
+          }
+          p.codes[((size_t)(rb0 + i) * p.n_words + wd) * 32 + lane] = word;
+        }
+      }
+    }
+  }
+}
+
+using RcFn = void (*)(const RankCodeParams);
+
+RcFn rc_pick(bool le, int cw) {
+  if (cw == 32) return le ? rank_code_kernel<true, 32> : rank_code_kernel<false, 32>;
+  return le ? rank_code_kernel<true, 16> : rank_code_kernel<false, 16>;
+}
+
+// Host twin of the bucket map in rank_code(): same fp32 operations, same
+// order, no contraction (volatile intermediates).
+uint32_t host_bucket(float x, float lo, float hi, float s, uint32_t B) {
+  volatile float xc = std::fmin(std::fmax(x, lo), hi);
+  volatile float d = xc - lo;
+  volatile float y = d * s;
+  const float yy = std::fmin((float)y, (float)(B - 1u));
+  return (uint32_t)yy;
+}
+
+}  // namespace
+
+// Bucket tables for the sorted distinct thresholds of each compact feature
+// (sorted[c], feature id orig[c]); words group 1 (CW 32) or 2 (CW 16) features.
+hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
+                             int cw, RankBuckets *out) {
+  const int n_fc = (int)sorted.size();
+  const int per_word = cw == 32 ? 1 : 2;
+  const int n_words = (n_fc + per_word - 1) / per_word;
+  RankBuckets R;
+  R.n_words = n_words;
+  R.feat.assign((size_t)n_fc * 8, 0u);
+  std::vector<std::vector<uint8_t>> tabs(n_fc);
+  for (int c = 0; c < n_fc; ++c) {
+    const std::vector<float> &u = sorted[c];
+    const uint32_t m = (uint32_t)u.size();
+    float lo = 0.f, hi = 0.f;
+    bool any = false;
+    for (float v : u)
+      if (std::isfinite(v)) {
+        if (!any) lo = v;
+        hi = v;
+        any = true;
+      }
+    uint32_t B = 1;
+    while (B < m && B < 16384u) B <<= 1;
+    float s = 0.f;
+    if (hi > lo) {
+      const float range = hi - lo;
+      s = std::isfinite(range) ? (float)B / range : (float)B / FLT_MAX;
+      if (!(s <= FLT_MAX)) s = FLT_MAX;     // tiny range: keep s finite (0 * s must stay 0)
+      if (!(s > 0.f)) s = FLT_MIN;
+    } else {
+      B = 1;
+    }
+    std::vector<uint32_t> start(B + 1, 0);
+    std::vector<uint32_t> bk(m);
+    for (uint32_t j = 0; j < m; ++j) bk[j] = host_bucket(u[j], lo, hi, s, B);
+    uint32_t maxocc = 0;
+    {
+      uint32_t j = 0;
+      for (uint32_t b = 0; b <= B; ++b) {
+        while (j < m && bk[j] < b) ++j;
+        start[b] = j;
+      }
+      for (uint32_t b = 0; b < B; ++b) maxocc = std::max(maxocc, start[b + 1] - start[b]);
+    }
+    uint32_t S = 0;
+    while ((1u << S) <= maxocc) ++S;        // bit_length(maxocc) search steps
+    const size_t sbytes = ((size_t)(B + 1) * 2 + 3) & ~size_t(3);
+    const size_t ubytes = ((size_t)(m + 1) * 4);
+    std::vector<uint8_t> t(sbytes + ubytes, 0);
+    for (uint32_t b = 0; b <= B; ++b) {
+      const uint16_t v = (uint16_t)start[b];
+      std::memcpy(t.data() + 2 * b, &v, 2);
+    }
+    std::memcpy(t.data() + sbytes, u.data(), (size_t)m * 4);
+    const float pad = INFINITY;
+    std::memcpy(t.data() + sbytes + (size_t)m * 4, &pad, 4);
+    tabs[c] = std::move(t);
+    uint32_t *fm = R.feat.data() + (size_t)c * 8;
+    fm[0] = (uint32_t)orig[c];
+    fm[1] = B;
+    fm[2] = S;
+    fm[3] = 0;                                 // start offset: set when grouped
+    std::memcpy(&fm[4], &lo, 4);
+    std::memcpy(&fm[5], &hi, 4);
+    std::memcpy(&fm[6], &s, 4);
+    fm[7] = (uint32_t)sbytes;                  // u offset relative to start; rebased below
+  }
+  // groups of whole words, <= kRcSmemCap bytes each (an oversized word is a
+  // group of its own and is searched from global memory)
+  size_t goff = 0, gbytes = 0;
+  int wbeg = 0;
+  auto close = [&](int wend) {
+    R.groups.insert(R.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)wbeg, (uint32_t)wend});
+    R.max_group_bytes = std::max(R.max_group_bytes, gbytes <= kRcSmemCap ? gbytes : (size_t)0);
+    goff += gbytes;
+    gbytes = 0;
+    wbeg = wend;
+    R.n_groups++;
+  };
+  for (int wd = 0; wd < n_words; ++wd) {
+    size_t wb = 0;
+    for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
+    if (gbytes > 0 && gbytes + wb > kRcSmemCap) close(wd);
+    for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) {
+      const int c = wd * per_word + q;
+      uint32_t *fm = R.feat.data() + (size_t)c * 8;
+      fm[3] = (uint32_t)gbytes;
+      fm[7] += (uint32_t)gbytes;
+      const size_t tb = (tabs[c].size() + 15) & ~size_t(15);
+      tabs[c].resize(tb, 0);
+      R.pool.insert(R.pool.end(), tabs[c].begin(), tabs[c].end());
+      gbytes += tb;
+    }
+  }
+  if (gbytes) close(n_words);
+  *out = std::move(R);
+  return HB_OK;
+}
+
+int sm_count(int device);
+
+hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks) {
+  RcFn fn = rc_pick(m.cmp == HB_CMP_LE, m.rank_cw);
+  RankCodeParams p;
+  p.X = a.X;
+  p.n = a.n;
+  p.ldx = a.ldx;
+  const uint8_t *aux = static_cast<const uint8_t *>(m.d_rb);
+  p.feat = reinterpret_cast<const uint4 *>(aux);
+  p.groups = reinterpret_cast<const uint4 *>(aux + m.rb_groups_off);
+  p.pool = aux + m.rb_pool_off;
+  p.n_fc = m.rank_nfc;
+  p.n_words = m.rank_nwords;
+  p.codes = codes;
+  p.nblocks = nblocks;
+  const int smem = (int)m.rb_smem;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(rank codes)");
+  // ~4 CTAs per SM in total, spread over the feature groups (blockIdx.y)
+  const int64_t want = std::max<int64_t>(1, (4LL * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (nblocks + kRcWarps * kRcRows - 1) / (kRcWarps * kRcRows)));
+  fn<<<dim3(gx, m.rb_ngroups), 32 * kRcWarps, smem, a.stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "rank_code_kernel launch");
+  return HB_OK;
+}
+
+}  // namespace hb

@@ -362,6 +362,7 @@ static TtFn pick_wide(int R, int nacc) {
 }
 
 hb_status launch_tt(const Model &m, const RunArgs &a) {
+  if (m.tt_blocks) return launch_tt_blocks(m, a);
   if (m.tt_cluster) {
     const hb_status st = launch_tt_cluster(m, a);
     if (st != HB_E_UNSUPPORTED) return st;   // unaligned rows: tt_wide_kernel below

@@ -16,7 +16,8 @@ TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
 STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
 KERNEL_NAME = {0: "ptt_kernel", 1: "pttr_kernel", 2: "tt_kernel", 3: "tt_wide_kernel",
-               4: "gemm_tc_kernel", 5: "gemm_kernel", 6: "tt_cluster_kernel"}
+               4: "gemm_tc_kernel", 5: "gemm_kernel", 6: "tt_cluster_kernel",
+               7: "ttb_kernel"}
 OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5}
 
 # every symbol include/hb.h declares (checked by tests/test_abi.py)
@@ -50,7 +51,7 @@ class _Info(C.Structure):
                 ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64),
                 ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32),
                 ("kernel", C.c_int32), ("rows_per_cta", C.c_int32),
-                ("code_cell_bits", C.c_int32), ("reserved", C.c_int32)]
+                ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32)]
 
 
 def _load():

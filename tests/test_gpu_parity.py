@@ -134,26 +134,38 @@ def test_strategy_parity(strat, D, kind, cmp, monkeypatch):
     n = 1500 + seed % 97                 # several 512-row tiles + ragged tail
     Xd, Xh = X_pair(seed, n, F, special_q24=SPECIAL_Q24)
     # PTT has three node layouts: rank-coded 4-B records with 32- or 16-bit
-    # code cells, and fp32 8-B records
-    for rank, cw in ((("1", "32"), ("1", "16"), ("0", "0")) if strat == "ptt" else (("1", "0"),)):
+    # code cells (codes computed in the scorer, or by the pre-pass launch), and
+    # fp32 8-B records
+    layouts = (("1", "32", "0"), ("1", "16", "0"), ("1", "32", "1"), ("1", "16", "1"), ("0", "0", "0"))
+    for rank, cw, pre in (layouts if strat == "ptt" else (("1", "0", "0"),)):
         monkeypatch.setenv("HB_PTT_RANK", rank)
         monkeypatch.setenv("HB_RANK_CW", cw)
+        monkeypatch.setenv("HB_RANK_PRE", pre)
         m = hb.Model(e, strategy=strat, device=0)
         assert m.info["strategy_name"] == strat
         if strat == "ptt":
             assert m.info["node_record_bytes"] == (4 if rank == "1" else 8)
             assert m.info["code_cell_bits"] == int(cw)
+            assert m.info["rank_prepass"] == int(pre)
         check_all(e, m, Xd, Xh)
 
 
+def _set_layout(monkeypatch, rank):
+    """PTT node layout by name: "0" fp32 nodes; "1" / "16" rank-coded with
+    32- / 16-bit cells, codes in the scorer; "pre32" / "pre16" the same with
+    codes from the pre-pass launch."""
+    monkeypatch.setenv("HB_PTT_RANK", "0" if rank == "0" else "1")
+    monkeypatch.setenv("HB_RANK_CW", "16" if rank.endswith("16") else ("32" if rank == "pre32" else "0"))
+    monkeypatch.setenv("HB_RANK_PRE", "1" if rank.startswith("pre") else "0")
+
+
 @pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("rank", ["1", "0", "16"])
+@pytest.mark.parametrize("rank", ["1", "0", "16", "pre32", "pre16"])
 def test_ptt_special_thresholds(cmp, rank, monkeypatch):
     """Thresholds at +-Inf and -0/+0 (mixed on one feature) against X holding
     NaN, +-Inf, +-0 and exact ties: the rank code must reproduce every fp32
     decision (reading R3), for both PTT node layouts."""
-    monkeypatch.setenv("HB_PTT_RANK", "0" if rank == "0" else "1")
-    monkeypatch.setenv("HB_RANK_CW", "16" if rank == "16" else "0")
+    _set_layout(monkeypatch, rank)
     e = _forest("binary", 33, 6, 5, 17, "mixed", cmp, grid=synth.GRID_COARSE)
     rng = np.random.default_rng(3)
     internal = np.nonzero(e.left != -1)[0]
@@ -168,14 +180,17 @@ def test_ptt_special_thresholds(cmp, rank, monkeypatch):
 
 @pytest.mark.parametrize("kind", ["reg", "binary", "multiclass", "rf", "k7", "k12"])
 @pytest.mark.parametrize("cmp", [0, 1])
-def test_tt_wide_kernel_parity(kind, cmp, monkeypatch):
-    """The wide-row TT kernel (R rows per CTA, lanes = tree slot x row, nodes
-    through L1/L2, early exit) forced on ordinary inputs, plus its natural use
-    on F = 2000 rows."""
+@pytest.mark.parametrize("blocks", ["1", "0"])
+def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
+    """The wide-row TT kernels (R rows per CTA, lanes = tree slot x row, nodes
+    through L1/L2) forced on ordinary inputs: ttb_kernel (2-level node blocks,
+    persistent per-lane cursors) and tt_wide_kernel (8-B nodes, early exit)."""
     monkeypatch.setenv("HB_TT_WIDE", "1")
+    monkeypatch.setenv("HB_TT_BLOCK", blocks)
     seed = zlib.crc32(f"wide{kind}{cmp}".encode()) & 0xFFFF
     e = _forest(kind, 45, 9, 37, seed, FAMILIES[seed % 3], cmp)
     m = hb.Model(e, strategy="tt", device=0)
+    assert m.info["kernel_name"] == ("ttb_kernel" if blocks == "1" else "tt_wide_kernel")
     Xd, Xh = X_pair(seed, 1000 + seed % 53, 37, special_q24=SPECIAL_Q24)
     check_all(e, m, Xd, Xh)
 
@@ -184,8 +199,35 @@ def test_tt_wide_rows_natural():
     e = _forest("binary", 30, 12, 2000, 3, "mixed", 0)
     m = hb.Model(e, device=0)
     assert m.info["strategy_name"] == "tt" and m.info["x_in_smem"] == 1
+    assert m.info["kernel_name"] == "tt_wide_kernel"
     Xd, Xh = X_pair(5, 333, 2000, special_q24=SPECIAL_Q24)
     check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("cmp", [0, 1])
+@pytest.mark.parametrize("sync", ["1", "0"])
+def test_tt_blocks_tree_shapes(cmp, sync, monkeypatch):
+    """2-level node blocks on every shape that pads: single-leaf trees, a
+    stump, depth 2 (one full block) and 3 (a block plus leaf-only children),
+    left and right chains of odd and even depth (padding slots at every
+    level), bushy trees; more trees than a CTA has cursor slots (persistent
+    cursors take several trees each); rows not a multiple of the row tile."""
+    monkeypatch.setenv("HB_TT_WIDE", "1")
+    monkeypatch.setenv("HB_TT_BLOCK", "1")
+    monkeypatch.setenv("HB_TTB_SYNC", sync)
+    F = 9
+    trees = [dict(feature=[0], threshold=[0.0], left=[-1], right=[-1], leaf_value=[0.75]),
+             dict(feature=[2, 0, 0], threshold=[0.5, 0, 0], left=[1, -1, -1], right=[2, -1, -1],
+                  leaf_value=[0.0, -1.5, 2.25])]
+    trees += [_chain_tree(d, F, d, left_chain=d % 2 == 0) for d in (2, 3, 5, 6, 13)]
+    bushy = synth.gen_forest(300, 7, F, seed=4 + cmp, family="mixed", grid=synth.GRID_COARSE)
+    trees += [bushy.tree(i) for i in range(300)]
+    trees += [dict(feature=[5], threshold=[0.0], left=[-1], right=[-1], leaf_value=[-0.125])]
+    e = synth.from_trees(trees, F, cmp=cmp)
+    m = hb.Model(e, strategy="tt", device=0)
+    assert m.info["kernel_name"] == "ttb_kernel"
+    Xd, Xh = X_pair(12, 2111, F, grid=synth.GRID_COARSE, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh, kinds=("predict", "raw", "leaf", "leaf_hash"))
 
 
 @pytest.mark.parametrize("kind", ["k7", "k12", "rf_reg"])
@@ -587,11 +629,56 @@ def test_sixteen_outputs_vector_leaves(strat, small, monkeypatch):
     check_all(e, m, Xd, Xh)
 
 
+@pytest.mark.parametrize("cmp", [0, 1])
+@pytest.mark.parametrize("cw", ["32", "16"])
+def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
+    """Bucketed rank search of the pre-pass (hb_rank_codes.cu) at its edges:
+    a feature with ~35K distinct thresholds (16384 buckets, table searched from
+    global memory), thresholds at +-FLT_MAX / denormals / a few-ulp cluster
+    (tiny bucket range), a single-threshold feature, a feature whose only
+    finite threshold sits between +-Inf ones; X holds every threshold, its fp32
+    neighbours, NaN, +-Inf and +-0. Every decision must equal the fp32 walk."""
+    _set_layout(monkeypatch, "pre" + cw)
+    rng = np.random.default_rng(40 + cmp)
+    F = 5
+    e = synth.gen_forest(400, 8, F, seed=41, family="balanced", cmp=cmp,
+                         post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
+    internal = np.nonzero(e.left != -1)[0]
+    feat = rng.choice(F, internal.size, p=[0.8, 0.05, 0.05, 0.05, 0.05]).astype(np.int32)
+    e.feature[internal] = feat
+    f32 = np.float32
+    fmax = np.finfo(f32).max
+    tiny = np.finfo(f32).smallest_subnormal
+    pools = {
+        0: (rng.integers(-2**20, 2**20, 40000) * 2.0**-10).astype(f32),
+        1: np.array([fmax, -fmax, 3e38, -3e38, tiny, -tiny, 2 * tiny, 1.0,
+                     np.nextafter(f32(1), f32(2)), np.nextafter(f32(1), f32(0)),
+                     np.nextafter(np.nextafter(f32(1), f32(2)), f32(2))], f32),
+        2: np.array([0.5], f32),
+        3: np.array([np.inf, -np.inf, -2.0], f32),
+        4: np.array([1.0, np.nextafter(f32(1), f32(2)), np.nextafter(f32(1), f32(0))], f32),
+    }
+    for f, pool in pools.items():
+        idx = internal[feat == f]
+        e.threshold[idx] = pool[rng.integers(0, pool.size, idx.size)]
+    n = 3000
+    Xh = np.empty((n, F), f32)
+    specials = np.array([np.nan, np.inf, -np.inf, 0.0, -0.0, fmax, -fmax], f32)
+    for f, pool in pools.items():
+        cand = np.concatenate([pool, np.nextafter(pool, f32(np.inf)), np.nextafter(pool, f32(-np.inf)),
+                               specials])
+        Xh[:, f] = cand[rng.integers(0, cand.size, n)]
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["node_record_bytes"] == 4 and m.info["rank_prepass"] == 1
+    assert m.info["code_cell_bits"] == int(cw)
+    Xd = torch.from_numpy(Xh).cuda()
+    check_all(e, m, Xd, Xh)
+
+
 @pytest.mark.parametrize("D", [1, 2, 9, 10])
-@pytest.mark.parametrize("rank", ["0", "1", "16"])
+@pytest.mark.parametrize("rank", ["0", "1", "16", "pre32", "pre16"])
 def test_ptt_depth_range(D, rank, monkeypatch):
-    monkeypatch.setenv("HB_PTT_RANK", "0" if rank == "0" else "1")
-    monkeypatch.setenv("HB_RANK_CW", "16" if rank == "16" else "0")
+    _set_layout(monkeypatch, rank)
     e = synth.gen_forest(13, D, 10, seed=D, family="skinny", post=synth.POST_SIGMOID,
                          task=synth.TASK_CLASSIFICATION, base_score=[0.125])
     m = hb.Model(e, strategy="ptt", device=0)
