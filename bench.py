@@ -320,8 +320,14 @@ def run_ours(args):
     roofline = {
         "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "mean_levels_per_tree": levels,
-        "traffic": prof.get("smem_ld_bytes_per_launch") if same_launch else None,
-        "traffic_dram": prof.get("dram_bytes_per_launch") if same_launch else None,
+        # contract: traffic = dram__bytes_read.sum + dram__bytes_write.sum per
+        # launch (one ncu --set full capture); the kernel is bound on chip, so
+        # the comparable figure for achieved/algorithmic bytes is the SMEM one
+        "traffic": prof.get("dram_bytes_per_launch") if same_launch else None,
+        "traffic_smem": prof.get("smem_ld_bytes_per_launch") if same_launch else None,
+        "traffic_note": "traffic = DRAM bytes per launch (X + output when the model is L2-resident); "
+                        "traffic_smem = SMEM load wavefronts x 128 B per launch, the on-chip "
+                        "counterpart of the algorithmic bytes",
         "traffic_source": prof.get("source"),
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
         "kernel_ms_covers": ("rank_code_kernel + pttr_kernel (both launches of one hb_predict call; "

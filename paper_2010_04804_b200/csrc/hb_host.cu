@@ -548,6 +548,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.t_smem = 0;
         c.ch = kTreeGroup;
         m->cfg = c;
+        m->tt_g = env_int("HB_TT_G", 4);
         // opt-in (HB_TT_BLOCK=1): 2-level node blocks walked by per-lane
         // cursors (hb_ttb.cu); measured slower than
         // tt_wide_kernel on C5, so AUTO keeps tt_wide_kernel

@@ -70,7 +70,7 @@ struct Model {
   int rank_pre = 0;
   int rank_nwords = 0;       // 32-bit code words per row (n_fc or ceil(n_fc / 2))
   void *d_rb = nullptr;      // [feat | groups | bucket tables]
-  size_t rb_groups_off = 0, rb_pool_off = 0, rb_smem = 0;
+  size_t rb_groups_off = 0, rb_pool_off = 0, rb_smem = 0, rb_smem_cap = 0;
   int rb_ngroups = 0;
   cudaMemPool_t mempool = nullptr;
 
@@ -103,6 +103,7 @@ struct Model {
   size_t ttb_leaf_off = 0, ttb_lorig_off = 0, ttb_cls_off = 0;
   int64_t ttb_nblocks = 0;
   int ttb_sync = 1;          // lanes of a warp advance a cursor together
+  int tt_g = 4;              // tt_wide_kernel: concurrent walks per lane (4, 6, 8)
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
@@ -144,6 +145,7 @@ struct RankBuckets {
   std::vector<uint8_t> pool;
   int n_groups = 0, n_words = 0;
   size_t max_group_bytes = 0;     // largest SMEM-resident group
+  size_t smem_cap = 0;            // groups up to this size are staged in SMEM
 };
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
                              int cw, RankBuckets *out);

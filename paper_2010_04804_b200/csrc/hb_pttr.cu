@@ -300,6 +300,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     m->rb_pool_off = pool_off;
     m->rb_ngroups = R.n_groups;
     m->rb_smem = R.max_group_bytes;
+    m->rb_smem_cap = R.smem_cap;
     m->rank_nwords = R.n_words;
     m->rank_ngroups = 0;
     // per-call code scratch: stream-ordered allocations from a model-owned

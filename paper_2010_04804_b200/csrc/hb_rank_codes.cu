@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -34,7 +35,7 @@ namespace hb {
 namespace {
 
 constexpr int kRcWarps = 8;                 // warps per CTA of the pre-pass
-constexpr uint32_t kRcSmemCap = 48 * 1024;  // per-CTA table budget (4 CTAs / SM)
+constexpr uint32_t kRcSmemMax = 200 * 1024; // largest per-CTA table budget
 constexpr int kRcBatch = 16;                // X loads in flight together per lane
 constexpr int kRcRows = 4;                  // 32-row blocks per warp iteration
 
@@ -45,30 +46,36 @@ struct RankCodeParams {
   const uint4 *groups;    // [n_groups] {pool byte offset, bytes, word_begin, word_end}
   const uint8_t *pool;
   int n_fc, n_words;
+  int pair_loads;         // CW 16: word w = features 2w, 2w+1 = one aligned float2 of X
+  uint32_t smem_cap;      // groups up to this size are staged in SMEM
   uint32_t *codes;        // [nblocks][n_words][32]
   int64_t nblocks;
 };
 
 template <bool LE>
 __device__ __forceinline__ uint32_t rank_code(float x, const uint4 m0, const uint4 m1, const uint8_t *tb) {
-  if (x != x) return 0xFFFFu;
+  // branch-free: NaN clamps to lo (fmaxf), walks bucket 0 (compares false)
+  // and is replaced by 0xFFFF at the end
   const float lo = __uint_as_float(m1.x), hi = __uint_as_float(m1.y), s = __uint_as_float(m1.z);
   const float xc = fminf(fmaxf(x, lo), hi);
   float y = __fmul_rn(__fsub_rn(xc, lo), s);
   y = fminf(y, (float)(m0.y - 1u));
   const uint32_t b = __float2uint_rz(y);
-  const uint16_t *start = reinterpret_cast<const uint16_t *>(tb + m0.w);
+  // bucket entry: first threshold index | count << 16 (one load)
+  const uint32_t be = reinterpret_cast<const uint32_t *>(tb + m0.w)[b];
   const float *u = reinterpret_cast<const float *>(tb + m1.w);
-  uint32_t base = start[b];
-  uint32_t cnt = (uint32_t)start[b + 1] - base;
-  for (uint32_t k = 0; k < m0.z; ++k) {
+  uint32_t base = be & 0xFFFFu;
+  uint32_t cnt = be >> 16;
+#pragma unroll
+  for (uint32_t k = 0; k < 16; ++k) {
+    if (k >= m0.z) break;                      // S steps (warp-uniform)
     const uint32_t half = cnt >> 1;
     const float v = u[base + half];              // u has one pad slot: in range when cnt == 0
     const bool go = cnt != 0 && (LE ? v < x : v <= x);
     base = go ? base + half + 1u : base;
     cnt = go ? cnt - half - 1u : half;
   }
-  return base;
+  return x != x ? 0xFFFFu : base;
 }
 
 template <bool LE, int CW>
@@ -76,7 +83,7 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankC
   extern __shared__ __align__(16) uint8_t smem[];
   const uint4 g = __ldg(p.groups + blockIdx.y);
   const uint8_t *tb = p.pool + g.x;
-  if (g.y <= kRcSmemCap) {
+  if (g.y <= p.smem_cap) {
     const uint4 *src = reinterpret_cast<const uint4 *>(tb);
     uint4 *dst = reinterpret_cast<uint4 *>(smem);
     for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
@@ -93,20 +100,32 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankC
   constexpr int NB = kRcBatch / (kRcRows * PW) > 0 ? kRcBatch / (kRcRows * PW) : 1;   // words per batch
   for (int64_t rb0 = ((int64_t)blockIdx.x * kRcWarps + warp) * kRcRows; rb0 < p.nblocks;
        rb0 += (int64_t)gridDim.x * kRcWarps * kRcRows) {
+    // rows past n (and row blocks past the end) read row 0 and are not stored
+    const float *xr[kRcRows];
+#pragma unroll
+    for (int i = 0; i < kRcRows; ++i) {
+      const int64_t row = (rb0 + i) * 32 + lane;
+      xr[i] = p.X + (row < p.n ? row : 0) * p.ldx;
+    }
     for (int w0 = (int)g.z; w0 < (int)g.w; w0 += NB) {
       float xv[kRcRows][NB][PW];
 #pragma unroll
-      for (int i = 0; i < kRcRows; ++i) {
-        const int64_t row = (rb0 + i) * 32 + lane;
-        const bool in = row < p.n;
-        const float *xr = p.X + (in ? row : 0) * p.ldx;
+      for (int j = 0; j < NB; ++j) {
+        const int wc = min(w0 + j, (int)g.w - 1);   // clamped: loads stay unconditional
+        if (PW == 2 && p.pair_loads) {
+          // word = features 2w, 2w+1 = X columns 2w, 2w+1: one 8-B load
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
+          for (int i = 0; i < kRcRows; ++i) {
+            const float2 v = __ldg(reinterpret_cast<const float2 *>(xr[i] + 2 * wc));
+            xv[i][j][0] = v.x;
+            xv[i][j][PW - 1] = v.y;
+          }
+        } else {
 #pragma unroll
           for (int q = 0; q < PW; ++q) {
-            const int fc = min((w0 + j) * PW + q, p.n_fc - 1);
-            const uint32_t f = __ldg(reinterpret_cast<const uint32_t *>(p.feat + 2 * fc));
-            xv[i][j][q] = (in && w0 + j < (int)g.w) ? __ldg(xr + f) : 0.f;
+            const uint32_t f = __ldg(reinterpret_cast<const uint32_t *>(p.feat + 2 * min(wc * PW + q, p.n_fc - 1)));
+#pragma unroll
+            for (int i = 0; i < kRcRows; ++i) xv[i][j][q] = __ldg(xr[i] + f);
           }
         }
       }
@@ -120,7 +139,6 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankC
         const uint4 b0 = __ldg(p.feat + 2 * (has1 ? f1 : f0)), b1 = __ldg(p.feat + 2 * (has1 ? f1 : f0) + 1);
 #pragma unroll
         for (int i = 0; i < kRcRows; ++i) {
-          if (rb0 + i >= p.nblocks) break;
           uint32_t word;
           if (CW == 32) {
             word = ((uint32_t)wd << 23) | rank_code<LE>(xv[i][j][0], a0, a1, tb);
@@ -129,7 +147,7 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankC
             const uint32_t c1 = has1 ? rank_code<LE>(xv[i][j][PW - 1], b0, b1, tb) : 0u;
             word = c0 | (c1 << 16);
           }
-          p.codes[((size_t)(rb0 + i) * p.n_words + wd) * 32 + lane] = word;
+          if (rb0 + i < p.nblocks) p.codes[((size_t)(rb0 + i) * p.n_words + wd) * 32 + lane] = word;
         }
       }
     }
@@ -159,6 +177,10 @@ uint32_t host_bucket(float x, float lo, float hi, float s, uint32_t B) {
 // (sorted[c], feature id orig[c]); words group 1 (CW 32) or 2 (CW 16) features.
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
                              int cw, RankBuckets *out) {
+  // per-CTA table budget: 48 KB -> 4 CTAs (32 warps) per SM (HB_RC_SMEM_KB overrides)
+  const char *ev = std::getenv("HB_RC_SMEM_KB");
+  const size_t cap = std::min<size_t>(kRcSmemMax, (ev && *ev ? (size_t)std::atoi(ev) : 48) * 1024);
+  out->smem_cap = cap;
   const int n_fc = (int)sorted.size();
   const int per_word = cw == 32 ? 1 : 2;
   const int n_words = (n_fc + per_word - 1) / per_word;
@@ -178,7 +200,7 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
         any = true;
       }
     uint32_t B = 1;
-    while (B < m && B < 16384u) B <<= 1;
+    while (2 * B < m && B < 16384u) B <<= 1;     // <= 2 thresholds per bucket on average
     float s = 0.f;
     if (hi > lo) {
       const float range = hi - lo;
@@ -202,12 +224,12 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     }
     uint32_t S = 0;
     while ((1u << S) <= maxocc) ++S;        // bit_length(maxocc) search steps
-    const size_t sbytes = ((size_t)(B + 1) * 2 + 3) & ~size_t(3);
+    const size_t sbytes = (size_t)B * 4;
     const size_t ubytes = ((size_t)(m + 1) * 4);
     std::vector<uint8_t> t(sbytes + ubytes, 0);
-    for (uint32_t b = 0; b <= B; ++b) {
-      const uint16_t v = (uint16_t)start[b];
-      std::memcpy(t.data() + 2 * b, &v, 2);
+    for (uint32_t b = 0; b < B; ++b) {
+      const uint32_t v = start[b] | ((start[b + 1] - start[b]) << 16);
+      std::memcpy(t.data() + 4 * b, &v, 4);
     }
     std::memcpy(t.data() + sbytes, u.data(), (size_t)m * 4);
     const float pad = INFINITY;
@@ -223,13 +245,13 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     std::memcpy(&fm[6], &s, 4);
     fm[7] = (uint32_t)sbytes;                  // u offset relative to start; rebased below
   }
-  // groups of whole words, <= kRcSmemCap bytes each (an oversized word is a
+  // groups of whole words, <= cap bytes each (an oversized word is a
   // group of its own and is searched from global memory)
   size_t goff = 0, gbytes = 0;
   int wbeg = 0;
   auto close = [&](int wend) {
     R.groups.insert(R.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)wbeg, (uint32_t)wend});
-    R.max_group_bytes = std::max(R.max_group_bytes, gbytes <= kRcSmemCap ? gbytes : (size_t)0);
+    R.max_group_bytes = std::max(R.max_group_bytes, gbytes <= cap ? gbytes : (size_t)0);
     goff += gbytes;
     gbytes = 0;
     wbeg = wend;
@@ -238,7 +260,7 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
   for (int wd = 0; wd < n_words; ++wd) {
     size_t wb = 0;
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
-    if (gbytes > 0 && gbytes + wb > kRcSmemCap) close(wd);
+    if (gbytes > 0 && gbytes + wb > cap) close(wd);
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) {
       const int c = wd * per_word + q;
       uint32_t *fm = R.feat.data() + (size_t)c * 8;
@@ -251,6 +273,7 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     }
   }
   if (gbytes) close(n_words);
+  R.smem_cap = cap;
   *out = std::move(R);
   return HB_OK;
 }
@@ -271,11 +294,16 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   p.n_words = m.rank_nwords;
   p.codes = codes;
   p.nblocks = nblocks;
+  p.smem_cap = (uint32_t)m.rb_smem_cap;
+  p.pair_loads = m.rank_cw == 16 && m.rank_nfc == m.n_features && m.n_features % 2 == 0 &&
+                 a.ldx % 2 == 0 && (reinterpret_cast<uintptr_t>(a.X) & 7) == 0;
   const int smem = (int)m.rb_smem;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(rank codes)");
-  // ~4 CTAs per SM in total, spread over the feature groups (blockIdx.y)
-  const int64_t want = std::max<int64_t>(1, (4LL * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
+  // as many CTAs as fit per SM (by table SMEM, at most 4), spread over the
+  // feature groups (blockIdx.y)
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / std::max<size_t>(m.rb_smem_cap, 1)));
+  const int64_t want = std::max<int64_t>(1, ((int64_t)per_sm * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (nblocks + kRcWarps * kRcRows - 1) / (kRcWarps * kRcRows)));
   fn<<<dim3(gx, m.rb_ngroups), 32 * kRcWarps, smem, a.stream>>>(p);
   e = cudaGetLastError();

@@ -216,11 +216,10 @@ __device__ __forceinline__ void wide_step(const uint2 *n, uint32_t &i, const flo
   i = nx;
 }
 
-template <bool LE, int NACC, int R>
+template <bool LE, int NACC, int R, int G>           // G: trees walked at once per lane
 __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int L = 32 / R;                       // tree slots per warp
-  constexpr int G = 4;                            // trees walked at once per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int sub = lane / R, r = lane % R;
@@ -343,21 +342,24 @@ static TtFn pick_nacc(int nacc) {
 int sm_count(int device);
 
 template <bool LE, int R>
-static TtFn pick_wide_nacc(int nacc) {
+static TtFn pick_wide_nacc(int nacc, int g) {
+  // 6 or 8 concurrent walks per lane only for scalar outputs (register budget)
+  if (nacc == 1 && g >= 8) return tt_wide_kernel<LE, 1, R, 8>;
+  if (nacc == 1 && g >= 6) return tt_wide_kernel<LE, 1, R, 6>;
   switch (nacc) {
-    case 1: return tt_wide_kernel<LE, 1, R>;
-    case 4: return tt_wide_kernel<LE, 4, R>;
-    case 8: return tt_wide_kernel<LE, 8, R>;
-    default: return tt_wide_kernel<LE, 16, R>;
+    case 1: return tt_wide_kernel<LE, 1, R, 4>;
+    case 4: return tt_wide_kernel<LE, 4, R, 4>;
+    case 8: return tt_wide_kernel<LE, 8, R, 4>;
+    default: return tt_wide_kernel<LE, 16, R, 4>;
   }
 }
 
 template <bool LE>
-static TtFn pick_wide(int R, int nacc) {
+static TtFn pick_wide(int R, int nacc, int g) {
   switch (R) {
-    case 32: return pick_wide_nacc<LE, 32>(nacc);
-    case 16: return pick_wide_nacc<LE, 16>(nacc);
-    default: return pick_wide_nacc<LE, 8>(nacc);
+    case 32: return pick_wide_nacc<LE, 32>(nacc, g);
+    case 16: return pick_wide_nacc<LE, 16>(nacc, g);
+    default: return pick_wide_nacc<LE, 8>(nacc, g);
   }
 }
 
@@ -368,8 +370,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
     if (st != HB_E_UNSUPPORTED) return st;   // unaligned rows: tt_wide_kernel below
   }
   const bool wide = m.cfg.wide_rows > 0;
-  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc)
-                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc))
+  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g)
+                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g))
                  : (m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc));
   TtParams p;
   p.X = a.X;

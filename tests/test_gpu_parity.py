@@ -640,11 +640,11 @@ def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
     neighbours, NaN, +-Inf and +-0. Every decision must equal the fp32 walk."""
     _set_layout(monkeypatch, "pre" + cw)
     rng = np.random.default_rng(40 + cmp)
-    F = 5
+    F = 6     # even and all used: 16-bit cells load feature pairs as one float2
     e = synth.gen_forest(400, 8, F, seed=41, family="balanced", cmp=cmp,
                          post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
     internal = np.nonzero(e.left != -1)[0]
-    feat = rng.choice(F, internal.size, p=[0.8, 0.05, 0.05, 0.05, 0.05]).astype(np.int32)
+    feat = rng.choice(F, internal.size, p=[0.75, 0.05, 0.05, 0.05, 0.05, 0.05]).astype(np.int32)
     e.feature[internal] = feat
     f32 = np.float32
     fmax = np.finfo(f32).max
@@ -657,6 +657,7 @@ def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
         2: np.array([0.5], f32),
         3: np.array([np.inf, -np.inf, -2.0], f32),
         4: np.array([1.0, np.nextafter(f32(1), f32(2)), np.nextafter(f32(1), f32(0))], f32),
+        5: np.array([-tiny, 0.0, tiny, -1e-30, 1e-30], f32),
     }
     for f, pool in pools.items():
         idx = internal[feat == f]
@@ -673,6 +674,14 @@ def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
     assert m.info["code_cell_bits"] == int(cw)
     Xd = torch.from_numpy(Xh).cuda()
     check_all(e, m, Xd, Xh)
+    # odd row stride: 16-bit cells fall back to one load per feature
+    Xp = np.zeros((n, F + 1), f32)
+    Xp[:, :F] = Xh
+    Xpd = torch.from_numpy(Xp).cuda()
+    for kind in ("raw", "leaf"):
+        a = m.run(Xpd[:, :F], kind).cpu().numpy()
+        b = m.run(Xd, kind).cpu().numpy()
+        assert np.array_equal(a, b), kind
 
 
 @pytest.mark.parametrize("D", [1, 2, 9, 10])
