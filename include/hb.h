@@ -16,7 +16,12 @@
  *  - Device pointers: X / out of the hb_predict* family are caller-owned
  *    DEVICE pointers on the model's device (checked with
  *    cudaPointerGetAttributes; host or foreign-device pointers give
- *    HB_E_INVALID). The library never allocates per call on these paths.
+ *    HB_E_INVALID). The only per-call device memory is the scratch of the
+ *    rank-code pre-pass (models with hb_model_info.rank_prepass = 1): one
+ *    stream-ordered allocation of ceil(n_rows / 32) * 128 * words bytes from
+ *    a pool the model owns and keeps warm (cudaMallocFromPoolAsync /
+ *    cudaFreeAsync on `stream`; no device-wide synchronisation; HB_E_OOM if
+ *    it cannot be satisfied). It is also capturable in a CUDA graph.
  *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *    stream). Calls only enqueue work and return once the launch succeeded;
  *    asynchronous kernel faults surface at the caller's synchronisation.

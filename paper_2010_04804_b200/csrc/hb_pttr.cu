@@ -339,7 +339,13 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   if (m.rank_pre) {
     const int64_t nblocks = (a.n + 31) / 32;
     const size_t bytes = std::max<size_t>((size_t)nblocks * m.rank_nwords * 128, 128);
-    e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&codes), bytes, m.mempool, a.stream);
+    // under stream capture the allocation becomes a graph memory node, which
+    // CUDA supports for the device's default pool
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(a.stream, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusNone;
+    e = cap == cudaStreamCaptureStatusActive
+            ? cudaMallocAsync(reinterpret_cast<void **>(&codes), bytes, a.stream)
+            : cudaMallocFromPoolAsync(reinterpret_cast<void **>(&codes), bytes, m.mempool, a.stream);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync(rank codes)");
     const hb_status st = launch_rank_codes(m, a, codes, nblocks);
     if (st != HB_OK) {

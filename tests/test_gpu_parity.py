@@ -430,9 +430,16 @@ def test_rejects_host_pointers_and_bad_args():
         m.predict(torch.zeros(10, 4, device="cuda"))   # ldx < F
 
 
-def test_streams_and_concurrency():
+@pytest.mark.parametrize("pre", ["0", "1"])
+def test_streams_and_concurrency(pre, monkeypatch):
+    """One model scoring on four streams at once; with the rank-code pre-pass
+    every call takes its own stream-ordered scratch from the model's pool."""
+    monkeypatch.setenv("HB_RANK_PRE", pre)
+    if pre == "1":
+        monkeypatch.setenv("HB_PTT_RANK", "1")
     e = _forest("binary", 64, 8, 28, 2, "balanced", 0)
     m = hb.Model(e, device=0)
+    assert m.info["rank_prepass"] == int(pre)
     Xd, Xh = X_pair(3, 20000, 28)
     ref = m.predict_proba(Xd).cpu()
     streams = [torch.cuda.Stream() for _ in range(4)]
@@ -443,6 +450,36 @@ def test_streams_and_concurrency():
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o.cpu(), ref)      # same kernel, same order: identical
+
+
+@pytest.mark.parametrize("pre,n", [("0", 20000), ("1", 20000), ("0", 300)])
+def test_cuda_graph_capture(pre, n, monkeypatch):
+    """hb_predict under CUDA-graph capture (the bench's small-batch timing and
+    a serving loop use it): row-tile scorer, rank-code pre-pass (its
+    stream-ordered scratch becomes graph memory nodes) and small-batch kernel;
+    replays equal eager calls bit for bit."""
+    monkeypatch.setenv("HB_RANK_PRE", pre)
+    monkeypatch.setenv("HB_SMALL_BATCH", "4096")
+    if pre == "1":
+        monkeypatch.setenv("HB_PTT_RANK", "1")
+    e = _forest("binary", 64, 8, 28, 21, "balanced", 0)
+    m = hb.Model(e, device=0)
+    Xd, Xh = X_pair(21, n, 28)
+    ref = m.predict_proba(Xd).cpu()
+    out = torch.empty_like(ref, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        m.run(Xd, "proba", out=out, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(3):
+            m.run(Xd, "proba", out=out, stream=s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), ref)
 
 
 def test_tree_shard_partials_reduce_to_unsharded():
@@ -469,7 +506,9 @@ def test_tree_shard_partials_reduce_to_unsharded():
 
 
 @pytest.mark.parametrize("kind", ["predict", "proba", "raw", "leaf_hash"])
-def test_predict_host_end_to_end(kind):
+@pytest.mark.parametrize("pre", ["0", "1"])
+def test_predict_host_end_to_end(kind, pre, monkeypatch):
+    monkeypatch.setenv("HB_RANK_PRE", pre)
     e = _forest("binary", 50, 8, 28, 7, "balanced", 0)
     m = hb.Model(e, device=0)
     n = 300_000
