@@ -216,8 +216,10 @@ def run_ours(args):
 
         def step():
             m.run(X, kind, out=out, stream=stream)
-        # rank-code pre-pass models launch rank_code_kernel + pttr_kernel per call
-        launches_per_step = 2 if m.info.get("rank_prepass") else 1
+        # rank-code pre-pass models launch rank_code_kernel + pttr_kernel per
+        # call, except on the small-batch path (one kernel)
+        small = n <= int(os.environ.get("HB_SMALL_BATCH", "4096"))
+        launches_per_step = 2 if m.info.get("rank_prepass") and not small else 1
     else:
         # trees sharded, all rows on every rank; one NCCL reduce of fp32
         # partials to rank 0, which finalizes (strong scaling)
@@ -354,7 +356,7 @@ def run_ours(args):
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
         "kernel_ms_covers": ("rank_code_kernel + pttr_kernel (both launches of one hb_predict call; "
                              "their split is in the ncu launch list under profiles/)")
-        if info.get("rank_prepass") else kname,
+        if info.get("rank_prepass") and kname != "small_batch_kernel" else kname,
         "algorithmic_bytes_per_row": per_row,
         "peak_source": ("measured L2 read microbenchmark (tools/peaks.cu), this run" if l2_wide else
                         "measured LDS.128 microbenchmark (tools/peaks.cu), this run")

@@ -46,3 +46,44 @@ def test_gpu_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 300000 * 28 * 4
     assert d["gpu_launches"] == 3 and d["scaling"] == "weak" and d["n_gpus"] == 1
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+@pytest.mark.gpu
+def test_gpu_arm_small_batch_graph_and_prepass():
+    """C1 (150 rows) is timed through a CUDA graph of 200 calls per step; a
+    C2-shaped run (rank-code pre-pass) counts two launches per call."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    d = _run(["--config", "C1", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e"])
+    assert d["gpu_launches"] == 3 * 200 and "CUDA graph" in d["config"]["timing"]
+    assert d["roofline"]["kernel"] == "small_batch_kernel" and d["value"] > 0
+    d = _run(["--config", "C2", "--steps", "3", "--warmup", "3", "--rows", "200000", "--no-cpu",
+              "--no-e2e"])
+    assert d["roofline"]["layout"] == "ptt-rank-pre" and d["gpu_launches"] == 6
+
+
+def _torchrun(args, timeout=900):
+    env = dict(os.environ, HB_BENCH_ONE_DEVICE="1", HB_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2"] + args
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert out.returncode == 0 and len(lines) == 1, out.stdout[-2000:] + out.stderr[-3000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,extra", [("C3", ["--rows", "200000"]), ("C5", ["--rows", "2000"])])
+def test_multi_rank_bench_on_one_device(cfg, extra):
+    """The torchrun path of bench.py (2 ranks; both on this box's one GPU,
+    gloo for the collectives): row shards with no data-path collective (C3),
+    tree shards + one reduce of fp32 partials + finalize on rank 0 (C5)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    d = _torchrun(["--config", cfg, "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e"] + extra)
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["scaling"] == ("weak" if cfg == "C3" else "strong")
+    assert d["config"]["trees_per_gpu"] == (500 if cfg == "C3" else 5000)

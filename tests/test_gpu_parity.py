@@ -705,8 +705,9 @@ def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
     Xh = np.empty((n, F), f32)
     specials = np.array([np.nan, np.inf, -np.inf, 0.0, -0.0, fmax, -fmax], f32)
     for f, pool in pools.items():
-        cand = np.concatenate([pool, np.nextafter(pool, f32(np.inf)), np.nextafter(pool, f32(-np.inf)),
-                               specials])
+        with np.errstate(over="ignore"):     # nextafter(FLT_MAX, inf) = inf is wanted
+            up, down = np.nextafter(pool, f32(np.inf)), np.nextafter(pool, f32(-np.inf))
+        cand = np.concatenate([pool, up, down, specials])
         Xh[:, f] = cand[rng.integers(0, cand.size, n)]
     m = hb.Model(e, strategy="ptt", device=0)
     assert m.info["node_record_bytes"] == 4 and m.info["rank_prepass"] == 1
