@@ -535,7 +535,9 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         const int nacc = K == 1 ? 1 : (K <= 4 ? 4 : (K <= 8 ? 8 : 16));
         c.nw = 32;
         c.wide_rows = 0;
+        const int force_r = env_int("HB_TT_WIDE_ROWS", 0);   // tuning override (32/16/8)
         for (int R : {32, 16, 8}) {
+          if (force_r && R != force_r) continue;
           const long bytes = (long)fmap.used.size() * R * 4 + (long)c.nw * R * (4L * nacc + 8);
           if (bytes <= kSmemBudget) {
             c.wide_rows = R;

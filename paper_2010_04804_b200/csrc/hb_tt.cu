@@ -34,6 +34,7 @@ struct TtParams {
   int K, w, task, post, kind;
   void *out;
   int nw, ns, ch, ntiles, x_smem, t_smem;
+  int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
 };
 
 template <bool LE>
@@ -231,12 +232,30 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row0 = (int64_t)tile * R;
     // coalesced X tile load: consecutive threads -> consecutive features of a row
-    for (int idx = threadIdx.x; idx < R * p.F; idx += blockDim.x) {
-      const int rr = idx / p.F, f = idx - rr * p.F;
-      const int64_t gr = row0 + rr;
-      const int fo = p.fmap ? __ldg(p.fmap + f) : f;
-      xs[f * R + (rr ^ xw_swz<R>(f))] = gr < p.n ? __ldg(p.X + gr * p.ldx + fo) : 0.f;
+    if (!p.fmap && p.vec4 && (p.F & 3) == 0) {
+      const int F4 = p.F >> 2;
+      for (int idx = threadIdx.x; idx < R * F4; idx += blockDim.x) {
+        const int rr = idx / F4, f = 4 * (idx - rr * F4);
+        const int64_t gr = row0 + rr;
+        const float4 v = gr < p.n ? __ldg(reinterpret_cast<const float4 *>(p.X + gr * p.ldx + f))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        xs[(f + 0) * R + (rr ^ xw_swz<R>(f + 0))] = v.x;
+        xs[(f + 1) * R + (rr ^ xw_swz<R>(f + 1))] = v.y;
+        xs[(f + 2) * R + (rr ^ xw_swz<R>(f + 2))] = v.z;
+        xs[(f + 3) * R + (rr ^ xw_swz<R>(f + 3))] = v.w;
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < R * p.F; idx += blockDim.x) {
+        const int rr = idx / p.F, f = idx - rr * p.F;
+        const int64_t gr = row0 + rr;
+        const int fo = p.fmap ? __ldg(p.fmap + f) : f;
+        xs[f * R + (rr ^ xw_swz<R>(f))] = gr < p.n ? __ldg(p.X + gr * p.ldx + fo) : 0.f;
+      }
     }
+    // warm L2 with the next tile's rows while this one is walked (the fill
+    // above is not overlapped with compute: one 8 KB row per lane group)
+    if (threadIdx.x == 0 && p.x_prefetch)
+      dev::prefetch_rows_l2(p.X, (int64_t)(tile + gridDim.x) * R, R, p.n, p.ldx);
     __syncthreads();
     const int64_t row = row0 + r;
     float acc[NACC];
@@ -401,6 +420,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.ch = m.cfg.ch;
   p.x_smem = m.cfg.x_smem;
   p.t_smem = m.cfg.t_smem;
+  p.x_prefetch = m.cfg.prefetch;
   const int64_t rows_per_tile = wide ? (int64_t)m.cfg.wide_rows : (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");

@@ -22,6 +22,12 @@ cases = [
     ("tt-wide", synth.gen_forest(24, 11, 12, seed=2, family="mixed"), {"HB_TT_WIDE": "1"}, "tt"),
     ("ptt-rank-wrap", synth.gen_forest(300, 8, 12, seed=4), {"HB_PTT_RANK": "1", "HB_CH": "8"}, "ptt"),
     ("ptt-fp32-wrap", synth.gen_forest(300, 8, 12, seed=4), {"HB_PTT_RANK": "0", "HB_CH": "8"}, "ptt"),
+    ("ptt-rank-prepass-32", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32"}, "ptt"),
+    ("ptt-rank-prepass-16", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16"}, "ptt"),
+    ("tt-blocks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
+     {"HB_TT_WIDE": "1", "HB_TT_BLOCK": "1"}, "tt"),
     ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
     ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
 ]
