@@ -181,7 +181,9 @@ hb_status hb_compile(const hb_ensemble *e, int32_t strategy, int32_t device, hb_
 hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tree_end,
                            int32_t strategy, int32_t device, hb_model **out);
 
-/* One fused scoring launch writing `kind` (hb_output) for rows [0, n_rows). */
+/* One fused scoring launch writing `kind` (hb_output) for rows [0, n_rows)
+ * (two for rank_prepass models on more than the small-batch row count: the
+ * rank-code pre-pass, then the scorer; both on `stream`). */
 hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                         int32_t kind, void *out, void *stream);
 

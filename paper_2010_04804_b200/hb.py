@@ -171,7 +171,7 @@ class Model:
         raise ValueError(kind)
 
     def run(self, X, kind="predict", out=None, stream=None):
-        """One fused scoring launch (hb_predict_ex) on torch CUDA tensors.
+        """One fused scoring launch (hb_predict_ex; two with the rank-code pre-pass) on torch CUDA tensors.
         X: float32 [n, >= F] with unit column stride. Returns `out`."""
         import torch
         if X.dtype != torch.float32 or X.dim() != 2 or X.stride(1) != 1:
