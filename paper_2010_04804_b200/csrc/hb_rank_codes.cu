@@ -281,6 +281,7 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
 int sm_count(int device);
 
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks) {
+  if (m.rb_ngroups == 0 || nblocks == 0) return HB_OK;   // no split uses any feature: no codes
   RcFn fn = rc_pick(m.cmp == HB_CMP_LE, m.rank_cw);
   RankCodeParams p;
   p.X = a.X;

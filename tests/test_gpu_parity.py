@@ -306,6 +306,26 @@ def test_single_feature_and_single_leaf_trees(strat):
     check_all(e0, m0, Xd, Xh)
 
 
+@pytest.mark.parametrize("cw", ["32", "16"])
+def test_prepass_forced_on_degenerate_models(cw, monkeypatch):
+    """The rank-code pre-pass forced on models it would never be picked for:
+    no split at all (D = 0: nothing to code, no pre-pass launch), one feature,
+    and an odd feature count with 16-bit cells (half-empty last word)."""
+    monkeypatch.setenv("HB_PTT_RANK", "1")
+    monkeypatch.setenv("HB_RANK_PRE", "1")
+    monkeypatch.setenv("HB_RANK_CW", cw)
+    leafy = [dict(feature=[-1], threshold=[np.nan], left=[-1], right=[-1], leaf_value=[0.25 * i])
+             for i in range(5)]
+    Xd, Xh = X_pair(8, 1300, 3, special_q24=SPECIAL_Q24)
+    for e in (synth.from_trees(leafy, 3),
+              synth.gen_forest(9, 4, 1, seed=4, family="mixed"),
+              synth.gen_forest(11, 5, 3, seed=5, family="skinny", grid=synth.GRID_COARSE)):
+        m = hb.Model(e, strategy="ptt", device=0)
+        assert m.info["rank_prepass"] == 1
+        F = e.n_features
+        check_all(e, m, Xd[:, :F].contiguous(), np.ascontiguousarray(Xh[:, :F]))
+
+
 def _perfect_d3_sign_tree(cmp):
     """Perfect depth-3 tree whose 7 internal nodes test features 0..6 at 0."""
     feat, thr, L, R, val = [], [], [], [], []
