@@ -128,20 +128,22 @@ def time_oracle(e, cfg, budget_s=12.0, max_rows=None, threads=0):
     return rows / dt, used, f"first {rows} rows of {cfg.name} (seed {cfg.seed_x:#x}), full model", dt
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return ""
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
     import synth
     cfg, e = synth.make_config(args.config)
-    cpu_model = ""
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                cpu_model = line.split(":", 1)[1].strip()
-                break
-    except OSError:
-        pass
     # size each step for ~4 s of CPU work (HB_REF_STEP_S overrides)
     step_s = float(os.environ.get("HB_REF_STEP_S", "4.0"))
     rate0, used, _, _ = time_oracle(e, cfg, budget_s=min(1.0, step_s))
@@ -163,7 +165,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(cfg, e, rows, args),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": used, "kind": "oracle",
-                         "sample": f"first {rows} rows of {cfg.name} per step", "cpu": cpu_model},
+                         "sample": f"first {rows} rows of {cfg.name} per step", "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -397,7 +399,11 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu:
         rate, used, sample, secs = time_oracle(e, cfg, budget_s=12.0)
         cpu = {"value": rate, "unit": "rows/s", "cores": used, "kind": "oracle", "sample": sample,
-               "seconds": secs}
+               "seconds": secs, "cpu": cpu_model()}
+        # the oracle on all host cores, plus one core
+        r1, u1, s1, t1_ = time_oracle(e, cfg, budget_s=3.0, threads=1)
+        cpu["single_core"] = {"value": r1, "unit": "rows/s", "cores": u1, "sample": s1,
+                              "seconds": t1_}
 
     if rank == 0:
         line = {
