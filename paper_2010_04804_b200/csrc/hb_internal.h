@@ -72,6 +72,8 @@ struct Model {
   void *d_rb = nullptr;      // [feat | groups | bucket tables]
   size_t rb_groups_off = 0, rb_pool_off = 0, rb_smem = 0, rb_smem_cap = 0;
   int rb_ngroups = 0;
+  uint32_t rb_max_span = 0;  // widest X column span of a table group (staged pre-pass)
+  bool rb_global = false;    // some table group is searched from global memory
   cudaMemPool_t mempool = nullptr;
 
   // small-batch path (hb_small.cu): PTT fp32 or TT records walked by
@@ -141,11 +143,14 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a);
 // rank-code pre-pass tables (hb_rank_codes.cu)
 struct RankBuckets {
   std::vector<uint32_t> feat;     // [n_fc][8] {f, B, S, start off, lo, hi, s, u off}
-  std::vector<uint32_t> groups;   // [n_groups][4] {pool off, bytes, word_begin, word_end}
+  std::vector<uint32_t> groups;   // [n_groups][8] {pool off, bytes, word_begin, word_end,
+                                  //                col_lo, ncols, staged pitch, 0}
   std::vector<uint8_t> pool;
   int n_groups = 0, n_words = 0;
   size_t max_group_bytes = 0;     // largest SMEM-resident group
   size_t smem_cap = 0;            // groups up to this size are staged in SMEM
+  uint32_t max_span = 0;          // widest X column span of one group
+  bool any_global = false;        // some group's table exceeds the cap (searched from global memory)
 };
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
                              int cw, RankBuckets *out);

@@ -313,6 +313,8 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     m->rb_ngroups = R.n_groups;
     m->rb_smem = R.max_group_bytes;
     m->rb_smem_cap = R.smem_cap;
+    m->rb_max_span = R.max_span;
+    m->rb_global = R.any_global;
     m->rank_nwords = R.n_words;
     m->rank_ngroups = 0;
     // per-call code scratch: stream-ordered allocations from a model-owned

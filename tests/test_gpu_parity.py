@@ -306,14 +306,16 @@ def test_single_feature_and_single_leaf_trees(strat):
     check_all(e0, m0, Xd, Xh)
 
 
+@pytest.mark.parametrize("staged", ["0", "1"])
 @pytest.mark.parametrize("cw", ["32", "16"])
-def test_prepass_forced_on_degenerate_models(cw, monkeypatch):
+def test_prepass_forced_on_degenerate_models(cw, staged, monkeypatch):
     """The rank-code pre-pass forced on models it would never be picked for:
     no split at all (D = 0: nothing to code, no pre-pass launch), one feature,
     and an odd feature count with 16-bit cells (half-empty last word)."""
     monkeypatch.setenv("HB_PTT_RANK", "1")
     monkeypatch.setenv("HB_RANK_PRE", "1")
     monkeypatch.setenv("HB_RANK_CW", cw)
+    monkeypatch.setenv("HB_RC_STAGED", staged)
     leafy = [dict(feature=[-1], threshold=[np.nan], left=[-1], right=[-1], leaf_value=[0.25 * i])
              for i in range(5)]
     Xd, Xh = X_pair(8, 1300, 3, special_q24=SPECIAL_Q24)
@@ -688,9 +690,10 @@ def test_sixteen_outputs_vector_leaves(strat, small, monkeypatch):
     check_all(e, m, Xd, Xh)
 
 
+@pytest.mark.parametrize("staged", ["0", "1"])
 @pytest.mark.parametrize("cmp", [0, 1])
 @pytest.mark.parametrize("cw", ["32", "16"])
-def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
+def test_rank_prepass_bucket_edges(cmp, cw, staged, monkeypatch):
     """Bucketed rank search of the pre-pass (hb_rank_codes.cu) at its edges:
     a feature with ~35K distinct thresholds (16384 buckets, table searched from
     global memory), thresholds at +-FLT_MAX / denormals / a few-ulp cluster
@@ -698,6 +701,7 @@ def test_rank_prepass_bucket_edges(cmp, cw, monkeypatch):
     finite threshold sits between +-Inf ones; X holds every threshold, its fp32
     neighbours, NaN, +-Inf and +-0. Every decision must equal the fp32 walk."""
     _set_layout(monkeypatch, "pre" + cw)
+    monkeypatch.setenv("HB_RC_STAGED", staged)
     rng = np.random.default_rng(40 + cmp)
     F = 6     # even and all used: 16-bit cells load feature pairs as one float2
     e = synth.gen_forest(400, 8, F, seed=41, family="balanced", cmp=cmp,
@@ -795,3 +799,28 @@ def test_tt_cluster_kernel_parity(kind, cmp, monkeypatch):
     # unaligned rows fall back to tt_wide_kernel inside the same model
     Xd2, Xh2 = X_pair(seed + 1, 301, F, ldx=F + 1)
     check_all(e, m, Xd2, Xh2, kinds=("raw", "leaf"))
+
+
+@pytest.mark.parametrize("rb", ["1", "2", "4"])
+@pytest.mark.parametrize("cw", ["32", "16"])
+def test_rank_prepass_staged_spans(cw, rb, monkeypatch):
+    """Staged pre-pass (cp.async X staging, hb_rank_codes.cu): table groups
+    whose features are scattered columns (the copied span has gaps), an odd
+    row stride (4-B aligned rows only), row counts that end inside a 32-row
+    block and inside a stage of RB blocks, several small table groups
+    (HB_RC_SMEM_KB=4), and RB = 1, 2, 4 blocks per stage. Leaf ids and
+    scores must match the oracle exactly / within tolerance."""
+    _set_layout(monkeypatch, "pre" + cw)
+    monkeypatch.setenv("HB_RC_STAGED", "1")
+    monkeypatch.setenv("HB_RC_RB", rb)
+    monkeypatch.setenv("HB_RC_SMEM_KB", "4")
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")     # small n must reach the pre-pass too
+    used = np.sort(np.random.default_rng(11).choice(61, 13, replace=False))
+    for cmp in (0, 1):
+        e = synth.gen_forest(45, 7, 61, seed=12 + cmp, family="balanced", features=used, cmp=cmp,
+                             post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
+        m = hb.Model(e, strategy="ptt", device=0)
+        assert m.info["rank_prepass"] == 1 and m.info["code_cell_bits"] == int(cw)
+        for n, ldx in ((1, 61), (33, 63), (4 * 32 * 5 + 7, 61), (2000, 67)):
+            Xd, Xh = X_pair(20 + n, n, 61, ldx=ldx, special_q24=SPECIAL_Q24)
+            check_all(e, m, Xd, Xh)
