@@ -38,7 +38,7 @@ namespace {
 constexpr int kRcWarps = 8;                 // warps per CTA of the pre-pass
 constexpr uint32_t kRcSmemMax = 200 * 1024; // largest per-CTA table budget
 constexpr int kRcBatch = 16;                // X loads in flight together per lane
-constexpr int kRcRows = 4;                  // 32-row blocks per warp iteration
+constexpr int kRcRows = 4;                  // 32-row blocks per warp iteration (HB_RC_ROWS=8: eight)
 
 struct RankCodeParams {
   const float *X;
@@ -55,34 +55,154 @@ struct RankCodeParams {
   uint32_t stage_off;     // staged kernel: SMEM byte offset of the X staging buffers
 };
 
-template <bool LE>
-__device__ __forceinline__ uint32_t rank_code(float x, const uint4 m0, const uint4 m1, const uint8_t *tb) {
-  // branch-free: NaN clamps to lo (fmaxf), walks bucket 0 (compares false)
-  // and is replaced by 0xFFFF at the end
-  const float lo = __uint_as_float(m1.x), hi = __uint_as_float(m1.y), s = __uint_as_float(m1.z);
-  const float xc = fminf(fmaxf(x, lo), hi);
-  float y = __fmul_rn(__fsub_rn(xc, lo), s);
-  y = fminf(y, (float)(m0.y - 1u));
-  const uint32_t b = __float2uint_rz(y);
-  // bucket entry: first threshold index | count << 16 (one load)
-  const uint32_t be = reinterpret_cast<const uint32_t *>(tb + m0.w)[b];
-  const float *u = reinterpret_cast<const float *>(tb + m1.w);
-  uint32_t base = be & 0xFFFFu;
-  uint32_t cnt = be >> 16;
-#pragma unroll
-  for (uint32_t k = 0; k < 16; ++k) {
-    if (k >= m0.z) break;                      // S steps (warp-uniform)
-    const uint32_t half = cnt >> 1;
-    const float v = u[base + half];              // u has one pad slot: in range when cnt == 0
-    const bool go = cnt != 0 && (LE ? v < x : v <= x);
-    base = go ? base + half + 1u : base;
-    cnt = go ? cnt - half - 1u : half;
+// Table reads: SMEM-resident groups use 32-bit shared addresses (LDS), the
+// others the read-only global path.
+template <bool SM>
+__device__ __forceinline__ uint32_t tab_u32(const uint8_t *tb, uint32_t tsm, uint32_t off) {
+  if (SM) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(tsm + off));
+    return v;
   }
-  return x != x ? 0xFFFFu : base;
+  return __ldg(reinterpret_cast<const uint32_t *>(tb + off));
 }
 
-template <bool LE, int CW>
-__global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankCodeParams p) {
+// NC rank codes in lockstep: the bucket step of every search first, then
+// S_max binary-search steps with all NC loads of a step issued back to back
+// (the searches are independent: their latencies overlap). A search whose own
+// S is smaller has cnt == 0 after S steps, and further steps are no-ops (they
+// read the pad slot u[base] and keep base), so running S_max steps is exact.
+template <bool LE, bool SM, int NC>
+__device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const uint4 *m0, const uint4 *m1,
+                                                    const int (&mi)[NC], uint32_t smax, const uint8_t *tb,
+                                                    uint32_t tsm, uint32_t (&code)[NC]) {
+  uint32_t base[NC], cnt[NC], uo[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const uint4 a = m0[mi[c]], b = m1[mi[c]];
+    const float lo = __uint_as_float(b.x), hi = __uint_as_float(b.y), sc = __uint_as_float(b.z);
+    const float xc = fminf(fmaxf(x[c], lo), hi);            // NaN -> lo: walks bucket 0, replaced below
+    float y = __fmul_rn(__fsub_rn(xc, lo), sc);
+    y = fminf(y, (float)(a.y - 1u));
+    const uint32_t bk = __float2uint_rz(y);
+    const uint32_t be = tab_u32<SM>(tb, tsm, a.w + 4u * bk);   // first index | count << 16
+    base[c] = be & 0xFFFFu;
+    cnt[c] = be >> 16;
+    uo[c] = b.w;
+  }
+  for (uint32_t k = 0; k < smax; ++k) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint32_t half = cnt[c] >> 1;
+      const float v = __uint_as_float(tab_u32<SM>(tb, tsm, uo[c] + 4u * (base[c] + half)));
+      const bool go = cnt[c] != 0 && (LE ? v < x[c] : v <= x[c]);
+      base[c] = go ? base[c] + half + 1u : base[c];
+      cnt[c] = go ? cnt[c] - half - 1u : half;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) code[c] = x[c] != x[c] ? 0xFFFFu : base[c];
+}
+
+template <bool LE, int CW, bool SM, int ROWS>
+__device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const uint4 g, const uint8_t *tb) {
+  const uint32_t tsm = SM ? (uint32_t)__cvta_generic_to_shared(tb) : 0u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // one warp = ROWS 32-row blocks, all words of this group: lane = row, so
+  // the strided X reads of consecutive features hit the sectors the first one
+  // brought into L1, and each word store is one coalesced 128-B line. X loads
+  // of ROWS blocks x NB words are issued before the first search, so the
+  // HBM latency is paid once per batch, not once per feature; the searches
+  // then run two features x ROWS rows in lockstep.
+  constexpr int PW = CW == 32 ? 1 : 2;                   // features per word
+  constexpr int NB = kRcBatch / (ROWS * PW) > 0 ? kRcBatch / (ROWS * PW) : 1;   // words per batch
+  constexpr int NS = NB * PW;                            // feature slots per batch (even)
+  static_assert(NS % 2 == 0, "feature slots go in pairs");
+  for (int64_t rb0 = ((int64_t)blockIdx.x * kRcWarps + warp) * ROWS; rb0 < p.nblocks;
+       rb0 += (int64_t)gridDim.x * kRcWarps * ROWS) {
+    // rows past n (and row blocks past the end) read row 0 and are not stored
+    const float *xr[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      const int64_t row = (rb0 + i) * 32 + lane;
+      xr[i] = p.X + (row < p.n ? row : 0) * p.ldx;
+    }
+    for (int w0 = (int)g.z; w0 < (int)g.w; w0 += NB) {
+      // feature slot s = j * PW + q: word w0 + j, compact feature PW * (w0 + j) + q
+      // (clamped to a valid feature: loads stay unconditional)
+      int cf[NS];
+      bool ok[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const int wd = w0 + s / PW, c = PW * wd + s % PW;
+        ok[s] = wd < (int)g.w && c < p.n_fc;
+        cf[s] = ok[s] ? c : PW * (int)g.z;
+      }
+      float xv[NS][ROWS];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (PW == 2 && p.pair_loads) {
+          // word = features 2w, 2w+1 = X columns 2w, 2w+1: one 8-B load
+          const int wc = min(w0 + j, (int)g.w - 1);
+#pragma unroll
+          for (int i = 0; i < ROWS; ++i) {
+            const float2 v = __ldg(reinterpret_cast<const float2 *>(xr[i] + 2 * wc));
+            xv[j * PW][i] = v.x;
+            xv[j * PW + PW - 1][i] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < PW; ++q) {
+            const uint32_t f = __ldg(reinterpret_cast<const uint32_t *>(p.feat + 2 * cf[j * PW + q]));
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i) xv[j * PW + q][i] = __ldg(xr[i] + f);
+          }
+        }
+      }
+#pragma unroll
+      for (int sp = 0; sp < NS; sp += 2) {
+        uint4 M0[2], M1[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          M0[e] = __ldg(p.feat + 2 * cf[sp + e]);
+          M1[e] = __ldg(p.feat + 2 * cf[sp + e] + 1);
+        }
+        float x8[2 * ROWS];
+        int mi[2 * ROWS];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int i = 0; i < ROWS; ++i) {
+            x8[e * ROWS + i] = xv[sp + e][i];
+            mi[e * ROWS + i] = e;
+          }
+        const uint32_t smax = max(ok[sp] ? M0[0].z : 0u, ok[sp + 1] ? M0[1].z : 0u);
+        uint32_t code[2 * ROWS];
+        rank_codes_lockstep<LE, SM, 2 * ROWS>(x8, M0, M1, mi, smax, tb, tsm, code);
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+          if (rb0 + i >= p.nblocks) continue;
+          if (CW == 32) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int wd = w0 + sp + e;
+              if (ok[sp + e])
+                p.codes[((size_t)(rb0 + i) * p.n_words + wd) * 32 + lane] = ((uint32_t)wd << 23) | code[e * ROWS + i];
+            }
+          } else {
+            const int wd = w0 + sp / 2;
+            if (ok[sp])
+              p.codes[((size_t)(rb0 + i) * p.n_words + wd) * 32 + lane] =
+                  code[i] | ((ok[sp + 1] ? code[ROWS + i] : 0u) << 16);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool LE, int CW, int ROWS>
+__global__ void __launch_bounds__(32 * kRcWarps, ROWS == 4 ? 4 : 3) rank_code_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint4 g = __ldg(p.groups + 2 * blockIdx.y);
   const uint8_t *tb = p.pool + g.x;
@@ -91,78 +211,21 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_kernel(const RankC
     uint4 *dst = reinterpret_cast<uint4 *>(smem);
     for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
-    tb = smem;
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // one warp = kRcRows 32-row blocks, all words of this group: lane = row, so
-  // the strided X reads of consecutive features hit the sectors the first one
-  // brought into L1, and each word store is one coalesced 128-B line. X loads
-  // of kRcRows blocks x NB words are issued before the first search, so the
-  // HBM latency is paid once per batch, not once per feature.
-  constexpr int PW = CW == 32 ? 1 : 2;                   // features per word
-  constexpr int NB = kRcBatch / (kRcRows * PW) > 0 ? kRcBatch / (kRcRows * PW) : 1;   // words per batch
-  for (int64_t rb0 = ((int64_t)blockIdx.x * kRcWarps + warp) * kRcRows; rb0 < p.nblocks;
-       rb0 += (int64_t)gridDim.x * kRcWarps * kRcRows) {
-    // rows past n (and row blocks past the end) read row 0 and are not stored
-    const float *xr[kRcRows];
-#pragma unroll
-    for (int i = 0; i < kRcRows; ++i) {
-      const int64_t row = (rb0 + i) * 32 + lane;
-      xr[i] = p.X + (row < p.n ? row : 0) * p.ldx;
-    }
-    for (int w0 = (int)g.z; w0 < (int)g.w; w0 += NB) {
-      float xv[kRcRows][NB][PW];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int wc = min(w0 + j, (int)g.w - 1);   // clamped: loads stay unconditional
-        if (PW == 2 && p.pair_loads) {
-          // word = features 2w, 2w+1 = X columns 2w, 2w+1: one 8-B load
-#pragma unroll
-          for (int i = 0; i < kRcRows; ++i) {
-            const float2 v = __ldg(reinterpret_cast<const float2 *>(xr[i] + 2 * wc));
-            xv[i][j][0] = v.x;
-            xv[i][j][PW - 1] = v.y;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < PW; ++q) {
-            const uint32_t f = __ldg(reinterpret_cast<const uint32_t *>(p.feat + 2 * min(wc * PW + q, p.n_fc - 1)));
-#pragma unroll
-            for (int i = 0; i < kRcRows; ++i) xv[i][j][q] = __ldg(xr[i] + f);
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int wd = w0 + j;
-        if (wd >= (int)g.w) break;
-        const int f0 = PW * wd, f1 = PW * wd + 1;
-        const uint4 a0 = __ldg(p.feat + 2 * f0), a1 = __ldg(p.feat + 2 * f0 + 1);
-        const bool has1 = PW == 2 && f1 < p.n_fc;
-        const uint4 b0 = __ldg(p.feat + 2 * (has1 ? f1 : f0)), b1 = __ldg(p.feat + 2 * (has1 ? f1 : f0) + 1);
-#pragma unroll
-        for (int i = 0; i < kRcRows; ++i) {
-          uint32_t word;
-          if (CW == 32) {
-            word = ((uint32_t)wd << 23) | rank_code<LE>(xv[i][j][0], a0, a1, tb);
-          } else {
-            const uint32_t c0 = rank_code<LE>(xv[i][j][0], a0, a1, tb);
-            const uint32_t c1 = has1 ? rank_code<LE>(xv[i][j][PW - 1], b0, b1, tb) : 0u;
-            word = c0 | (c1 << 16);
-          }
-          if (rb0 + i < p.nblocks) p.codes[((size_t)(rb0 + i) * p.n_words + wd) * 32 + lane] = word;
-        }
-      }
-    }
+    rank_code_body<LE, CW, true, ROWS>(p, g, smem);
+  } else {
+    rank_code_body<LE, CW, false, ROWS>(p, g, tb);
   }
 }
 
 using RcFn = void (*)(const RankCodeParams);
 
-RcFn rc_pick(bool le, int cw) {
-  if (cw == 32) return le ? rank_code_kernel<true, 32> : rank_code_kernel<false, 32>;
-  return le ? rank_code_kernel<true, 16> : rank_code_kernel<false, 16>;
+template <int ROWS>
+RcFn rc_pick_rows(bool le, int cw) {
+  if (cw == 32) return le ? rank_code_kernel<true, 32, ROWS> : rank_code_kernel<false, 32, ROWS>;
+  return le ? rank_code_kernel<true, 16, ROWS> : rank_code_kernel<false, 16, ROWS>;
 }
+
+RcFn rc_pick(bool le, int cw, int rows) { return rows == 8 ? rc_pick_rows<8>(le, cw) : rc_pick_rows<4>(le, cw); }
 
 // Staged variant: the X columns a table group needs are copied into per-warp
 // SMEM buffers with cp.async (LDGSTS) — lanes walk the [rows x columns] span
@@ -181,19 +244,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool LE, int CW, int RB>
-__global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(const RankCodeParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint4 g = __ldg(p.groups + 2 * blockIdx.y);
-  const uint4 gs = __ldg(p.groups + 2 * blockIdx.y + 1);   // {col_lo, ncols, pitch, 0}
-  const uint8_t *tb = p.pool + g.x;
-  if (g.y <= p.smem_cap) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(tb);
-    uint4 *dst = reinterpret_cast<uint4 *>(smem);
-    for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
-    tb = smem;
-  }
-  __syncthreads();
+template <bool LE, int CW, int RB, bool SM>
+__device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, const uint4 g, const uint4 gs,
+                                                      const uint8_t *tb, uint8_t *smem) {
+  const uint32_t tsm = SM ? (uint32_t)__cvta_generic_to_shared(tb) : 0u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncols = (int)gs.y, pitch = (int)gs.z;
   const uint32_t stage_words = (uint32_t)(RB * 32 * pitch);
@@ -225,6 +279,7 @@ __global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(cons
     cp_async_commit();   // empty groups keep the wait count uniform
   };
   constexpr int PW = CW == 32 ? 1 : 2;
+  constexpr int WS = 2 / PW;          // words per feature pair
   int64_t u = (int64_t)blockIdx.x * kRcWarps + warp;
 #pragma unroll
   for (int s = 0; s < kStStages - 1; ++s) issue(u + s * ustep, s);
@@ -234,32 +289,63 @@ __global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(cons
     cp_async_wait<kStStages - 1>();
     __syncwarp();
     const uint32_t *xr = xs + st * stage_words + lane * pitch;
-    for (int wd = (int)g.z; wd < (int)g.w; ++wd) {
-      const int f0 = PW * wd, f1 = PW * wd + 1;
-      const uint4 a0 = __ldg(p.feat + 2 * f0), a1 = __ldg(p.feat + 2 * f0 + 1);
-      const bool has1 = PW == 2 && f1 < p.n_fc;
-      const uint4 b0 = __ldg(p.feat + 2 * (has1 ? f1 : f0)), b1 = __ldg(p.feat + 2 * (has1 ? f1 : f0) + 1);
-      const int c0 = (int)(a0.x - gs.x), c1 = (int)(b0.x - gs.x);
+    // two features x RB rows per lockstep search
+    for (int wd = (int)g.z; wd < (int)g.w; wd += WS) {
+      uint4 M0[2], M1[2];
+      bool ok[2];
+      float x8[2 * RB];
+      int mi[2 * RB];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = PW * wd + e;
+        ok[e] = (PW == 2 ? wd : wd + e) < (int)g.w && c < p.n_fc;
+        const int cc = ok[e] ? c : PW * wd;
+        M0[e] = __ldg(p.feat + 2 * cc);
+        M1[e] = __ldg(p.feat + 2 * cc + 1);
+        const int col = (int)(M0[e].x - gs.x);
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          x8[e * RB + i] = __uint_as_float(xr[i * 32 * pitch + col]);
+          mi[e * RB + i] = e;
+        }
+      }
+      const uint32_t smax = max(M0[0].z, ok[1] ? M0[1].z : 0u);
+      uint32_t code[2 * RB];
+      rank_codes_lockstep<LE, SM, 2 * RB>(x8, M0, M1, mi, smax, tb, tsm, code);
 #pragma unroll
       for (int i = 0; i < RB; ++i) {
-        const float x0 = __uint_as_float(xr[i * 32 * pitch + c0]);
-        uint32_t word;
-        if (CW == 32) {
-          word = ((uint32_t)wd << 23) | rank_code<LE>(x0, a0, a1, tb);
-        } else {
-          const float x1 = __uint_as_float(xr[i * 32 * pitch + c1]);
-          const uint32_t k0 = rank_code<LE>(x0, a0, a1, tb);
-          const uint32_t k1 = has1 ? rank_code<LE>(x1, b0, b1, tb) : 0u;
-          word = k0 | (k1 << 16);
-        }
         const int64_t blk = u * RB + i;
-        if (blk < p.nblocks) p.codes[((size_t)blk * p.n_words + wd) * 32 + lane] = word;
+        if (blk >= p.nblocks) continue;
+        uint32_t *dst = p.codes + ((size_t)blk * p.n_words + wd) * 32 + lane;
+        if (CW == 32) {
+          dst[0] = ((uint32_t)wd << 23) | code[i];
+          if (ok[1]) dst[32] = ((uint32_t)(wd + 1) << 23) | code[RB + i];
+        } else {
+          dst[0] = code[i] | ((ok[1] ? code[RB + i] : 0u) << 16);
+        }
       }
     }
     __syncwarp();        // every lane is done with stage st before it is refilled
     st = st == kStStages - 1 ? 0 : st + 1;
   }
   cp_async_wait<0>();
+}
+
+template <bool LE, int CW, int RB>
+__global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(const RankCodeParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint4 g = __ldg(p.groups + 2 * blockIdx.y);
+  const uint4 gs = __ldg(p.groups + 2 * blockIdx.y + 1);   // {col_lo, ncols, pitch, 0}
+  const uint8_t *tb = p.pool + g.x;
+  if (g.y <= p.smem_cap) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(tb);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem);
+    for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+    rank_code_staged_body<LE, CW, RB, true>(p, g, gs, smem, smem);
+  } else {
+    rank_code_staged_body<LE, CW, RB, false>(p, g, gs, tb, smem);
+  }
 }
 
 template <bool LE, int CW>
@@ -441,16 +527,18 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   const bool fits = staged_smem <= (size_t)kRcSmemMax + stage_budget && m.rb_max_span > 0;
   bool staged = fits && m.rb_global;
   if (ev && *ev && std::atoi(ev) >= 0) staged = fits && std::atoi(ev) != 0;   // -1: AUTO
-  RcFn fn = staged ? staged_pick(m.cmp == HB_CMP_LE, m.rank_cw, rb) : rc_pick(m.cmp == HB_CMP_LE, m.rank_cw);
+  const char *erows = std::getenv("HB_RC_ROWS");
+  const int rows = erows && std::atoi(erows) == 8 ? 8 : kRcRows;
+  RcFn fn = staged ? staged_pick(m.cmp == HB_CMP_LE, m.rank_cw, rb) : rc_pick(m.cmp == HB_CMP_LE, m.rank_cw, rows);
   const int smem = (int)(staged ? staged_smem : m.rb_smem);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(rank codes)");
   // as many CTAs as fit per SM (by SMEM, at most 4), spread over the feature
   // groups (blockIdx.y)
   const size_t per_cta = staged ? staged_smem : std::max<size_t>(m.rb_smem_cap, 1);
-  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / per_cta));
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(!staged && rows == 8 ? 3 : 4, (220 * 1024) / per_cta));
   const int64_t want = std::max<int64_t>(1, ((int64_t)per_sm * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
-  const int64_t rows_per_cta = (int64_t)kRcWarps * (staged ? rb : kRcRows);
+  const int64_t rows_per_cta = (int64_t)kRcWarps * (staged ? rb : rows);
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (nblocks + rows_per_cta - 1) / rows_per_cta));
   fn<<<dim3(gx, m.rb_ngroups), 32 * kRcWarps, smem, a.stream>>>(p);
   e = cudaGetLastError();

@@ -306,7 +306,7 @@ def test_single_feature_and_single_leaf_trees(strat):
     check_all(e0, m0, Xd, Xh)
 
 
-@pytest.mark.parametrize("staged", ["0", "1"])
+@pytest.mark.parametrize("staged", ["0", "1", "0:8"])
 @pytest.mark.parametrize("cw", ["32", "16"])
 def test_prepass_forced_on_degenerate_models(cw, staged, monkeypatch):
     """The rank-code pre-pass forced on models it would never be picked for:
@@ -315,7 +315,8 @@ def test_prepass_forced_on_degenerate_models(cw, staged, monkeypatch):
     monkeypatch.setenv("HB_PTT_RANK", "1")
     monkeypatch.setenv("HB_RANK_PRE", "1")
     monkeypatch.setenv("HB_RANK_CW", cw)
-    monkeypatch.setenv("HB_RC_STAGED", staged)
+    monkeypatch.setenv("HB_RC_STAGED", staged.split(":")[0])
+    monkeypatch.setenv("HB_RC_ROWS", staged.split(":")[1] if ":" in staged else "4")
     leafy = [dict(feature=[-1], threshold=[np.nan], left=[-1], right=[-1], leaf_value=[0.25 * i])
              for i in range(5)]
     Xd, Xh = X_pair(8, 1300, 3, special_q24=SPECIAL_Q24)
@@ -690,7 +691,7 @@ def test_sixteen_outputs_vector_leaves(strat, small, monkeypatch):
     check_all(e, m, Xd, Xh)
 
 
-@pytest.mark.parametrize("staged", ["0", "1"])
+@pytest.mark.parametrize("staged", ["0", "1", "0:8"])   # direct, staged, direct with 8 row blocks per batch
 @pytest.mark.parametrize("cmp", [0, 1])
 @pytest.mark.parametrize("cw", ["32", "16"])
 def test_rank_prepass_bucket_edges(cmp, cw, staged, monkeypatch):
@@ -701,7 +702,8 @@ def test_rank_prepass_bucket_edges(cmp, cw, staged, monkeypatch):
     finite threshold sits between +-Inf ones; X holds every threshold, its fp32
     neighbours, NaN, +-Inf and +-0. Every decision must equal the fp32 walk."""
     _set_layout(monkeypatch, "pre" + cw)
-    monkeypatch.setenv("HB_RC_STAGED", staged)
+    monkeypatch.setenv("HB_RC_STAGED", staged.split(":")[0])
+    monkeypatch.setenv("HB_RC_ROWS", staged.split(":")[1] if ":" in staged else "4")
     rng = np.random.default_rng(40 + cmp)
     F = 6     # even and all used: 16-bit cells load feature pairs as one float2
     e = synth.gen_forest(400, 8, F, seed=41, family="balanced", cmp=cmp,
