@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -334,6 +335,149 @@ static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLa
   return HB_OK;
 }
 
+// Sector-paired TT layout for tt_wide_kernel: nodes are
+// placed so that a "root" node and its two children share one 32-B L2 sector
+// (slots s, s+1, s+2 with s % 4 in {0, 1}), and the children of those children
+// start new sectors. Record (8 B): {N_F | flag << 15 | N_R << 16, N_T}; the
+// left child is N_R - 1 (flag 0: root, children adjacent in its sector) or
+// N_R - 4 (flag 1: the pair sits at the same offset of two consecutive
+// sectors). A walk then misses L1 at most once per two levels: the second
+// level of each sector is an L1 hit. Leaves keep the self-loop {j << 16, NaN}.
+// Needs F <= 32768 and <= 65535 slots per tree; node array 32-B aligned.
+static hb_status build_tt_sector(const hb_ensemble *e, int t0, int t1, int Tpad, HostLayout *L,
+                                 const FeatureMap *fm, int top) {
+  const int w = e->leaf_width;
+  const uint32_t qnan = 0x7FC00000u;
+  struct Tree {
+    std::vector<uint32_t> rec;     // 2 words per slot
+    std::vector<int32_t> orig;     // slot -> original node id of a leaf (-1 otherwise)
+  };
+  std::vector<Tree> trees(t1 - t0);
+  size_t maxslots = 4;
+  for (int t = t0; t < t1; ++t) {
+    Tree &T = trees[t - t0];
+    const int64_t a = e->node_offset[t];
+    int nsec = 0;
+    std::vector<int> ll_free;      // sector pairs (A, A+1) whose offset 3 is free in both
+    auto grow = [&](int sectors) {
+      const size_t n = (size_t)sectors * 4;
+      const size_t old = T.orig.size();
+      T.rec.resize(2 * n);
+      T.orig.resize(n, -1);
+      for (size_t j = old; j < n; ++j) T.rec[2 * j] = (uint32_t)j << 16, T.rec[2 * j + 1] = qnan;
+    };
+    auto alloc_pair = [&]() {
+      const int A = nsec;
+      nsec += 2;
+      grow(nsec);
+      return A;
+    };
+    auto feat = [&](int o) -> uint32_t {
+      return (uint32_t)(fm ? fm->remap[e->feature[a + o]] : e->feature[a + o]);
+    };
+    auto set_leaf = [&](int o, int slot) {
+      T.rec[2 * slot] = (uint32_t)slot << 16;
+      T.rec[2 * slot + 1] = qnan;
+      T.orig[slot] = o;
+    };
+    std::function<void(int, int)> place_root, place_mid;
+    // o internal at slot s (s % 4 in {0, 1}): children at s + 1, s + 2
+    place_root = [&](int o, int s) {
+      T.rec[2 * s] = feat(o) | ((uint32_t)(s + 2) << 16);
+      T.rec[2 * s + 1] = f2u(e->threshold[a + o]);
+      place_mid(e->left[a + o], s + 1);
+      place_mid(e->right[a + o], s + 2);
+    };
+    // o at slot s whose children (if any) go to (p, p + 4) of two new sectors
+    place_mid = [&](int o, int s) {
+      if (e->left[a + o] == -1) {
+        set_leaf(o, s);
+        return;
+      }
+      const int gl = e->left[a + o], gr = e->right[a + o];
+      const bool lleaf = e->left[a + gl] == -1, rleaf = e->left[a + gr] == -1;
+      int p;
+      if (lleaf && rleaf && !ll_free.empty()) {
+        p = 4 * ll_free.back() + 3;          // two leaves: reuse free offset-3 slots
+        ll_free.pop_back();
+      } else {
+        const int A = alloc_pair();
+        p = 4 * A;
+        if (!lleaf && !rleaf) ll_free.push_back(A);
+      }
+      T.rec[2 * s] = feat(o) | 0x8000u | ((uint32_t)(p + 4) << 16);
+      T.rec[2 * s + 1] = f2u(e->threshold[a + o]);
+      if (lleaf) set_leaf(gl, p);
+      else place_root(gl, p);
+      if (rleaf) set_leaf(gr, p + 4);
+      else place_root(gr, p + 4);
+    };
+    if (top <= 0) {
+      nsec = 1;
+      grow(1);
+      if (e->left[a] == -1) set_leaf(0, 0);
+      else place_root(0, 0);
+    } else {
+      // top levels in BFS order (siblings adjacent, flag 0): they are shared
+      // by the rows of a tile and pack densely into a few L1 lines; nodes at
+      // depth top - 1 start the sector-paired part below
+      struct Q { int o, slot, depth; };
+      std::vector<Q> q(1, Q{0, 0, 0});
+      int nb = 1;
+      std::vector<int> right_slot;
+      for (size_t k = 0; k < q.size(); ++k) {
+        const Q c = q[k];
+        right_slot.push_back(-1);
+        if (e->left[a + c.o] != -1 && c.depth < top - 1) {
+          q.push_back(Q{e->left[a + c.o], nb, c.depth + 1});
+          q.push_back(Q{e->right[a + c.o], nb + 1, c.depth + 1});
+          right_slot[k] = nb + 1;
+          nb += 2;
+        }
+      }
+      nsec = (nb + 3) / 4;
+      grow(nsec);
+      for (size_t k = 0; k < q.size(); ++k) {
+        const Q c = q[k];
+        if (e->left[a + c.o] == -1) {
+          set_leaf(c.o, c.slot);
+        } else if (right_slot[k] >= 0) {
+          T.rec[2 * c.slot] = feat(c.o) | ((uint32_t)right_slot[k] << 16);
+          T.rec[2 * c.slot + 1] = f2u(e->threshold[a + c.o]);
+        } else {
+          place_mid(c.o, c.slot);
+        }
+      }
+    }
+    if (T.orig.size() > 65535) return fail(HB_E_UNSUPPORTED, "TT sector layout: tree needs more than 65535 slots");
+    maxslots = std::max(maxslots, T.orig.size());
+  }
+  L->nslots = (int)maxslots;
+  L->stride = (32 + (size_t)8 * maxslots + (size_t)4 * w * maxslots + 31) & ~size_t(31);
+  L->trees.assign((size_t)Tpad * L->stride, 0);
+  L->leafmap.assign((size_t)Tpad * maxslots, -1);
+  for (int lt = 0; lt < Tpad; ++lt) {
+    uint8_t *rec = L->trees.data() + (size_t)lt * L->stride;
+    uint32_t *hdr = reinterpret_cast<uint32_t *>(rec);
+    uint32_t *node = reinterpret_cast<uint32_t *>(rec + 32);
+    float *leaf = reinterpret_cast<float *>(rec + 32 + (size_t)8 * maxslots);
+    for (size_t j = 0; j < maxslots; ++j) node[2 * j] = (uint32_t)j << 16, node[2 * j + 1] = qnan;
+    if (lt >= t1 - t0) continue;
+    const int t = t0 + lt;
+    const int64_t a = e->node_offset[t];
+    hdr[0] = (uint32_t)(w == 1 ? tree_out(e, t) : 0);
+    const Tree &T = trees[lt];
+    std::memcpy(node, T.rec.data(), T.rec.size() * 4);
+    for (size_t j = 0; j < T.orig.size(); ++j) {
+      const int o = T.orig[j];
+      if (o < 0) continue;
+      L->leafmap[(size_t)lt * maxslots + j] = o;
+      for (int k = 0; k < w; ++k) leaf[j * w + k] = e->leaf_value[(a + o) * w + k];
+    }
+  }
+  return HB_OK;
+}
+
 static int env_int(const char *name, int dflt) {
   const char *v = std::getenv(name);
   if (!v || !*v) return dflt;
@@ -425,6 +569,8 @@ static void free_model(Model *m) {
   cudaFree(m->d_tops);
   cudaFree(m->d_rb);
   cudaFree(m->d_ttb);
+  cudaFree(m->d_ttw);
+  cudaFree(m->d_ttw_leafmap);
   if (m->mempool) cudaMemPoolDestroy(m->mempool);   // deferred until pending frees complete
   delete m;
 }
@@ -551,6 +697,22 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.ch = kTreeGroup;
         m->cfg = c;
         m->tt_g = env_int("HB_TT_G", 4);
+        // sector-paired records (one L2 sector per two levels of a walk)
+        if (env_int("HB_TT_SECTOR", 0) == 1 && fmap.used.size() <= 32768) {
+          HostLayout S;
+          st = build_tt_sector(e, t0, t1, m->n_trees_pad, &S, &fmap, env_int("HB_TT_SECTOR_TOP", 4));
+          if (st == HB_OK) {
+            st = upload(S.trees, reinterpret_cast<uint8_t **>(&m->d_ttw), &m->device_bytes);
+            if (st != HB_OK) return st;
+            st = upload(S.leafmap, &m->d_ttw_leafmap, &m->device_bytes);
+            if (st != HB_OK) return st;
+            m->ttw_stride = S.stride;
+            m->ttw_nslots = S.nslots;
+            m->tt_sector = 1;
+          } else if (st != HB_E_UNSUPPORTED) {
+            return st;
+          }
+        }
         // opt-in (HB_TT_BLOCK=1): 2-level node blocks walked by per-lane
         // cursors (hb_ttb.cu); measured slower than
         // tt_wide_kernel on C5, so AUTO keeps tt_wide_kernel

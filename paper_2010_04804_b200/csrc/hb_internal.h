@@ -106,6 +106,13 @@ struct Model {
   int64_t ttb_nblocks = 0;
   int ttb_sync = 1;          // lanes of a warp advance a cursor together
   int tt_g = 4;              // tt_wide_kernel: concurrent walks per lane (4, 6, 8)
+  // sector-paired TT records for tt_wide_kernel (hb_host.cu build_tt_sector):
+  // a root and its two children share one 32-B sector; own records + leafmap
+  int tt_sector = 0;
+  void *d_ttw = nullptr;
+  int32_t *d_ttw_leafmap = nullptr;
+  size_t ttw_stride = 0;
+  int ttw_nslots = 0;
 
   size_t device_bytes = 0;
   LaunchCfg cfg;

@@ -519,13 +519,15 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   while (rb > 1 && (size_t)kRcWarps * kStStages * rb * 32 * pitch * 4 > stage_budget) rb >>= 1;
   if (erb && *erb) rb = std::atoi(erb) >= 4 ? 4 : (std::atoi(erb) >= 2 ? 2 : 1);
   const size_t staged_smem = tbytes + (size_t)kRcWarps * kStStages * rb * 32 * pitch * 4;
-  // AUTO: staged when some table group is searched from global memory (its
-  // table exceeds the SMEM cap): those searches are L1-latency bound and the
-  // cp.async pipeline keeps X off the dependency chain (C4: 49.2 -> 46.9 ms per
-  // step). SMEM-resident tables keep the direct kernel, which runs twice the
-  // CTAs per SM (C2 pre-pass 0.49 ms direct vs 0.94 ms staged).
+  // AUTO: staged when the table groups are narrow (<= 2 features each, e.g.
+  // C4: ~40 KB per feature, 54 single-feature groups) or some group is
+  // searched from global memory. A narrow group has few searches per row
+  // block, so the direct kernel waits on its strided X loads; the cp.async
+  // pipeline keeps hundreds of rows in flight per warp (C4: 49.2 -> 46.4 ms
+  // per step). Wider groups keep the direct kernel, which runs twice the CTAs
+  // per SM (C2, 5 features per group: 0.42 ms direct vs 0.90 ms staged).
   const bool fits = staged_smem <= (size_t)kRcSmemMax + stage_budget && m.rb_max_span > 0;
-  bool staged = fits && m.rb_global;
+  bool staged = fits && (m.rb_global || m.rank_nfc <= 2 * m.rb_ngroups);
   if (ev && *ev && std::atoi(ev) >= 0) staged = fits && std::atoi(ev) != 0;   // -1: AUTO
   const char *erows = std::getenv("HB_RC_ROWS");
   const int rows = erows && std::atoi(erows) == 8 ? 8 : kRcRows;

@@ -37,6 +37,11 @@ struct TtParams {
   int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
 };
 
+// node array offset inside a record: 16 B (BFS layout), 32 B (sector layout:
+// 32-B aligned so a root and its children share one L2 sector)
+template <bool SEC>
+constexpr int node_off() { return SEC ? 32 : 16; }
+
 template <bool LE>
 __device__ __forceinline__ uint32_t tt_walk(const uint2 *nodes, const float *xrow, int xstride,
                                             int depth) {
@@ -204,20 +209,22 @@ __device__ __forceinline__ int xw_swz(int f) {
   return (f >> S) & (R - 1);
 }
 
-template <bool LE, int R>
+template <bool LE, int R, bool SEC>
 __device__ __forceinline__ void wide_step(const uint2 *n, uint32_t &i, const float *xs, int r,
                                           bool &done) {
   const uint2 d = __ldg(n + i);
-  const int f = (int)(d.x & 0xFFFFu);
+  const int f = (int)(d.x & (SEC ? 0x7FFFu : 0xFFFFu));
   const float x = xs[f * R + (r ^ xw_swz<R>(f))];
   const float t = __uint_as_float(d.y);
   const bool pr = LE ? (x <= t) : (x < t);
-  const uint32_t nx = (d.x >> 16) - (pr ? 1u : 0u);
+  // left child = N_R - 1 (BFS; sector roots) or N_R - 4 (sector layout, flag bit 15)
+  const uint32_t dl = SEC ? ((d.x & 0x8000u) ? 4u : 1u) : 1u;
+  const uint32_t nx = (d.x >> 16) - (pr ? dl : 0u);
   done = done && (nx == i);
   i = nx;
 }
 
-template <bool LE, int NACC, int R, int G>           // G: trees walked at once per lane
+template <bool LE, int NACC, int R, int G, bool SEC> // G: trees walked at once per lane; SEC: sector layout
 __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int L = 32 / R;                       // tree slots per warp
@@ -273,13 +280,13 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         const int t = base + sub + g * slots;
         valid[g] = t < p.n_trees_pad;               // uniform across the warp
         rec[g] = p.trees + (size_t)(valid[g] ? t : base + sub) * p.stride;
-        nd[g] = reinterpret_cast<const uint2 *>(rec[g] + 16);
+        nd[g] = reinterpret_cast<const uint2 *>(rec[g] + node_off<SEC>());
         idx[g] = 0;
       }
       for (int l = 0; l < p.depth; ++l) {
         bool done = true;
 #pragma unroll
-        for (int g = 0; g < G; ++g) wide_step<LE, R>(nd[g], idx[g], xs, r, done);
+        for (int g = 0; g < G; ++g) wide_step<LE, R, SEC>(nd[g], idx[g], xs, r, done);
         if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
       }
 #pragma unroll
@@ -360,26 +367,31 @@ static TtFn pick_nacc(int nacc) {
 
 int sm_count(int device);
 
-template <bool LE, int R>
+template <bool LE, int R, bool SEC>
 static TtFn pick_wide_nacc(int nacc, int g) {
   // 6 or 8 concurrent walks per lane only for scalar outputs (register budget)
-  if (nacc == 1 && g >= 8) return tt_wide_kernel<LE, 1, R, 8>;
-  if (nacc == 1 && g >= 6) return tt_wide_kernel<LE, 1, R, 6>;
+  if (nacc == 1 && g >= 8) return tt_wide_kernel<LE, 1, R, 8, SEC>;
+  if (nacc == 1 && g >= 6) return tt_wide_kernel<LE, 1, R, 6, SEC>;
   switch (nacc) {
-    case 1: return tt_wide_kernel<LE, 1, R, 4>;
-    case 4: return tt_wide_kernel<LE, 4, R, 4>;
-    case 8: return tt_wide_kernel<LE, 8, R, 4>;
-    default: return tt_wide_kernel<LE, 16, R, 4>;
+    case 1: return tt_wide_kernel<LE, 1, R, 4, SEC>;
+    case 4: return tt_wide_kernel<LE, 4, R, 4, SEC>;
+    case 8: return tt_wide_kernel<LE, 8, R, 4, SEC>;
+    default: return tt_wide_kernel<LE, 16, R, 4, SEC>;
+  }
+}
+
+template <bool LE, bool SEC>
+static TtFn pick_wide_r(int R, int nacc, int g) {
+  switch (R) {
+    case 32: return pick_wide_nacc<LE, 32, SEC>(nacc, g);
+    case 16: return pick_wide_nacc<LE, 16, SEC>(nacc, g);
+    default: return pick_wide_nacc<LE, 8, SEC>(nacc, g);
   }
 }
 
 template <bool LE>
-static TtFn pick_wide(int R, int nacc, int g) {
-  switch (R) {
-    case 32: return pick_wide_nacc<LE, 32>(nacc, g);
-    case 16: return pick_wide_nacc<LE, 16>(nacc, g);
-    default: return pick_wide_nacc<LE, 8>(nacc, g);
-  }
+static TtFn pick_wide(int R, int nacc, int g, bool sec) {
+  return sec ? pick_wide_r<LE, true>(R, nacc, g) : pick_wide_r<LE, false>(R, nacc, g);
 }
 
 hb_status launch_tt(const Model &m, const RunArgs &a) {
@@ -389,8 +401,9 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
     if (st != HB_E_UNSUPPORTED) return st;   // unaligned rows: tt_wide_kernel below
   }
   const bool wide = m.cfg.wide_rows > 0;
-  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g)
-                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g))
+  const bool sec = wide && m.tt_sector;
+  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g, sec)
+                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g, sec))
                  : (m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc));
   TtParams p;
   p.X = a.X;
@@ -400,13 +413,13 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.fmap = m.d_fmap;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   p.depth = m.depth;
-  p.trees = static_cast<const uint8_t *>(m.d_trees);
-  p.stride = (uint32_t)m.stride;
+  p.trees = static_cast<const uint8_t *>(sec ? m.d_ttw : m.d_trees);
+  p.stride = (uint32_t)(sec ? m.ttw_stride : m.stride);
   p.n_trees_pad = m.n_trees_pad;
   p.n_trees = m.n_trees;
   p.tree_begin = m.tree_begin;
-  p.leafmap = m.d_leafmap;
-  p.nslots = m.nslots;
+  p.leafmap = sec ? m.d_ttw_leafmap : m.d_leafmap;
+  p.nslots = sec ? m.ttw_nslots : m.nslots;
   p.scale = m.d_scale;
   p.base = m.d_base;
   p.K = m.n_outputs;

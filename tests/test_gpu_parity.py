@@ -180,19 +180,52 @@ def test_ptt_special_thresholds(cmp, rank, monkeypatch):
 
 @pytest.mark.parametrize("kind", ["reg", "binary", "multiclass", "rf", "k7", "k12"])
 @pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("blocks", ["1", "0"])
+@pytest.mark.parametrize("blocks", ["1", "0", "sector"])
 def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
     """The wide-row TT kernels (R rows per CTA, lanes = tree slot x row, nodes
     through L1/L2) forced on ordinary inputs: ttb_kernel (2-level node blocks,
-    persistent per-lane cursors) and tt_wide_kernel (8-B nodes, early exit)."""
+    persistent per-lane cursors) and tt_wide_kernel (8-B nodes, early exit) on
+    the BFS and the sector-paired record layouts."""
     monkeypatch.setenv("HB_TT_WIDE", "1")
-    monkeypatch.setenv("HB_TT_BLOCK", blocks)
+    monkeypatch.setenv("HB_TT_BLOCK", "1" if blocks == "1" else "0")
+    monkeypatch.setenv("HB_TT_SECTOR", "1" if blocks == "sector" else "0")
     seed = zlib.crc32(f"wide{kind}{cmp}".encode()) & 0xFFFF
     e = _forest(kind, 45, 9, 37, seed, FAMILIES[seed % 3], cmp)
     m = hb.Model(e, strategy="tt", device=0)
     assert m.info["kernel_name"] == ("ttb_kernel" if blocks == "1" else "tt_wide_kernel")
     Xd, Xh = X_pair(seed, 1000 + seed % 53, 37, special_q24=SPECIAL_Q24)
     check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_tt_sector_layout_tree_shapes(cmp, monkeypatch):
+    """Sector-paired TT records (hb_host.cu build_tt_sector) on every shape the
+    placement distinguishes: single-leaf trees, a stump, chains of odd and
+    even depth (leaf + internal child pairs at every level), bushy mixed trees
+    (leaf + leaf pairs reuse free sector slots), a depth-12 balanced tree; the
+    BFS layout on the same model must give the same leaf ids."""
+    monkeypatch.setenv("HB_TT_WIDE", "1")
+    monkeypatch.setenv("HB_TT_BLOCK", "0")
+    F = 9
+    trees = [dict(feature=[0], threshold=[0.0], left=[-1], right=[-1], leaf_value=[0.75]),
+             dict(feature=[2, 0, 0], threshold=[0.5, 0, 0], left=[1, -1, -1], right=[2, -1, -1],
+                  leaf_value=[0.0, -1.5, 2.25])]
+    trees += [_chain_tree(d, F, d, left_chain=d % 2 == 0) for d in (2, 3, 5, 6, 13)]
+    bushy = synth.gen_forest(200, 9, F, seed=4 + cmp, family="mixed", grid=synth.GRID_COARSE)
+    trees += [bushy.tree(i) for i in range(200)]
+    deep = synth.gen_forest(3, 12, F, seed=9 + cmp, family="balanced")
+    trees += [deep.tree(i) for i in range(3)]
+    e = synth.from_trees(trees, F, cmp=cmp)
+    Xd, Xh = X_pair(12, 2111, F, grid=synth.GRID_COARSE, special_q24=SPECIAL_Q24)
+    leaves = []
+    for sec in ("1:0", "1:1", "1:4", "1:6", "0:0"):     # sector layout with 0/1/4/6 BFS top levels; BFS layout
+        monkeypatch.setenv("HB_TT_SECTOR", sec.split(":")[0])
+        monkeypatch.setenv("HB_TT_SECTOR_TOP", sec.split(":")[1])
+        m = hb.Model(e, strategy="tt", device=0)
+        assert m.info["kernel_name"] == "tt_wide_kernel"
+        check_all(e, m, Xd, Xh, kinds=("predict", "raw", "leaf", "leaf_hash"))
+        leaves.append(m.predict_leaf(Xd).cpu().numpy())
+    assert all(np.array_equal(leaves[0], lv) for lv in leaves[1:])
 
 
 def test_tt_wide_rows_natural():
