@@ -326,7 +326,7 @@ def run_ours(args):
             peaks = {"error": str(ex)}
     smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
     layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "") + \
-        ("-pre" if info.get("rank_prepass") else "")
+        ("-pre" if info.get("rank_prepass") else "") + ("-sector" if info.get("tt_sector") else "")
     prof = load_profile(args.config, layout)
     kname = info["kernel_name"]
     if n <= int(os.environ.get("HB_SMALL_BATCH", "4096")):

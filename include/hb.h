@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 1
+#define HB_ABI_VERSION 2   /* 2: hb_model_info.tt_sector appended */
 
 typedef enum {
   HB_OK = 0,
@@ -156,6 +156,8 @@ typedef struct {
   int32_t code_cell_bits;       /* rank-coded PTT: 32 or 16-bit X code cells    */
   int32_t rank_prepass;         /* rank-coded PTT: 1 if a separate launch (rank_code_kernel)
                                    computes the X codes into stream-ordered scratch */
+  int32_t tt_sector;            /* wide-row TT: 1 if tt_wide_kernel walks sector-paired
+                                   records (a node and both children in one 32-B sector) */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the

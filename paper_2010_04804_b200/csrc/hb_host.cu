@@ -697,8 +697,17 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.ch = kTreeGroup;
         m->cfg = c;
         m->tt_g = env_int("HB_TT_G", 4);
-        // sector-paired records (one L2 sector per two levels of a walk)
-        if (env_int("HB_TT_SECTOR", 0) == 1 && fmap.used.size() <= 32768) {
+        // sector-paired records (one L2 sector per two levels of a walk):
+        // AUTO when the BFS records exceed 3/4 of L2, i.e. deep levels come
+        // from HBM (C5, 10k trees on one GPU: 16.96 -> 15.57 ms); an
+        // L2-resident model keeps the BFS records (C5 1/8 shard: 1.83 ms BFS
+        // vs 2.03-2.14 ms sector: siblings 4 slots apart touch more sectors
+        // per tile). HB_TT_SECTOR=0/1 forces.
+        int l2_bytes = 0;
+        cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
+        const int want_sector = env_int("HB_TT_SECTOR", -1);
+        const bool big = (double)m->n_trees_pad * (double)L.stride > 0.75 * (double)l2_bytes;
+        if ((want_sector == 1 || (want_sector == -1 && big)) && fmap.used.size() <= 32768) {
           HostLayout S;
           st = build_tt_sector(e, t0, t1, m->n_trees_pad, &S, &fmap, env_int("HB_TT_SECTOR_TOP", 4));
           if (st == HB_OK) {
@@ -1043,6 +1052,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
                        : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);
   info->code_cell_bits = m.ptt_rank ? m.rank_cw : 0;
   info->rank_prepass = m.rank_pre;
+  info->tt_sector = m.tt_sector;
   return HB_OK;
 }
 

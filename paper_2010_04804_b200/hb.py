@@ -51,7 +51,8 @@ class _Info(C.Structure):
                 ("device_bytes", C.c_int64), ("tree_stride_bytes", C.c_int64),
                 ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32),
                 ("kernel", C.c_int32), ("rows_per_cta", C.c_int32),
-                ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32)]
+                ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32),
+                ("tt_sector", C.c_int32)]
 
 
 def _load():

@@ -223,6 +223,7 @@ def test_tt_sector_layout_tree_shapes(cmp, monkeypatch):
         monkeypatch.setenv("HB_TT_SECTOR_TOP", sec.split(":")[1])
         m = hb.Model(e, strategy="tt", device=0)
         assert m.info["kernel_name"] == "tt_wide_kernel"
+        assert m.info["tt_sector"] == int(sec.split(":")[0])
         check_all(e, m, Xd, Xh, kinds=("predict", "raw", "leaf", "leaf_hash"))
         leaves.append(m.predict_leaf(Xd).cpu().numpy())
     assert all(np.array_equal(leaves[0], lv) for lv in leaves[1:])
