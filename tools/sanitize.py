@@ -26,6 +26,14 @@ cases = [
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32"}, "ptt"),
     ("ptt-rank-prepass-16", synth.gen_forest(40, 6, 12, seed=1),
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16"}, "ptt"),
+    ("ptt-rank-prepass-staged-16", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "1"}, "ptt"),
+    ("ptt-rank-prepass-staged-32-rb1", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_STAGED": "1", "HB_RC_RB": "1"}, "ptt"),
+    ("ptt-rank-prepass-rows8", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "0", "HB_RC_ROWS": "8"}, "ptt"),
+    ("tt-wide-sector", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
+     {"HB_TT_WIDE": "1", "HB_TT_SECTOR": "1"}, "tt"),
     ("tt-blocks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
      {"HB_TT_WIDE": "1", "HB_TT_BLOCK": "1"}, "tt"),
     ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
