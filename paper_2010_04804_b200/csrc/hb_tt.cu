@@ -35,6 +35,7 @@ struct TtParams {
   void *out;
   int nw, ns, ch, ntiles, x_smem, t_smem;
   int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
+  int top_prefetch;       // tt_wide_kernel: L1 prefetch of the next tree group's top levels
 };
 
 // node array offset inside a record: 16 B (BFS layout), 32 B (sector layout:
@@ -283,6 +284,19 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         nd[g] = reinterpret_cast<const uint2 *>(rec[g] + node_off<SEC>());
         idx[g] = 0;
       }
+      if (p.top_prefetch && r < 2) {
+        // warm L1 with the top levels (first two 128-B lines of the node
+        // array) of this lane's trees in the NEXT group: their first walk
+        // step would otherwise be an L2 round trip per group
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int t = base + G * slots + sub + g * slots;
+          if (t < p.n_trees_pad) {
+            const uint8_t *q = p.trees + (size_t)t * p.stride + node_off<SEC>() + 128 * r;
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+          }
+        }
+      }
       for (int l = 0; l < p.depth; ++l) {
         bool done = true;
 #pragma unroll
@@ -434,6 +448,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.x_smem = m.cfg.x_smem;
   p.t_smem = m.cfg.t_smem;
   p.x_prefetch = m.cfg.prefetch;
+  p.top_prefetch = m.tt_top_prefetch;
   const int64_t rows_per_tile = wide ? (int64_t)m.cfg.wide_rows : (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");

@@ -189,6 +189,7 @@ def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
     monkeypatch.setenv("HB_TT_WIDE", "1")
     monkeypatch.setenv("HB_TT_BLOCK", "1" if blocks == "1" else "0")
     monkeypatch.setenv("HB_TT_SECTOR", "1" if blocks == "sector" else "0")
+    monkeypatch.setenv("HB_TT_TOP_PF", "1" if kind in ("reg", "k7") else "0")
     seed = zlib.crc32(f"wide{kind}{cmp}".encode()) & 0xFFFF
     e = _forest(kind, 45, 9, 37, seed, FAMILIES[seed % 3], cmp)
     m = hb.Model(e, strategy="tt", device=0)
