@@ -698,6 +698,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         m->cfg = c;
         m->tt_g = env_int("HB_TT_G", 4);
         m->tt_top_prefetch = env_int("HB_TT_TOP_PF", 0);
+        m->tt_cursor = env_int("HB_TT_CURSOR", 0);
         // sector-paired records (one L2 sector per two levels of a walk):
         // AUTO when the BFS records exceed 3/4 of L2, i.e. deep levels come
         // from HBM (C5, 10k trees on one GPU: 16.96 -> 15.57 ms); an

@@ -36,6 +36,7 @@ struct TtParams {
   int nw, ns, ch, ntiles, x_smem, t_smem;
   int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
   int top_prefetch;       // tt_wide_kernel: L1 prefetch of the next tree group's top levels
+  int cursor;             // tt_wide_kernel: per-lane tree cursors instead of warp-synchronous groups
 };
 
 // node array offset inside a record: 16 B (BFS layout), 32 B (sector layout:
@@ -270,6 +271,69 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
     uint64_t h = 0;
+    // leaf of tree t reached (record rc, slot leaf): add its value / emit its id
+    auto finish = [&](int t, const uint8_t *rc, uint32_t leaf) {
+      const float *lv = reinterpret_cast<const float *>(rc + node_off<SEC>() + (size_t)8 * p.nslots);
+      if (p.w == 1) {
+        const float v = __ldg(lv + leaf);
+        if (NACC == 1) {
+          acc[0] += v;
+        } else {
+          const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rc));
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k0 == (uint32_t)k) acc[k] += v;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NACC; ++k)
+          if (k < p.K) acc[k] += __ldg(lv + leaf * p.w + k);
+      }
+      if (lm && t < p.n_trees) {
+        const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
+        if (lm == 1) {
+          if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+        } else {
+          h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+        }
+      }
+    };
+    if (p.cursor) {
+      // per-lane cursors: each of a lane's G walks moves on to its next tree
+      // (t += G * slots) as soon as it sits on a leaf, so a lane never idles
+      // on a finished walk while the warp's slowest path completes; the warp
+      // leaves the loop when every lane has run out of trees
+      const int tstep = G * slots;
+      int t[G];
+      uint32_t ix[G];
+      const uint8_t *rc[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        t[g] = warp * L + sub + g * slots;
+        ix[g] = 0;
+        rc[g] = p.trees + (size_t)min(t[g], p.n_trees_pad - 1) * p.stride;
+      }
+      while (true) {
+        bool act = false;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          if (t[g] < p.n_trees_pad) {
+            act = true;
+            bool dn = true;
+            uint32_t i = ix[g];
+            wide_step<LE, R, SEC>(reinterpret_cast<const uint2 *>(rc[g] + node_off<SEC>()), i, xs, r, dn);
+            if (dn) {
+              finish(t[g], rc[g], i);
+              t[g] += tstep;
+              i = 0;
+              rc[g] = p.trees + (size_t)min(t[g], p.n_trees_pad - 1) * p.stride;
+            }
+            ix[g] = i;
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, act)) break;
+      }
+    } else {
     // warp-uniform loop over groups of G tree slots (t = base + sub + g*slots)
     for (int base = warp * L; base < p.n_trees_pad; base += G * slots) {
       const uint8_t *rec[G];
@@ -304,35 +368,9 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
       }
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (!valid[g]) continue;
-        const int t = base + sub + g * slots;
-        const float *lv = reinterpret_cast<const float *>(nd[g] + p.nslots);
-        const uint32_t leaf = idx[g];
-        if (p.w == 1) {
-          const float v = __ldg(lv + leaf);
-          if (NACC == 1) {
-            acc[0] += v;
-          } else {
-            const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rec[g]));
-#pragma unroll
-            for (int k = 0; k < NACC; ++k)
-              if (k0 == (uint32_t)k) acc[k] += v;
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += __ldg(lv + leaf * p.w + k);
-        }
-        if (lm && t < p.n_trees) {
-          const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
-          if (lm == 1) {
-            if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
-          } else {
-            h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
-          }
-        }
-      }
+      for (int g = 0; g < G; ++g)
+        if (valid[g]) finish(base + sub + g * slots, rec[g], idx[g]);
+    }
     }
     // combine the L tree slots of a row inside the warp, then across warps
 #pragma unroll
@@ -449,6 +487,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.t_smem = m.cfg.t_smem;
   p.x_prefetch = m.cfg.prefetch;
   p.top_prefetch = m.tt_top_prefetch;
+  p.cursor = m.tt_cursor;
   const int64_t rows_per_tile = wide ? (int64_t)m.cfg.wide_rows : (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");

@@ -180,7 +180,7 @@ def test_ptt_special_thresholds(cmp, rank, monkeypatch):
 
 @pytest.mark.parametrize("kind", ["reg", "binary", "multiclass", "rf", "k7", "k12"])
 @pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("blocks", ["1", "0", "sector"])
+@pytest.mark.parametrize("blocks", ["1", "0", "sector", "cursor", "sector-cursor"])
 def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
     """The wide-row TT kernels (R rows per CTA, lanes = tree slot x row, nodes
     through L1/L2) forced on ordinary inputs: ttb_kernel (2-level node blocks,
@@ -188,7 +188,8 @@ def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
     the BFS and the sector-paired record layouts."""
     monkeypatch.setenv("HB_TT_WIDE", "1")
     monkeypatch.setenv("HB_TT_BLOCK", "1" if blocks == "1" else "0")
-    monkeypatch.setenv("HB_TT_SECTOR", "1" if blocks == "sector" else "0")
+    monkeypatch.setenv("HB_TT_SECTOR", "1" if blocks.startswith("sector") else "0")
+    monkeypatch.setenv("HB_TT_CURSOR", "1" if blocks.endswith("cursor") else "0")
     monkeypatch.setenv("HB_TT_TOP_PF", "1" if kind in ("reg", "k7") else "0")
     seed = zlib.crc32(f"wide{kind}{cmp}".encode()) & 0xFFFF
     e = _forest(kind, 45, 9, 37, seed, FAMILIES[seed % 3], cmp)
@@ -219,9 +220,12 @@ def test_tt_sector_layout_tree_shapes(cmp, monkeypatch):
     e = synth.from_trees(trees, F, cmp=cmp)
     Xd, Xh = X_pair(12, 2111, F, grid=synth.GRID_COARSE, special_q24=SPECIAL_Q24)
     leaves = []
-    for sec in ("1:0", "1:1", "1:4", "1:6", "0:0"):     # sector layout with 0/1/4/6 BFS top levels; BFS layout
+    # sector layout with 0/1/4/6 BFS top levels, BFS layout; warp-synchronous
+    # groups or per-lane tree cursors
+    for sec in ("1:0:0", "1:1:0", "1:4:1", "1:6:0", "0:0:0", "0:0:1"):
         monkeypatch.setenv("HB_TT_SECTOR", sec.split(":")[0])
         monkeypatch.setenv("HB_TT_SECTOR_TOP", sec.split(":")[1])
+        monkeypatch.setenv("HB_TT_CURSOR", sec.split(":")[2])
         m = hb.Model(e, strategy="tt", device=0)
         assert m.info["kernel_name"] == "tt_wide_kernel"
         assert m.info["tt_sector"] == int(sec.split(":")[0])
