@@ -568,6 +568,7 @@ static void free_model(Model *m) {
   cudaFree(m->d_fmap);
   cudaFree(m->d_tops);
   cudaFree(m->d_rb);
+  cudaFree(m->d_rbc);
   cudaFree(m->d_ttb);
   cudaFree(m->d_ttw);
   cudaFree(m->d_ttw_leafmap);

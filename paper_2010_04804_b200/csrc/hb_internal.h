@@ -74,6 +74,12 @@ struct Model {
   int rb_ngroups = 0;
   uint32_t rb_max_span = 0;  // widest X column span of a table group (staged pre-pass)
   bool rb_global = false;    // some table group is searched from global memory
+  // cluster pre-pass plan: <= 8 table groups, one per CTA of a cluster
+  int rbc_cl = 0;            // CTAs per cluster (0: no cluster plan)
+  void *d_rbc = nullptr;     // [feat | groups | own | pool]
+  size_t rbc_groups_off = 0, rbc_own_off = 0, rbc_pool_off = 0, rbc_smem = 0;
+  uint32_t rbc_max_pitch = 0;
+  int rbc_tile = 2048;       // rows per cluster tile (2048 or 1024)
   cudaMemPool_t mempool = nullptr;
 
   // small-batch path (hb_small.cu): PTT fp32 or TT records walked by
@@ -162,8 +168,11 @@ struct RankBuckets {
   bool any_global = false;        // some group's table exceeds the cap (searched from global memory)
 };
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
-                             int cw, RankBuckets *out);
+                             int cw, RankBuckets *out, size_t cap_bytes = 0);
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
+// cluster pre-pass (hb_rank_codes_cluster.cu): all tables in one cluster's SMEM
+size_t rank_cluster_stage_bytes(uint32_t max_pitch, int tile);
+hb_status launch_rank_codes_cluster(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);
 hb_status launch_tt(const Model &m, const RunArgs &a);

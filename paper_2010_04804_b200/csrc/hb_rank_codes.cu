@@ -59,11 +59,9 @@ struct RankCodeParams {
 // others the read-only global path.
 template <bool SM>
 __device__ __forceinline__ uint32_t tab_u32(const uint8_t *tb, uint32_t tsm, uint32_t off) {
-  if (SM) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(tsm + off));
-    return v;
-  }
+  // plain loads (no asm): the compiler may schedule the independent loads of
+  // a lockstep step together; tb points into shared memory when SM
+  if (SM) return *reinterpret_cast<const uint32_t *>(tb + off);
   return __ldg(reinterpret_cast<const uint32_t *>(tb + off));
 }
 
@@ -95,8 +93,10 @@ __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const 
     for (int c = 0; c < NC; ++c) {
       const uint32_t half = cnt[c] >> 1;
       const float v = __uint_as_float(tab_u32<SM>(tb, tsm, uo[c] + 4u * (base[c] + half)));
-      const bool go = cnt[c] != 0 && (LE ? v < x[c] : v <= x[c]);
-      base[c] = go ? base[c] + half + 1u : base[c];
+      // branch-free (the load is unconditional: u has a pad slot), so the
+      // NC chains of one step overlap instead of each waiting on its load
+      const uint32_t go = (uint32_t)(LE ? v < x[c] : v <= x[c]) & (uint32_t)(cnt[c] != 0);
+      base[c] += go * (half + 1u);
       cnt[c] = go ? cnt[c] - half - 1u : half;
     }
   }
@@ -375,10 +375,11 @@ uint32_t host_bucket(float x, float lo, float hi, float s, uint32_t B) {
 // Bucket tables for the sorted distinct thresholds of each compact feature
 // (sorted[c], feature id orig[c]); words group 1 (CW 32) or 2 (CW 16) features.
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
-                             int cw, RankBuckets *out) {
+                             int cw, RankBuckets *out, size_t cap_bytes) {
   // per-CTA table budget: 48 KB -> 4 CTAs (32 warps) per SM (HB_RC_SMEM_KB overrides)
   const char *ev = std::getenv("HB_RC_SMEM_KB");
-  const size_t cap = std::min<size_t>(kRcSmemMax, (ev && *ev ? (size_t)std::atoi(ev) : 48) * 1024);
+  const size_t cap = cap_bytes ? cap_bytes
+                               : std::min<size_t>(kRcSmemMax, (ev && *ev ? (size_t)std::atoi(ev) : 48) * 1024);
   out->smem_cap = cap;
   const int n_fc = (int)sorted.size();
   const int per_word = cw == 32 ? 1 : 2;
@@ -491,6 +492,10 @@ int sm_count(int device);
 
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks) {
   if (m.rb_ngroups == 0 || nblocks == 0) return HB_OK;   // no split uses any feature: no codes
+  // the cluster kernel when the model has a cluster plan (all tables in one
+  // cluster's SMEM) and no per-group kernel is forced (HB_RC_STAGED=0/1)
+  const char *force = std::getenv("HB_RC_STAGED");
+  if (m.rbc_cl > 0 && !(force && *force && std::atoi(force) >= 0)) return launch_rank_codes_cluster(m, a, codes, nblocks);
   RankCodeParams p;
   p.X = a.X;
   p.n = a.n;
@@ -515,7 +520,7 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   const char *erb = std::getenv("HB_RC_RB");
   const size_t pitch = (size_t)(m.rb_max_span | 1u);
   const size_t stage_budget = 64 * 1024;
-  int rb = 4;
+  int rb = 2;           // C3: 13.46 ms per step with 2 row blocks per stage, 13.64 with 4
   while (rb > 1 && (size_t)kRcWarps * kStStages * rb * 32 * pitch * 4 > stage_budget) rb >>= 1;
   if (erb && *erb) rb = std::atoi(erb) >= 4 ? 4 : (std::atoi(erb) >= 2 ? 2 : 1);
   const size_t staged_smem = tbytes + (size_t)kRcWarps * kStStages * rb * 32 * pitch * 4;

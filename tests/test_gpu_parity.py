@@ -865,3 +865,29 @@ def test_rank_prepass_staged_spans(cw, rb, monkeypatch):
         for n, ldx in ((1, 61), (33, 63), (4 * 32 * 5 + 7, 61), (2000, 67)):
             Xd, Xh = X_pair(20 + n, n, 61, ldx=ldx, special_q24=SPECIAL_Q24)
             check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("cw", ["32", "16"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_rank_prepass_cluster(cw, cmp, monkeypatch):
+    """Cluster pre-pass (hb_rank_codes_cluster.cu): every table group in the
+    SMEM of one CTA of a thread-block cluster, X rows scattered to the owners
+    over DSMEM. Models whose tables split into 1..8 groups (tiny, C3-like
+    single-feature tables, many features with feature selection gaps), row
+    counts that end inside a tile, an odd row stride; codes must give the
+    exact fp32 walk."""
+    _set_layout(monkeypatch, "pre" + cw)
+    monkeypatch.setenv("HB_RC_STAGED", "-1")
+    monkeypatch.setenv("HB_RC_CLUSTER", "1")
+    used = np.sort(np.random.default_rng(21).choice(50, 37, replace=False))
+    cases = [synth.gen_forest(40, 6, 12, seed=1 + cmp, cmp=cmp),
+             synth.gen_forest(300, 8, 9, seed=2 + cmp, family="balanced", cmp=cmp,
+                              post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION),
+             synth.gen_forest(200, 8, 50, seed=3 + cmp, family="mixed", features=used, cmp=cmp)]
+    for e in cases:
+        m = hb.Model(e, strategy="ptt", device=0)
+        assert m.info["rank_prepass"] == 1 and m.info["code_cell_bits"] == int(cw)
+        F = e.n_features
+        for n, ldx in ((1, F), (1023, F + 1), (5000, F), (40000, F)):
+            Xd, Xh = X_pair(30 + n, n, F, ldx=ldx, special_q24=SPECIAL_Q24)
+            check_all(e, m, Xd, Xh, kinds=("predict", "raw", "leaf_hash"))
