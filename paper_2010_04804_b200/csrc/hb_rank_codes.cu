@@ -244,9 +244,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool LE, int CW, int RB, bool SM>
+template <bool LE, int CW, int RB, bool SM, bool ONE>
 __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, const uint4 g, const uint4 gs,
                                                       const uint8_t *tb, uint8_t *smem) {
+  // ONE (32-bit cells only): one feature per lockstep set, RB row blocks of
+  // it — for single-feature table groups, where a feature pair would leave
+  // half the chains idle
+  constexpr int NSL = (CW == 32 && ONE) ? 1 : 2;
   const uint32_t tsm = SM ? (uint32_t)__cvta_generic_to_shared(tb) : 0u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncols = (int)gs.y, pitch = (int)gs.z;
@@ -279,7 +283,7 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
     cp_async_commit();   // empty groups keep the wait count uniform
   };
   constexpr int PW = CW == 32 ? 1 : 2;
-  constexpr int WS = 2 / PW;          // words per feature pair
+  constexpr int WS = NSL / PW;        // words per lockstep set
   int64_t u = (int64_t)blockIdx.x * kRcWarps + warp;
 #pragma unroll
   for (int s = 0; s < kStStages - 1; ++s) issue(u + s * ustep, s);
@@ -289,14 +293,14 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
     cp_async_wait<kStStages - 1>();
     __syncwarp();
     const uint32_t *xr = xs + st * stage_words + lane * pitch;
-    // two features x RB rows per lockstep search
+    // NSL features x RB rows per lockstep search
     for (int wd = (int)g.z; wd < (int)g.w; wd += WS) {
-      uint4 M0[2], M1[2];
-      bool ok[2];
-      float x8[2 * RB];
-      int mi[2 * RB];
+      uint4 M0[NSL], M1[NSL];
+      bool ok[2] = {true, false};
+      float x8[NSL * RB];
+      int mi[NSL * RB];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
+      for (int e = 0; e < NSL; ++e) {
         const int c = PW * wd + e;
         ok[e] = (PW == 2 ? wd : wd + e) < (int)g.w && c < p.n_fc;
         const int cc = ok[e] ? c : PW * wd;
@@ -309,9 +313,9 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
           mi[e * RB + i] = e;
         }
       }
-      const uint32_t smax = max(M0[0].z, ok[1] ? M0[1].z : 0u);
-      uint32_t code[2 * RB];
-      rank_codes_lockstep<LE, SM, 2 * RB>(x8, M0, M1, mi, smax, tb, tsm, code);
+      const uint32_t smax = NSL == 1 ? M0[0].z : max(M0[0].z, ok[1] ? M0[NSL - 1].z : 0u);
+      uint32_t code[NSL * RB];
+      rank_codes_lockstep<LE, SM, NSL * RB>(x8, M0, M1, mi, smax, tb, tsm, code);
 #pragma unroll
       for (int i = 0; i < RB; ++i) {
         const int64_t blk = u * RB + i;
@@ -319,9 +323,9 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
         uint32_t *dst = p.codes + ((size_t)blk * p.n_words + wd) * 32 + lane;
         if (CW == 32) {
           dst[0] = ((uint32_t)wd << 23) | code[i];
-          if (ok[1]) dst[32] = ((uint32_t)(wd + 1) << 23) | code[RB + i];
+          if (NSL == 2 && ok[1]) dst[32] = ((uint32_t)(wd + 1) << 23) | code[(NSL - 1) * RB + i];
         } else {
-          dst[0] = code[i] | ((ok[1] ? code[RB + i] : 0u) << 16);
+          dst[0] = code[i] | ((ok[1] ? code[(NSL - 1) * RB + i] : 0u) << 16);
         }
       }
     }
@@ -331,7 +335,7 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
   cp_async_wait<0>();
 }
 
-template <bool LE, int CW, int RB>
+template <bool LE, int CW, int RB, bool ONE>
 __global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint4 g = __ldg(p.groups + 2 * blockIdx.y);
@@ -342,22 +346,25 @@ __global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(cons
     uint4 *dst = reinterpret_cast<uint4 *>(smem);
     for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
-    rank_code_staged_body<LE, CW, RB, true>(p, g, gs, smem, smem);
+    rank_code_staged_body<LE, CW, RB, true, ONE>(p, g, gs, smem, smem);
   } else {
-    rank_code_staged_body<LE, CW, RB, false>(p, g, gs, tb, smem);
+    rank_code_staged_body<LE, CW, RB, false, ONE>(p, g, gs, tb, smem);
   }
 }
 
-template <bool LE, int CW>
+template <bool LE, int CW, bool ONE>
 RcFn staged_pick_rb(int rb) {
-  if (rb >= 4) return rank_code_staged_kernel<LE, CW, 4>;
-  if (rb == 2) return rank_code_staged_kernel<LE, CW, 2>;
-  return rank_code_staged_kernel<LE, CW, 1>;
+  if (rb >= 4) return rank_code_staged_kernel<LE, CW, 4, ONE>;
+  if (rb == 2) return rank_code_staged_kernel<LE, CW, 2, ONE>;
+  return rank_code_staged_kernel<LE, CW, 1, ONE>;
 }
 
-RcFn staged_pick(bool le, int cw, int rb) {
-  if (cw == 32) return le ? staged_pick_rb<true, 32>(rb) : staged_pick_rb<false, 32>(rb);
-  return le ? staged_pick_rb<true, 16>(rb) : staged_pick_rb<false, 16>(rb);
+RcFn staged_pick(bool le, int cw, int rb, bool one) {
+  if (cw == 32) {
+    if (one) return le ? staged_pick_rb<true, 32, true>(rb) : staged_pick_rb<false, 32, true>(rb);
+    return le ? staged_pick_rb<true, 32, false>(rb) : staged_pick_rb<false, 32, false>(rb);
+  }
+  return le ? staged_pick_rb<true, 16, false>(rb) : staged_pick_rb<false, 16, false>(rb);
 }
 
 // Host twin of the bucket map in rank_code(): same fp32 operations, same
@@ -520,7 +527,14 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   const char *erb = std::getenv("HB_RC_RB");
   const size_t pitch = (size_t)(m.rb_max_span | 1u);
   const size_t stage_budget = 64 * 1024;
-  int rb = 2;           // C3: 13.46 ms per step with 2 row blocks per stage, 13.64 with 4
+  // single-feature groups (32-bit cells, one word per group): one feature
+  // per lockstep set over 4 row blocks (HB_RC_ONE=0/1 forces)
+  const char *eone = std::getenv("HB_RC_ONE");
+  bool one = m.rank_cw == 32 && m.rb_ngroups == m.rank_nwords;
+  if (eone && *eone) one = m.rank_cw == 32 && std::atoi(eone) != 0;
+  // 2 row blocks per stage: C3 13.13 ms per step (single-feature sets; 4
+  // blocks: 13.39); feature pairs: 13.46 (4 blocks: 13.64)
+  int rb = 2;
   while (rb > 1 && (size_t)kRcWarps * kStStages * rb * 32 * pitch * 4 > stage_budget) rb >>= 1;
   if (erb && *erb) rb = std::atoi(erb) >= 4 ? 4 : (std::atoi(erb) >= 2 ? 2 : 1);
   const size_t staged_smem = tbytes + (size_t)kRcWarps * kStStages * rb * 32 * pitch * 4;
@@ -536,7 +550,7 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   if (ev && *ev && std::atoi(ev) >= 0) staged = fits && std::atoi(ev) != 0;   // -1: AUTO
   const char *erows = std::getenv("HB_RC_ROWS");
   const int rows = erows && std::atoi(erows) == 8 ? 8 : kRcRows;
-  RcFn fn = staged ? staged_pick(m.cmp == HB_CMP_LE, m.rank_cw, rb) : rc_pick(m.cmp == HB_CMP_LE, m.rank_cw, rows);
+  RcFn fn = staged ? staged_pick(m.cmp == HB_CMP_LE, m.rank_cw, rb, one) : rc_pick(m.cmp == HB_CMP_LE, m.rank_cw, rows);
   const int smem = (int)(staged ? staged_smem : m.rb_smem);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(rank codes)");

@@ -842,7 +842,7 @@ def test_tt_cluster_kernel_parity(kind, cmp, monkeypatch):
     check_all(e, m, Xd2, Xh2, kinds=("raw", "leaf"))
 
 
-@pytest.mark.parametrize("rb", ["1", "2", "4"])
+@pytest.mark.parametrize("rb", ["1", "2", "4", "4:one", "2:one"])
 @pytest.mark.parametrize("cw", ["32", "16"])
 def test_rank_prepass_staged_spans(cw, rb, monkeypatch):
     """Staged pre-pass (cp.async X staging, hb_rank_codes.cu): table groups
@@ -853,7 +853,8 @@ def test_rank_prepass_staged_spans(cw, rb, monkeypatch):
     scores must match the oracle exactly / within tolerance."""
     _set_layout(monkeypatch, "pre" + cw)
     monkeypatch.setenv("HB_RC_STAGED", "1")
-    monkeypatch.setenv("HB_RC_RB", rb)
+    monkeypatch.setenv("HB_RC_RB", rb.split(":")[0])
+    monkeypatch.setenv("HB_RC_ONE", "1" if rb.endswith("one") else "0")   # one feature per lockstep set (32-bit)
     monkeypatch.setenv("HB_RC_SMEM_KB", "4")
     monkeypatch.setenv("HB_SMALL_BATCH", "0")     # small n must reach the pre-pass too
     used = np.sort(np.random.default_rng(11).choice(61, 13, replace=False))
