@@ -179,7 +179,10 @@ def workload_config(cfg, e, rows, args, mode="rows"):
     return {"workload": f"{cfg.name}: {cfg.note}", "rows_per_gpu": rows, "n_trees": e.n_trees,
             "max_depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": e.n_outputs,
             "family": cfg.family, "parallelism": par,
-            "l2": "inputs larger than L2 (X streamed once per step); model (<13 MB) L2-resident by design"}
+            "l2": ("X larger than L2 (streamed once per step, no flush needed); model (<13 MB) "
+                   "L2-resident by design" if cfg.depth <= 10 else
+                   "X larger than L2 (streamed once per step, no flush needed); depth-12 node records: "
+                   "a 1/8 tree shard (~60 MB) is L2-resident, all 10k trees (~480 MB) are not")}
 
 
 # ----------------------------------------------------------------- ours
@@ -411,7 +414,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak" if mode == "rows" else "strong",
             "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded splitmix64 grid X; random balanced depth-8 forest)",
+            "data": f"synthetic (seeded splitmix64 grid X; random {cfg.family} depth-{cfg.depth} forest)",
             "config": dict(workload_config(cfg, e, n, args, mode), strategy=info["strategy_name"],
                            output=kind, trees_per_gpu=t1 - t0,
                            timing=("CUDA graph of %d calls per timed step, value per call" % calls)

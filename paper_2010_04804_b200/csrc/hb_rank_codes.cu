@@ -53,6 +53,8 @@ struct RankCodeParams {
   uint32_t *codes;        // [nblocks][n_words][32]
   int64_t nblocks;
   uint32_t stage_off;     // staged kernel: SMEM byte offset of the X staging buffers
+  int gorder;             // staged kernel: 1 = blockIdx.x is the table group and each CTA
+                          // owns a contiguous row range (groups of the same rows co-resident)
 };
 
 // Table reads: SMEM-resident groups use 32-bit shared addresses (LDS), the
@@ -261,11 +263,18 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
   const int row_l = lane / ncols, col_l = lane - row_l * ncols;
   const float *xg = p.X + gs.x;
   const int64_t nunits = (p.nblocks + RB - 1) / RB;
-  const int64_t ustep = (int64_t)gridDim.x * kRcWarps;
+  // unit range of this CTA: strided over the grid (gorder 0) or one
+  // contiguous slice (gorder 1: the CTAs of all groups for the same rows are
+  // launched together and read the same X sectors at about the same time)
+  const int64_t nparts = p.gorder ? gridDim.y : gridDim.x;
+  const int64_t part = p.gorder ? blockIdx.y : blockIdx.x;
+  const int64_t uend = p.gorder ? (part + 1) * nunits / nparts : nunits;
+  const int64_t ustep = p.gorder ? (int64_t)kRcWarps : nparts * kRcWarps;
+  const int64_t ubeg = p.gorder ? part * nunits / nparts : part * kRcWarps;
   // copy unit u's rows (clamped to the last row: the tail block computes
   // valid, unused codes) into stage st
   auto issue = [&](int64_t u, int st) {
-    if (u < nunits) {
+    if (u < uend) {
       const int64_t r0 = u * RB * 32;
       const uint32_t d0 = xs_s + (uint32_t)st * stage_words * 4u;
       int row = row_l, col = col_l;
@@ -284,11 +293,11 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
   };
   constexpr int PW = CW == 32 ? 1 : 2;
   constexpr int WS = NSL / PW;        // words per lockstep set
-  int64_t u = (int64_t)blockIdx.x * kRcWarps + warp;
+  int64_t u = ubeg + warp;
 #pragma unroll
   for (int s = 0; s < kStStages - 1; ++s) issue(u + s * ustep, s);
   int st = 0;
-  for (; u < nunits; u += ustep) {
+  for (; u < uend; u += ustep) {
     issue(u + (kStStages - 1) * ustep, st == 0 ? kStStages - 1 : st - 1);
     cp_async_wait<kStStages - 1>();
     __syncwarp();
@@ -338,8 +347,9 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
 template <bool LE, int CW, int RB, bool ONE>
 __global__ void __launch_bounds__(32 * kRcWarps, 2) rank_code_staged_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint4 g = __ldg(p.groups + 2 * blockIdx.y);
-  const uint4 gs = __ldg(p.groups + 2 * blockIdx.y + 1);   // {col_lo, ncols, pitch, 0}
+  const int gi = p.gorder ? blockIdx.x : blockIdx.y;
+  const uint4 g = __ldg(p.groups + 2 * gi);
+  const uint4 gs = __ldg(p.groups + 2 * gi + 1);   // {col_lo, ncols, pitch, 0}
   const uint8_t *tb = p.pool + g.x;
   if (g.y <= p.smem_cap) {
     const uint4 *src = reinterpret_cast<const uint4 *>(tb);
@@ -561,7 +571,10 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   const int64_t want = std::max<int64_t>(1, ((int64_t)per_sm * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
   const int64_t rows_per_cta = (int64_t)kRcWarps * (staged ? rb : rows);
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (nblocks + rows_per_cta - 1) / rows_per_cta));
-  fn<<<dim3(gx, m.rb_ngroups), 32 * kRcWarps, smem, a.stream>>>(p);
+  const char *eord = std::getenv("HB_RC_ORDER");
+  p.gorder = staged && eord && *eord ? (std::atoi(eord) != 0) : 0;
+  const dim3 grid = p.gorder ? dim3(m.rb_ngroups, gx) : dim3(gx, m.rb_ngroups);
+  fn<<<grid, 32 * kRcWarps, smem, a.stream>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "rank_code_kernel launch");
   return HB_OK;

@@ -44,7 +44,10 @@ def test_gpu_arm_contract():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 300000 * 28 * 4
-    assert d["gpu_launches"] == 3 and d["scaling"] == "weak" and d["n_gpus"] == 1
+    # one hb_predict call per step: one launch, two when the model runs the
+    # rank-code pre-pass (C3's AUTO layout does)
+    per_call = 2 if d["roofline"]["layout"].endswith("-pre") else 1
+    assert d["gpu_launches"] == 3 * per_call and d["scaling"] == "weak" and d["n_gpus"] == 1
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
 
 
