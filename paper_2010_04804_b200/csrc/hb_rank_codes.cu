@@ -572,7 +572,10 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   const int64_t rows_per_cta = (int64_t)kRcWarps * (staged ? rb : rows);
   const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(want, (nblocks + rows_per_cta - 1) / rows_per_cta));
   const char *eord = std::getenv("HB_RC_ORDER");
-  p.gorder = staged && eord && *eord ? (std::atoi(eord) != 0) : 0;
+  // group-major grid with contiguous row slices for the staged kernel: the 28
+  // single-feature groups of C3 then read X from DRAM ~1.25x instead of ~5.4x
+  // (ncu: 6.1 -> 1.4 GB per launch; C3 13.12 -> 12.92 ms, C4 46.8 -> 46.0 ms)
+  p.gorder = staged && !(eord && *eord && std::atoi(eord) == 0);
   const dim3 grid = p.gorder ? dim3(m.rb_ngroups, gx) : dim3(gx, m.rb_ngroups);
   fn<<<grid, 32 * kRcWarps, smem, a.stream>>>(p);
   e = cudaGetLastError();
