@@ -416,8 +416,13 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
         hi = v;
         any = true;
       }
+    // <= 2 thresholds per bucket on average (HB_RC_DENSITY=d: <= 2/d)
+    static const int dens = [] {
+      const char *e = std::getenv("HB_RC_DENSITY");
+      return e && *e ? std::max(1, std::atoi(e)) : 1;
+    }();
     uint32_t B = 1;
-    while (2 * B < m && B < 16384u) B <<= 1;     // <= 2 thresholds per bucket on average
+    while (2 * B < m * (uint32_t)dens && B < 16384u) B <<= 1;
     float s = 0.f;
     if (hi > lo) {
       const float range = hi - lo;
