@@ -842,9 +842,10 @@ def test_tt_cluster_kernel_parity(kind, cmp, monkeypatch):
     check_all(e, m, Xd2, Xh2, kinds=("raw", "leaf"))
 
 
+@pytest.mark.parametrize("order", ["1", "0"])   # group-major grid with row slices / strided units
 @pytest.mark.parametrize("rb", ["1", "2", "4", "4:one", "2:one"])
 @pytest.mark.parametrize("cw", ["32", "16"])
-def test_rank_prepass_staged_spans(cw, rb, monkeypatch):
+def test_rank_prepass_staged_spans(cw, rb, order, monkeypatch):
     """Staged pre-pass (cp.async X staging, hb_rank_codes.cu): table groups
     whose features are scattered columns (the copied span has gaps), an odd
     row stride (4-B aligned rows only), row counts that end inside a 32-row
@@ -855,6 +856,7 @@ def test_rank_prepass_staged_spans(cw, rb, monkeypatch):
     monkeypatch.setenv("HB_RC_STAGED", "1")
     monkeypatch.setenv("HB_RC_RB", rb.split(":")[0])
     monkeypatch.setenv("HB_RC_ONE", "1" if rb.endswith("one") else "0")   # one feature per lockstep set (32-bit)
+    monkeypatch.setenv("HB_RC_ORDER", order)
     monkeypatch.setenv("HB_RC_SMEM_KB", "4")
     monkeypatch.setenv("HB_SMALL_BATCH", "0")     # small n must reach the pre-pass too
     used = np.sort(np.random.default_rng(11).choice(61, 13, replace=False))
