@@ -120,8 +120,15 @@ __device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const ui
   constexpr int NB = kRcBatch / (ROWS * PW) > 0 ? kRcBatch / (ROWS * PW) : 1;   // words per batch
   constexpr int NS = NB * PW;                            // feature slots per batch (even)
   static_assert(NS % 2 == 0, "feature slots go in pairs");
-  for (int64_t rb0 = ((int64_t)blockIdx.x * kRcWarps + warp) * ROWS; rb0 < p.nblocks;
-       rb0 += (int64_t)gridDim.x * kRcWarps * ROWS) {
+  // batches of ROWS row blocks: strided over the grid (gorder 0) or one
+  // contiguous slice per CTA (gorder 1, group-major grid: see the staged kernel)
+  const int64_t nbat = (p.nblocks + ROWS - 1) / ROWS;
+  const int64_t nparts = p.gorder ? gridDim.y : gridDim.x;
+  const int64_t part = p.gorder ? blockIdx.y : blockIdx.x;
+  const int64_t bend = p.gorder ? (part + 1) * nbat / nparts : nbat;
+  const int64_t bstep = p.gorder ? (int64_t)kRcWarps : nparts * kRcWarps;
+  for (int64_t bt = (p.gorder ? part * nbat / nparts : part * kRcWarps) + warp; bt < bend; bt += bstep) {
+    const int64_t rb0 = bt * ROWS;
     // rows past n (and row blocks past the end) read row 0 and are not stored
     const float *xr[ROWS];
 #pragma unroll
@@ -206,7 +213,7 @@ __device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const ui
 template <bool LE, int CW, int ROWS>
 __global__ void __launch_bounds__(32 * kRcWarps, ROWS == 4 ? 4 : 3) rank_code_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint4 g = __ldg(p.groups + 2 * blockIdx.y);
+  const uint4 g = __ldg(p.groups + 2 * (p.gorder ? blockIdx.x : blockIdx.y));
   const uint8_t *tb = p.pool + g.x;
   if (g.y <= p.smem_cap) {
     const uint4 *src = reinterpret_cast<const uint4 *>(tb);
@@ -580,7 +587,8 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   // group-major grid with contiguous row slices for the staged kernel: the 28
   // single-feature groups of C3 then read X from DRAM ~1.25x instead of ~5.4x
   // (ncu: 6.1 -> 1.4 GB per launch; C3 13.12 -> 12.92 ms, C4 46.8 -> 46.0 ms)
-  p.gorder = staged && !(eord && *eord && std::atoi(eord) == 0);
+  // (direct kernel on C2: 1.80 -> 1.78 ms per step); HB_RC_ORDER=0 reverts
+  p.gorder = !(eord && *eord && std::atoi(eord) == 0);
   const dim3 grid = p.gorder ? dim3(m.rb_ngroups, gx) : dim3(gx, m.rb_ngroups);
   fn<<<grid, 32 * kRcWarps, smem, a.stream>>>(p);
   e = cudaGetLastError();

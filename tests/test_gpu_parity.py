@@ -730,9 +730,9 @@ def test_sixteen_outputs_vector_leaves(strat, small, monkeypatch):
     check_all(e, m, Xd, Xh)
 
 
-@pytest.mark.parametrize("staged", ["0", "1", "0:8"])   # direct, staged, direct with 8 row blocks per batch
-@pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("cw", ["32", "16"])
+@pytest.mark.parametrize("staged", ["0", "1", "0:8", "0:4:0"])   # direct, staged, direct with 8 row
+@pytest.mark.parametrize("cmp", [0, 1])                          # blocks per batch, direct with the
+@pytest.mark.parametrize("cw", ["32", "16"])                     # strided (not group-major) grid
 def test_rank_prepass_bucket_edges(cmp, cw, staged, monkeypatch):
     """Bucketed rank search of the pre-pass (hb_rank_codes.cu) at its edges:
     a feature with ~35K distinct thresholds (16384 buckets, table searched from
@@ -743,6 +743,7 @@ def test_rank_prepass_bucket_edges(cmp, cw, staged, monkeypatch):
     _set_layout(monkeypatch, "pre" + cw)
     monkeypatch.setenv("HB_RC_STAGED", staged.split(":")[0])
     monkeypatch.setenv("HB_RC_ROWS", staged.split(":")[1] if ":" in staged else "4")
+    monkeypatch.setenv("HB_RC_ORDER", staged.split(":")[2] if staged.count(":") == 2 else "1")
     rng = np.random.default_rng(40 + cmp)
     F = 6     # even and all used: 16-bit cells load feature pairs as one float2
     e = synth.gen_forest(400, 8, F, seed=41, family="balanced", cmp=cmp,
