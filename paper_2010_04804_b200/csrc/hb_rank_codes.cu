@@ -19,6 +19,15 @@
 // computed on the host by applying the same b() to every u_j, so the result is
 // exact whatever rounding b() does — the fp32 compares against u_j decide.
 // NaN -> 0xFFFF (sorts after every threshold: "go right", as x < t is false).
+//
+// Two per-group kernels, one CTA = one table group in SMEM:
+//   rank_code_kernel         direct strided X loads (lane = row), for groups of
+//                            several features (C2);
+//   rank_code_staged_kernel  X columns staged with cp.async, for narrow groups
+//                            (C3, C4) or tables searched from global memory.
+// Both run the searches of a batch in lockstep (rank_codes_lockstep) and use
+// a group-major grid with contiguous row slices. The cluster variant (all
+// tables in one cluster's DSMEM) is in hb_rank_codes_cluster.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,14 +62,14 @@ struct RankCodeParams {
   uint32_t *codes;        // [nblocks][n_words][32]
   int64_t nblocks;
   uint32_t stage_off;     // staged kernel: SMEM byte offset of the X staging buffers
-  int gorder;             // staged kernel: 1 = blockIdx.x is the table group and each CTA
-                          // owns a contiguous row range (groups of the same rows co-resident)
+  int gorder;             // 1 = blockIdx.x is the table group and each CTA owns a contiguous
+                          // row range (the groups of the same rows run together); 0 = strided
 };
 
-// Table reads: SMEM-resident groups use 32-bit shared addresses (LDS), the
+// Table reads: SMEM-resident groups are plain shared-memory loads (LDS), the
 // others the read-only global path.
 template <bool SM>
-__device__ __forceinline__ uint32_t tab_u32(const uint8_t *tb, uint32_t tsm, uint32_t off) {
+__device__ __forceinline__ uint32_t tab_u32(const uint8_t *tb, uint32_t off) {
   // plain loads (no asm): the compiler may schedule the independent loads of
   // a lockstep step together; tb points into shared memory when SM
   if (SM) return *reinterpret_cast<const uint32_t *>(tb + off);
@@ -75,7 +84,7 @@ __device__ __forceinline__ uint32_t tab_u32(const uint8_t *tb, uint32_t tsm, uin
 template <bool LE, bool SM, int NC>
 __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const uint4 *m0, const uint4 *m1,
                                                     const int (&mi)[NC], uint32_t smax, const uint8_t *tb,
-                                                    uint32_t tsm, uint32_t (&code)[NC]) {
+                                                    uint32_t (&code)[NC]) {
   uint32_t base[NC], cnt[NC], uo[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -85,7 +94,7 @@ __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const 
     float y = __fmul_rn(__fsub_rn(xc, lo), sc);
     y = fminf(y, (float)(a.y - 1u));
     const uint32_t bk = __float2uint_rz(y);
-    const uint32_t be = tab_u32<SM>(tb, tsm, a.w + 4u * bk);   // first index | count << 16
+    const uint32_t be = tab_u32<SM>(tb, a.w + 4u * bk);   // first index | count << 16
     base[c] = be & 0xFFFFu;
     cnt[c] = be >> 16;
     uo[c] = b.w;
@@ -94,7 +103,7 @@ __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const 
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const uint32_t half = cnt[c] >> 1;
-      const float v = __uint_as_float(tab_u32<SM>(tb, tsm, uo[c] + 4u * (base[c] + half)));
+      const float v = __uint_as_float(tab_u32<SM>(tb, uo[c] + 4u * (base[c] + half)));
       // branch-free (the load is unconditional: u has a pad slot), so the
       // NC chains of one step overlap instead of each waiting on its load
       const uint32_t go = (uint32_t)(LE ? v < x[c] : v <= x[c]) & (uint32_t)(cnt[c] != 0);
@@ -108,7 +117,6 @@ __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const 
 
 template <bool LE, int CW, bool SM, int ROWS>
 __device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const uint4 g, const uint8_t *tb) {
-  const uint32_t tsm = SM ? (uint32_t)__cvta_generic_to_shared(tb) : 0u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // one warp = ROWS 32-row blocks, all words of this group: lane = row, so
   // the strided X reads of consecutive features hit the sectors the first one
@@ -187,7 +195,7 @@ __device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const ui
           }
         const uint32_t smax = max(ok[sp] ? M0[0].z : 0u, ok[sp + 1] ? M0[1].z : 0u);
         uint32_t code[2 * ROWS];
-        rank_codes_lockstep<LE, SM, 2 * ROWS>(x8, M0, M1, mi, smax, tb, tsm, code);
+        rank_codes_lockstep<LE, SM, 2 * ROWS>(x8, M0, M1, mi, smax, tb, code);
 #pragma unroll
         for (int i = 0; i < ROWS; ++i) {
           if (rb0 + i >= p.nblocks) continue;
@@ -260,7 +268,6 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
   // it — for single-feature table groups, where a feature pair would leave
   // half the chains idle
   constexpr int NSL = (CW == 32 && ONE) ? 1 : 2;
-  const uint32_t tsm = SM ? (uint32_t)__cvta_generic_to_shared(tb) : 0u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncols = (int)gs.y, pitch = (int)gs.z;
   const uint32_t stage_words = (uint32_t)(RB * 32 * pitch);
@@ -331,7 +338,7 @@ __device__ __forceinline__ void rank_code_staged_body(const RankCodeParams &p, c
       }
       const uint32_t smax = NSL == 1 ? M0[0].z : max(M0[0].z, ok[1] ? M0[NSL - 1].z : 0u);
       uint32_t code[NSL * RB];
-      rank_codes_lockstep<LE, SM, NSL * RB>(x8, M0, M1, mi, smax, tb, tsm, code);
+      rank_codes_lockstep<LE, SM, NSL * RB>(x8, M0, M1, mi, smax, tb, code);
 #pragma unroll
       for (int i = 0; i < RB; ++i) {
         const int64_t blk = u * RB + i;
