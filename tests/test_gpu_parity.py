@@ -640,6 +640,26 @@ def test_c5_shard_sampled():
     torch.cuda.empty_cache()
 
 
+def test_c5_full_model_sector_records_sampled():
+    """C5 with all 10k trees on one GPU: the BFS records exceed 3/4 of L2, so
+    AUTO builds sector-paired records (hb_model_info.tt_sector); sampled rows
+    of the proba / leaf hash against the oracle, in bench.py's launch shape."""
+    c, e = synth.make_config("C5")
+    m = hb.Model(e, device=0)
+    assert m.info["strategy_name"] == "tt" and m.info["tt_sector"] == 1
+    n = 20_000
+    X = synth.dev.gen_X_device(c.seed_x, n, c.n_features)
+    proba = m.predict_proba(X).cpu().numpy().astype(np.float64)
+    hsh = m.predict_leaf_hash(X).cpu().numpy().view(np.uint64)
+    for r0 in (0, n - 300):
+        Xh = synth.gen_X(c.seed_x, 300, c.n_features, row_offset=r0)
+        s = oracle.scores(e, Xh)
+        assert_scores(proba[r0:r0 + 300], oracle.proba(e, s["post"]), "C5 proba")
+        assert np.array_equal(hsh[r0:r0 + 300], oracle.leaf_hash(e, Xh))
+    del X
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("strat", ["ptt", "tt"])
 def test_isolation_forest_parity(strat):
     """f4: IsolationForest (Table 1) — sklearn-trained forest exported as
