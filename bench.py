@@ -358,8 +358,12 @@ def run_ours(args):
                         "traffic_smem = SMEM load wavefronts x 128 B per launch, the on-chip "
                         "counterpart of the algorithmic bytes",
         "traffic_source": prof.get("source"),
+        # cross-check in bytes the kernel really loads from SMEM (ncu), over the
+        # whole timed call (the pre-pass launch included when there is one)
+        "frac_ncu_smem_bytes": (prof["smem_ld_bytes_per_launch"] / (kern_ms * 1e-3) / 1e9 / smem_peak)
+        if (same_launch and bound == "smem" and prof.get("smem_ld_bytes_per_launch")) else None,
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
-        "kernel_ms_covers": ("rank_code_kernel + pttr_kernel (both launches of one hb_predict call; "
+        "kernel_ms_covers": ("rank-code pre-pass + pttr_kernel (both launches of one hb_predict call; "
                              "their split is in the ncu launch list under profiles/)")
         if info.get("rank_prepass") and kname != "small_batch_kernel" else kname,
         "algorithmic_bytes_per_row": per_row,
