@@ -710,6 +710,24 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
         const int want_sector = env_int("HB_TT_SECTOR", -1);
         const bool big = (double)m->n_trees_pad * (double)L.stride > 0.75 * (double)l2_bytes;
+        if (!(want_sector == 1 || (want_sector == -1 && big)) && env_int("HB_TT_PAIR", 0) == 1) {
+          // pair-aligned BFS records: node array at +24 so every sibling pair
+          // (2m+1, 2m+2) is one aligned 16-B word (lookahead walk, hb_tt.cu)
+          const size_t nbytes = (size_t)8 * L.nslots, lbytes = (size_t)4 * e->leaf_width * L.nslots;
+          const size_t stride2 = round16(24 + nbytes + lbytes);
+          std::vector<uint8_t> t2((size_t)m->n_trees_pad * stride2, 0);
+          for (int lt = 0; lt < m->n_trees_pad; ++lt) {
+            const uint8_t *src = L.trees.data() + (size_t)lt * L.stride;
+            uint8_t *dst = t2.data() + (size_t)lt * stride2;
+            std::memcpy(dst, src, 16);
+            std::memcpy(dst + 24, src + 16, nbytes + lbytes);
+          }
+          st = upload(t2, reinterpret_cast<uint8_t **>(&m->d_ttw), &m->device_bytes);
+          if (st != HB_OK) return st;
+          m->ttw_stride = stride2;
+          m->ttw_nslots = L.nslots;
+          m->tt_pair = 1;
+        }
         if ((want_sector == 1 || (want_sector == -1 && big)) && fmap.used.size() <= 32768) {
           HostLayout S;
           st = build_tt_sector(e, t0, t1, m->n_trees_pad, &S, &fmap, env_int("HB_TT_SECTOR_TOP", 4));

@@ -37,6 +37,9 @@ struct TtParams {
   int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
   int top_prefetch;       // tt_wide_kernel: L1 prefetch of the next tree group's top levels
   int cursor;             // tt_wide_kernel: per-lane tree cursors instead of warp-synchronous groups
+  int node_off;           // byte offset of the node array in a record (16 BFS; 24 pair-aligned BFS)
+  int lookahead;          // tt_wide_kernel over pair-aligned BFS records: load both children
+                          // of the current node (one 16-B load) while its X value is read
 };
 
 // node array offset inside a record: 16 B (BFS layout), 32 B (sector layout:
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   uint64_t *hred = reinterpret_cast<uint64_t *>(red + (size_t)nwarps * R * NACC);  // [nwarps][R]
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   const int slots = nwarps * L;
+  const int noff = SEC ? node_off<true>() : p.node_off;
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row0 = (int64_t)tile * R;
     // coalesced X tile load: consecutive threads -> consecutive features of a row
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
     uint64_t h = 0;
     // leaf of tree t reached (record rc, slot leaf): add its value / emit its id
     auto finish = [&](int t, const uint8_t *rc, uint32_t leaf) {
-      const float *lv = reinterpret_cast<const float *>(rc + node_off<SEC>() + (size_t)8 * p.nslots);
+      const float *lv = reinterpret_cast<const float *>(rc + noff + (size_t)8 * p.nslots);
       if (p.w == 1) {
         const float v = __ldg(lv + leaf);
         if (NACC == 1) {
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
             act = true;
             bool dn = true;
             uint32_t i = ix[g];
-            wide_step<LE, R, SEC>(reinterpret_cast<const uint2 *>(rc[g] + node_off<SEC>()), i, xs, r, dn);
+            wide_step<LE, R, SEC>(reinterpret_cast<const uint2 *>(rc[g] + noff), i, xs, r, dn);
             if (dn) {
               finish(t[g], rc[g], i);
               t[g] += tstep;
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         const int t = base + sub + g * slots;
         valid[g] = t < p.n_trees_pad;               // uniform across the warp
         rec[g] = p.trees + (size_t)(valid[g] ? t : base + sub) * p.stride;
-        nd[g] = reinterpret_cast<const uint2 *>(rec[g] + node_off<SEC>());
+        nd[g] = reinterpret_cast<const uint2 *>(rec[g] + noff);
         idx[g] = 0;
       }
       if (p.top_prefetch && r < 2) {
@@ -356,16 +360,47 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         for (int g = 0; g < G; ++g) {
           const int t = base + G * slots + sub + g * slots;
           if (t < p.n_trees_pad) {
-            const uint8_t *q = p.trees + (size_t)t * p.stride + node_off<SEC>() + 128 * r;
+            const uint8_t *q = p.trees + (size_t)t * p.stride + noff + 128 * r;
             asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
           }
         }
       }
-      for (int l = 0; l < p.depth; ++l) {
-        bool done = true;
+      if (!SEC && p.lookahead) {
+        // pair-aligned BFS records: siblings (R-1, R) share one 16-B word, so
+        // the next record is fetched (both candidates) as soon as the current
+        // one is known, in parallel with the X read and the compare. A leaf's
+        // self loop reads the aligned pair holding it ((R-1) | 1 = R).
+        uint2 dc[G];
 #pragma unroll
-        for (int g = 0; g < G; ++g) wide_step<LE, R, SEC>(nd[g], idx[g], xs, r, done);
-        if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
+        for (int g = 0; g < G; ++g) dc[g] = __ldg(nd[g]);
+        for (int l = 0; l < p.depth; ++l) {
+          bool done = true;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t rr = dc[g].x >> 16;
+            // a leaf at slot 0 (single-leaf or padding tree) has no pair below
+            // it: load any valid pair, the self loop keeps the record
+            const uint32_t pb = rr == 0 ? 1u : ((rr - 1u) | 1u);
+            const uint4 c = __ldg(reinterpret_cast<const uint4 *>(nd[g] + pb));
+            const int f = (int)(dc[g].x & 0xFFFFu);
+            const float x = xs[f * R + (r ^ xw_swz<R>(f))];
+            const float t = __uint_as_float(dc[g].y);
+            const bool pr = LE ? (x <= t) : (x < t);
+            const uint32_t nx = rr - (pr ? 1u : 0u);
+            const bool same = nx == idx[g];      // leaf: self loop, record unchanged
+            done = done && same;
+            idx[g] = nx;
+            if (!same) dc[g] = nx == pb ? make_uint2(c.x, c.y) : make_uint2(c.z, c.w);
+          }
+          if (__all_sync(0xFFFFFFFFu, done)) break;
+        }
+      } else {
+        for (int l = 0; l < p.depth; ++l) {
+          bool done = true;
+#pragma unroll
+          for (int g = 0; g < G; ++g) wide_step<LE, R, SEC>(nd[g], idx[g], xs, r, done);
+          if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
+        }
       }
 #pragma unroll
       for (int g = 0; g < G; ++g)
@@ -465,8 +500,11 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.fmap = m.d_fmap;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   p.depth = m.depth;
-  p.trees = static_cast<const uint8_t *>(sec ? m.d_ttw : m.d_trees);
-  p.stride = (uint32_t)(sec ? m.ttw_stride : m.stride);
+  const bool pair = wide && !sec && m.tt_pair;
+  p.trees = static_cast<const uint8_t *>(sec || pair ? m.d_ttw : m.d_trees);
+  p.stride = (uint32_t)(sec || pair ? m.ttw_stride : m.stride);
+  p.node_off = pair ? 24 : 16;
+  p.lookahead = pair ? 1 : 0;
   p.n_trees_pad = m.n_trees_pad;
   p.n_trees = m.n_trees;
   p.tree_begin = m.tree_begin;

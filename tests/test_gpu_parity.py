@@ -180,7 +180,7 @@ def test_ptt_special_thresholds(cmp, rank, monkeypatch):
 
 @pytest.mark.parametrize("kind", ["reg", "binary", "multiclass", "rf", "k7", "k12"])
 @pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("blocks", ["1", "0", "sector", "cursor", "sector-cursor"])
+@pytest.mark.parametrize("blocks", ["1", "0", "sector", "cursor", "sector-cursor", "pair"])
 def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
     """The wide-row TT kernels (R rows per CTA, lanes = tree slot x row, nodes
     through L1/L2) forced on ordinary inputs: ttb_kernel (2-level node blocks,
@@ -190,6 +190,7 @@ def test_tt_wide_kernel_parity(kind, cmp, blocks, monkeypatch):
     monkeypatch.setenv("HB_TT_BLOCK", "1" if blocks == "1" else "0")
     monkeypatch.setenv("HB_TT_SECTOR", "1" if blocks.startswith("sector") else "0")
     monkeypatch.setenv("HB_TT_CURSOR", "1" if blocks.endswith("cursor") else "0")
+    monkeypatch.setenv("HB_TT_PAIR", "1" if blocks == "pair" else "0")
     monkeypatch.setenv("HB_TT_TOP_PF", "1" if kind in ("reg", "k7") else "0")
     seed = zlib.crc32(f"wide{kind}{cmp}".encode()) & 0xFFFF
     e = _forest(kind, 45, 9, 37, seed, FAMILIES[seed % 3], cmp)
@@ -222,7 +223,8 @@ def test_tt_sector_layout_tree_shapes(cmp, monkeypatch):
     leaves = []
     # sector layout with 0/1/4/6 BFS top levels, BFS layout; warp-synchronous
     # groups or per-lane tree cursors
-    for sec in ("1:0:0", "1:1:0", "1:4:1", "1:6:0", "0:0:0", "0:0:1"):
+    for sec in ("1:0:0", "1:1:0", "1:4:1", "1:6:0", "0:0:0", "0:0:1", "0:0:0:pair"):
+        monkeypatch.setenv("HB_TT_PAIR", "1" if sec.endswith("pair") else "0")
         monkeypatch.setenv("HB_TT_SECTOR", sec.split(":")[0])
         monkeypatch.setenv("HB_TT_SECTOR_TOP", sec.split(":")[1])
         monkeypatch.setenv("HB_TT_CURSOR", sec.split(":")[2])
