@@ -917,3 +917,24 @@ def test_rank_prepass_cluster(cw, cmp, monkeypatch):
         for n, ldx in ((1, F), (1023, F + 1), (5000, F), (40000, F)):
             Xd, Xh = X_pair(30 + n, n, F, ldx=ldx, special_q24=SPECIAL_Q24)
             check_all(e, m, Xd, Xh, kinds=("predict", "raw", "leaf_hash"))
+
+
+def test_auto_layout_per_config():
+    """AUTO picks, for each BASELINE config, the layout DESIGN.md §4 measured
+    fastest: C1 any strategy (small-batch path per call), C2 rank-coded PTT
+    with 16-bit cells and the pre-pass, C3 and C4 rank-coded PTT with 32-bit
+    cells and the pre-pass, C4' in-kernel codes with 16-bit cells, C5's 1/8
+    tree shard TT over BFS records, all 10k C5 trees TT over sector-paired
+    records (they exceed L2)."""
+    want = {"C2": ("ptt", 16, 1), "C3": ("ptt", 32, 1), "C4": ("ptt", 32, 1), "C4p": ("ptt", 16, 0)}
+    for name, (strat, cw, pre) in want.items():
+        _, e = synth.make_config(name)
+        info = hb.Model(e, device=0).info
+        got = (info["strategy_name"], info["code_cell_bits"], info["rank_prepass"])
+        assert got == (strat, cw, pre), (name, got)
+        assert info["node_record_bytes"] == 4
+    _, e = synth.make_config("C5")
+    shard = hb.Model(e, tree_range=(0, 1250), device=0).info
+    assert shard["strategy_name"] == "tt" and shard["kernel_name"] == "tt_wide_kernel" and shard["tt_sector"] == 0
+    full = hb.Model(e, device=0).info
+    assert full["kernel_name"] == "tt_wide_kernel" and full["tt_sector"] == 1
