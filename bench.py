@@ -173,6 +173,18 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def launches_per_call(info, kind, small):
+    """Kernels one hb_predict call launches: rank-code pre-pass models two
+    (pre-pass + scorer) except on the small-batch path; a TT model walked in
+    L2-resident tree chunks one per chunk, plus the finalize for outputs that
+    need the post transform."""
+    chunk = info.get("tt_chunk_trees", 0)
+    if chunk and not small:
+        pad = (info["n_trees"] + 3) // 4 * 4
+        return -(-pad // chunk) + (1 if kind in ("predict", "proba", "margin") else 0)
+    return 2 if info.get("rank_prepass") and not small else 1
+
+
 def workload_config(cfg, e, rows, args, mode="rows"):
     par = (f"rows sharded over {args.gpus} GPU(s), no collective" if mode == "rows" else
            f"trees sharded over {args.gpus} GPU(s), one NCCL reduce of fp32 partials + finalize")
@@ -221,10 +233,8 @@ def run_ours(args):
 
         def step():
             m.run(X, kind, out=out, stream=stream)
-        # rank-code pre-pass models launch rank_code_kernel + pttr_kernel per
-        # call, except on the small-batch path (one kernel)
         small = n <= int(os.environ.get("HB_SMALL_BATCH", "4096"))
-        launches_per_step = 2 if m.info.get("rank_prepass") and not small else 1
+        launches_per_step = launches_per_call(m.info, kind, small)
     else:
         # trees sharded, all rows on every rank; one NCCL reduce of fp32
         # partials to rank 0, which finalizes (strong scaling)
@@ -242,7 +252,7 @@ def run_ours(args):
                 reduce_partials(raw, dst=0)
             if rank == 0:
                 m.finalize(raw, kind, out=out, stream=stream)
-        launches_per_step = 2
+        launches_per_step = launches_per_call(m.info, "raw", False) + 1
     info = m.info
 
     # request/response batch sizes (small-batch kernel) are launch-bound from
@@ -329,7 +339,8 @@ def run_ours(args):
             peaks = {"error": str(ex)}
     smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
     layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "") + \
-        ("-pre" if info.get("rank_prepass") else "") + ("-sector" if info.get("tt_sector") else "")
+        ("-pre" if info.get("rank_prepass") else "") + ("-sector" if info.get("tt_sector") else "") + \
+        ("-chunk" if info.get("tt_chunk_trees") else "")
     prof = load_profile(args.config, layout)
     kname = info["kernel_name"]
     if n <= int(os.environ.get("HB_SMALL_BATCH", "4096")):
@@ -365,7 +376,9 @@ def run_ours(args):
         "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
         "kernel_ms_covers": ("rank-code pre-pass + pttr_kernel (both launches of one hb_predict call; "
                              "their split is in the ncu launch list under profiles/)")
-        if info.get("rank_prepass") and kname != "small_batch_kernel" else kname,
+        if info.get("rank_prepass") and kname != "small_batch_kernel" else
+        (f"{kname} over L2-resident chunks of {info['tt_chunk_trees']} trees (one launch per chunk) + finalize"
+         if info.get("tt_chunk_trees") else kname),
         "algorithmic_bytes_per_row": per_row,
         "peak_source": ("measured L2 read microbenchmark (tools/peaks.cu), this run" if l2_wide else
                         "measured LDS.128 microbenchmark (tools/peaks.cu), this run")

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 2   /* 2: hb_model_info.tt_sector appended */
+#define HB_ABI_VERSION 3   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended */
 
 typedef enum {
   HB_OK = 0,
@@ -158,6 +158,8 @@ typedef struct {
                                    computes the X codes into stream-ordered scratch */
   int32_t tt_sector;            /* wide-row TT: 1 if tt_wide_kernel walks sector-paired
                                    records (a node and both children in one 32-B sector) */
+  int32_t tt_chunk_trees;       /* wide-row TT: trees per L2-resident chunk when the model is
+                                   walked in several launches (0: one launch) */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the

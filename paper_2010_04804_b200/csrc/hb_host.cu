@@ -700,12 +700,12 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         m->tt_g = env_int("HB_TT_G", 4);
         m->tt_top_prefetch = env_int("HB_TT_TOP_PF", 0);
         m->tt_cursor = env_int("HB_TT_CURSOR", 0);
-        // sector-paired records (one L2 sector per two levels of a walk):
-        // AUTO when the BFS records exceed 3/4 of L2, i.e. deep levels come
-        // from HBM (C5, 10k trees on one GPU: 16.96 -> 15.57 ms); an
-        // L2-resident model keeps the BFS records (C5 1/8 shard: 1.83 ms BFS
-        // vs 2.03-2.14 ms sector: siblings 4 slots apart touch more sectors
-        // per tile). HB_TT_SECTOR=0/1 forces.
+        // sector-paired records (one L2 sector per two levels of a walk,
+        // HB_TT_SECTOR=1): faster than one BFS launch when the records exceed
+        // L2 (C5, 10k trees on one GPU: 16.96 -> 15.57 ms), slower on an
+        // L2-resident model (C5 1/8 shard: 1.83 vs 2.03-2.14 ms: siblings 4
+        // slots apart touch more sectors per tile); L2-resident tree chunks
+        // (below) beat both, so AUTO uses those.
         int l2_bytes = 0;
         cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
         const int want_sector = env_int("HB_TT_SECTOR", -1);
@@ -728,7 +728,22 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
           m->ttw_nslots = L.nslots;
           m->tt_pair = 1;
         }
-        if ((want_sector == 1 || (want_sector == -1 && big)) && fmap.used.size() <= 32768) {
+        // models larger than L2: walk them in tree chunks whose records stay
+        // L2-resident (HB_TT_CHUNK: -1 auto, N trees, 0 off). Auto size: the
+        // chunk's actual node + leaf bytes (not the padded stride) = 0.4 x L2
+        // — C5, 10k trees on one GPU (measured, 100K rows): 1000 / 1500 /
+        // 2500 / 3336 / 5000 trees per chunk = 15.5 / 14.7 / 13.7 / 15.1 /
+        // 17.2 ms; sector-paired records 15.7 ms, one BFS launch 17.2 ms
+        const int want_chunk = env_int("HB_TT_CHUNK", -1);
+        if (want_chunk > 0 || (want_chunk == -1 && big && want_sector != 1)) {
+          double bytes = 0;
+          for (int t = t0; t < t1; ++t)
+            bytes += (double)(e->node_offset[t + 1] - e->node_offset[t]) * (8.0 + 4.0 * e->leaf_width);
+          const double per_tree = std::max(1.0, bytes / std::max(1, t1 - t0));
+          const int autoc = (int)(0.4 * (double)l2_bytes / per_tree) & ~(kTreeGroup - 1);
+          m->tt_chunk = std::max(kTreeGroup, want_chunk > 0 ? want_chunk : autoc);
+        }
+        if (m->tt_chunk == 0 && want_sector == 1 && fmap.used.size() <= 32768) {
           HostLayout S;
           st = build_tt_sector(e, t0, t1, m->n_trees_pad, &S, &fmap, env_int("HB_TT_SECTOR_TOP", 4));
           if (st == HB_OK) {
@@ -1074,6 +1089,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->code_cell_bits = m.ptt_rank ? m.rank_cw : 0;
   info->rank_prepass = m.rank_pre;
   info->tt_sector = m.tt_sector;
+  info->tt_chunk_trees = m.tt_chunk;
   return HB_OK;
 }
 

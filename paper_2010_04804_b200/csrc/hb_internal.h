@@ -117,6 +117,7 @@ struct Model {
   int tt_sector = 0;
   int tt_cursor = 0;         // tt_wide_kernel: per-lane tree cursors (HB_TT_CURSOR)
   int tt_pair = 0;           // tt_wide_kernel: pair-aligned BFS records in d_ttw + child lookahead
+  int tt_chunk = 0;          // tt_wide_kernel: trees per L2-resident chunk (0: one launch)
   int tt_top_prefetch = 0;   // tt_wide_kernel: prefetch.global.L1 of the next tree group's top lines
   void *d_ttw = nullptr;
   int32_t *d_ttw_leafmap = nullptr;

@@ -40,6 +40,10 @@ struct TtParams {
   int node_off;           // byte offset of the node array in a record (16 BFS; 24 pair-aligned BFS)
   int lookahead;          // tt_wide_kernel over pair-aligned BFS records: load both children
                           // of the current node (one 16-B load) while its X value is read
+  // tt_wide_kernel over one tree chunk of a model larger than L2 (launch_tt):
+  int accumulate;         // RAW / LEAF_HASH outputs are added to, not written
+  int leaf_stride;        // LEAF output row stride (the model's tree count)
+  int tree_off;           // first model-local tree of this chunk (LEAF column)
 };
 
 // node array offset inside a record: 16 B (BFS layout), 32 B (sector layout:
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       if (lm && t < p.n_trees) {
         const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
         if (lm == 1) {
-          if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+          if (row < p.n) static_cast<int32_t *>(p.out)[row * p.leaf_stride + p.tree_off + t] = id;
         } else {
           h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
         }
@@ -432,8 +436,16 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       }
       const int64_t orow = row0 + lane;
       if (orow < p.n) {
-        if (lm == 2) static_cast<uint64_t *>(p.out)[orow] = ht;
-        else if (lm == 0) dev::write_row<NACC>(p.kind, tot, p.K, p.task, p.post, p.scale, p.base, orow, p.out);
+        if (lm == 2) {
+          uint64_t *o = static_cast<uint64_t *>(p.out) + orow;
+          *o = p.accumulate ? *o + ht : ht;
+        } else if (lm == 0 && p.accumulate) {      // RAW partial of a later tree chunk
+#pragma unroll
+          for (int k = 0; k < NACC; ++k)
+            if (k < p.K) static_cast<float *>(p.out)[orow * p.K + k] += tot[k];
+        } else if (lm == 0) {
+          dev::write_row<NACC>(p.kind, tot, p.K, p.task, p.post, p.scale, p.base, orow, p.out);
+        }
       }
     }
     __syncthreads();
@@ -526,6 +538,9 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.x_prefetch = m.cfg.prefetch;
   p.top_prefetch = m.tt_top_prefetch;
   p.cursor = m.tt_cursor;
+  p.accumulate = 0;
+  p.leaf_stride = m.n_trees;
+  p.tree_off = 0;
   const int64_t rows_per_tile = wide ? (int64_t)m.cfg.wide_rows : (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
@@ -535,9 +550,47 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
                                        m.cfg.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tt)");
   const int threads = wide ? 32 * m.cfg.nw : 32 * (m.cfg.nw + 1);
-  fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "tt_kernel launch");
+  if (!(wide && !sec && !pair && m.tt_chunk > 0 && m.n_trees_pad > m.tt_chunk)) {
+    fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "tt_kernel launch");
+    return HB_OK;
+  }
+  // model larger than L2: walk it in L2-resident tree chunks (every chunk
+  // re-streams X from HBM, sequentially, instead of fetching deep node
+  // records from HBM at random); RAW / LEAF_HASH partials accumulate in the
+  // output, PREDICT / PROBA / MARGIN go through a raw scratch + finalize
+  const bool fin = a.kind == HB_OUT_PREDICT || a.kind == HB_OUT_PROBA || a.kind == HB_OUT_MARGIN;
+  float *raw = nullptr;
+  if (fin) {
+    e = cudaMallocAsync(reinterpret_cast<void **>(&raw), (size_t)a.n * m.n_outputs * sizeof(float), a.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(tt chunk partials)");
+  }
+  for (int t0 = 0; t0 < m.n_trees_pad; t0 += m.tt_chunk) {
+    TtParams pc = p;
+    pc.trees = p.trees + (size_t)t0 * p.stride;
+    pc.n_trees_pad = std::min(m.tt_chunk, m.n_trees_pad - t0);
+    pc.n_trees = std::max(0, std::min(m.tt_chunk, m.n_trees - t0));
+    pc.tree_begin = m.tree_begin + t0;
+    pc.leafmap = p.leafmap + (size_t)t0 * p.nslots;
+    pc.tree_off = t0;
+    pc.kind = fin ? HB_OUT_RAW : a.kind;
+    pc.out = fin ? static_cast<void *>(raw) : a.out;
+    pc.accumulate = t0 > 0 && pc.kind != HB_OUT_LEAF;
+    fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(pc);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      if (raw) cudaFreeAsync(raw, a.stream);
+      return cuda_fail(e, "tt_wide_kernel launch (tree chunk)");
+    }
+  }
+  if (fin) {
+    RunArgs f = a;
+    f.raw_in = raw;
+    const hb_status st = launch_finalize(m, f);
+    cudaFreeAsync(raw, a.stream);
+    if (st != HB_OK) return st;
+  }
   return HB_OK;
 }
 

@@ -52,7 +52,7 @@ class _Info(C.Structure):
                 ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32),
                 ("kernel", C.c_int32), ("rows_per_cta", C.c_int32),
                 ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32),
-                ("tt_sector", C.c_int32)]
+                ("tt_sector", C.c_int32), ("tt_chunk_trees", C.c_int32)]
 
 
 def _load():

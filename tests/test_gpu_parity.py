@@ -642,13 +642,22 @@ def test_c5_shard_sampled():
     torch.cuda.empty_cache()
 
 
-def test_c5_full_model_sector_records_sampled():
-    """C5 with all 10k trees on one GPU: the BFS records exceed 3/4 of L2, so
-    AUTO builds sector-paired records (hb_model_info.tt_sector); sampled rows
-    of the proba / leaf hash against the oracle, in bench.py's launch shape."""
+@pytest.mark.parametrize("layout", ["auto", "sector"])
+def test_c5_full_model_sampled(layout, monkeypatch):
+    """C5 with all 10k trees on one GPU: the BFS records exceed L2, so AUTO
+    walks the model in L2-resident tree chunks (hb_model_info.tt_chunk_trees,
+    partials accumulated, finalize at the end); forced sector-paired records
+    are the alternative. Sampled rows of the proba / leaf hash against the
+    oracle, in bench.py's launch shape."""
+    if layout == "sector":
+        monkeypatch.setenv("HB_TT_SECTOR", "1")
     c, e = synth.make_config("C5")
     m = hb.Model(e, device=0)
-    assert m.info["strategy_name"] == "tt" and m.info["tt_sector"] == 1
+    assert m.info["strategy_name"] == "tt"
+    if layout == "sector":
+        assert m.info["tt_sector"] == 1 and m.info["tt_chunk_trees"] == 0
+    else:
+        assert m.info["tt_sector"] == 0 and 0 < m.info["tt_chunk_trees"] < 10_000
     n = 20_000
     X = synth.dev.gen_X_device(c.seed_x, n, c.n_features)
     proba = m.predict_proba(X).cpu().numpy().astype(np.float64)
@@ -924,8 +933,8 @@ def test_auto_layout_per_config():
     fastest: C1 any strategy (small-batch path per call), C2 rank-coded PTT
     with 16-bit cells and the pre-pass, C3 and C4 rank-coded PTT with 32-bit
     cells and the pre-pass, C4' in-kernel codes with 16-bit cells, C5's 1/8
-    tree shard TT over BFS records, all 10k C5 trees TT over sector-paired
-    records (they exceed L2)."""
+    tree shard TT over BFS records in one launch, all 10k C5 trees TT in
+    L2-resident tree chunks (their records exceed L2)."""
     want = {"C2": ("ptt", 16, 1), "C3": ("ptt", 32, 1), "C4": ("ptt", 32, 1), "C4p": ("ptt", 16, 0)}
     for name, (strat, cw, pre) in want.items():
         _, e = synth.make_config(name)
@@ -936,5 +945,24 @@ def test_auto_layout_per_config():
     _, e = synth.make_config("C5")
     shard = hb.Model(e, tree_range=(0, 1250), device=0).info
     assert shard["strategy_name"] == "tt" and shard["kernel_name"] == "tt_wide_kernel" and shard["tt_sector"] == 0
+    assert shard["tt_chunk_trees"] == 0
     full = hb.Model(e, device=0).info
-    assert full["kernel_name"] == "tt_wide_kernel" and full["tt_sector"] == 1
+    assert full["kernel_name"] == "tt_wide_kernel" and full["tt_chunk_trees"] > 0
+
+
+@pytest.mark.parametrize("chunk", ["8", "20"])
+def test_tt_wide_tree_chunks(chunk, monkeypatch):
+    """tt_wide_kernel over L2-sized tree chunks (launch_tt): RAW and LEAF_HASH
+    partials accumulate across chunk launches, PREDICT / PROBA / MARGIN go
+    through a raw scratch + finalize, LEAF writes each chunk's columns; chunk
+    boundaries inside the real trees and inside the padding; MEAN / softmax
+    model and a binary sigmoid one."""
+    monkeypatch.setenv("HB_TT_WIDE", "1")
+    monkeypatch.setenv("HB_TT_SECTOR", "0")
+    monkeypatch.setenv("HB_TT_CHUNK", chunk)
+    for kind, seed in (("binary", 3), ("rf", 4), ("k7", 5)):
+        e = _forest(kind, 45, 9, 37, seed, "mixed", seed % 2)
+        m = hb.Model(e, strategy="tt", device=0)
+        assert m.info["kernel_name"] == "tt_wide_kernel"
+        Xd, Xh = X_pair(seed, 1000 + seed, 37, special_q24=SPECIAL_Q24)
+        check_all(e, m, Xd, Xh)
