@@ -405,7 +405,9 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
 int sm_count(int device);
 
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
+  const bool top = m.rank_cw == 32 && env_int2("HB_PTTR_TOP", 0) == 1;
   PttrFn fn = m.rank_cw == 16 ? pttr_fn16(m.depth, m.cmp == HB_CMP_LE, m.nacc)
+              : top           ? pttr_fn32_top(m.depth, m.cmp == HB_CMP_LE, m.nacc)
                               : pttr_fn32(m.depth, m.cmp == HB_CMP_LE, m.nacc);
   if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
   PttrParams p;

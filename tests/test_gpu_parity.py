@@ -153,14 +153,16 @@ def test_strategy_parity(strat, D, kind, cmp, monkeypatch):
 def _set_layout(monkeypatch, rank):
     """PTT node layout by name: "0" fp32 nodes; "1" / "16" rank-coded with
     32- / 16-bit cells, codes in the scorer; "pre32" / "pre16" the same with
-    codes from the pre-pass launch."""
+    codes from the pre-pass launch; "top" / "pretop" 32-bit cells with the
+    LDS.128 top-of-tree load (HB_PTTR_TOP)."""
     monkeypatch.setenv("HB_PTT_RANK", "0" if rank == "0" else "1")
-    monkeypatch.setenv("HB_RANK_CW", "16" if rank.endswith("16") else ("32" if rank == "pre32" else "0"))
+    monkeypatch.setenv("HB_RANK_CW", "16" if rank.endswith("16") else ("32" if rank in ("pre32", "top", "pretop") else "0"))
     monkeypatch.setenv("HB_RANK_PRE", "1" if rank.startswith("pre") else "0")
+    monkeypatch.setenv("HB_PTTR_TOP", "1" if rank.endswith("top") else "0")
 
 
 @pytest.mark.parametrize("cmp", [0, 1])
-@pytest.mark.parametrize("rank", ["1", "0", "16", "pre32", "pre16"])
+@pytest.mark.parametrize("rank", ["1", "0", "16", "pre32", "pre16", "top", "pretop"])
 def test_ptt_special_thresholds(cmp, rank, monkeypatch):
     """Thresholds at +-Inf and -0/+0 (mixed on one feature) against X holding
     NaN, +-Inf, +-0 and exact ties: the rank code must reproduce every fp32
@@ -822,7 +824,7 @@ def test_rank_prepass_bucket_edges(cmp, cw, staged, monkeypatch):
 
 
 @pytest.mark.parametrize("D", [1, 2, 9, 10])
-@pytest.mark.parametrize("rank", ["0", "1", "16", "pre32", "pre16"])
+@pytest.mark.parametrize("rank", ["0", "1", "16", "pre32", "pre16", "top", "pretop"])
 def test_ptt_depth_range(D, rank, monkeypatch):
     _set_layout(monkeypatch, rank)
     e = synth.gen_forest(13, D, 10, seed=D, family="skinny", post=synth.POST_SIGMOID,
@@ -966,3 +968,18 @@ def test_tt_wide_tree_chunks(chunk, monkeypatch):
         assert m.info["kernel_name"] == "tt_wide_kernel"
         Xd, Xh = X_pair(seed, 1000 + seed, 37, special_q24=SPECIAL_Q24)
         check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("kind", ["reg", "multiclass", "k7", "rf"])
+@pytest.mark.parametrize("rank", ["top", "pretop"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_pttr_top_load_kinds(kind, rank, cmp, monkeypatch):
+    """The LDS.128 top-of-tree variant (HB_PTTR_TOP) over every accumulator
+    shape (NACC 1 / class-ordered groups / vector leaves) and both predicates:
+    leaf ids and hashes bit-exact, scores within tolerance (check_all)."""
+    _set_layout(monkeypatch, rank)
+    e = _forest(kind, 37, 8, 11, 41, "mixed", cmp)
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["node_record_bytes"] == 4
+    Xd, Xh = X_pair(9, 2500, 11, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh)
