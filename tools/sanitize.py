@@ -42,10 +42,17 @@ cases = [
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_CLUSTER": "1"}, "ptt"),
     ("tt-blocks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
      {"HB_TT_WIDE": "1", "HB_TT_BLOCK": "1"}, "tt"),
+    ("ptt-rank-top-wrap", synth.gen_forest(300, 8, 12, seed=4),
+     {"HB_PTT_RANK": "1", "HB_RANK_CW": "32", "HB_PTTR_TOP": "1", "HB_CH": "8"}, "ptt"),
+    ("ptt-rank-pre-top", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_PTTR_TOP": "1"}, "ptt"),
     ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
     ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
 ]
+only = set(sys.argv[1:])   # optional case names; default: every case
 for name, e, env, strat in cases:
+    if only and name not in only:
+        continue
     os.environ.update(env)
     for n, small in ((3000, "0"), (40, "4096")):
         os.environ["HB_SMALL_BATCH"] = small
