@@ -414,6 +414,45 @@ def run_ours(args):
                "d2h_bytes_per_step": int(oh.numel() * oh.element_size()), "steps": args.e2e_steps,
                "api": "hb_predict_host (chunked H2D / score / D2H on two streams)"}
         del Xh, oh
+    elif not args.no_e2e and mode == "trees":
+        # every rank streams all rows from pinned host memory through
+        # hb_predict_host and gets its shard's raw partials back; the partials
+        # go to the device for the NCCL reduce, rank 0 finalizes and reads the
+        # result back (the partial round trip is n*K*4 B each way)
+        Xh = torch.empty((n, cfg.n_features), dtype=torch.float32).pin_memory()
+        Xh.copy_(X)
+        del X
+        rawh = torch.empty((n, e.n_outputs), dtype=torch.float32).pin_memory()
+        oh = torch.empty(shape, dtype=getattr(torch, dt)).pin_memory()
+
+        def e2e_step():
+            m.predict_host(Xh, "raw", out=rawh)
+            raw.copy_(rawh)
+            if dist:
+                reduce_partials(raw, dst=0)
+            if rank == 0:
+                m.finalize(raw, kind, out=out, stream=stream)
+                stream.synchronize()
+                oh.copy_(out)
+        e2e_step()  # warm (allocates staging)
+        if dist:
+            dist.barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            w0 = time.perf_counter()
+            e2e_step()
+            ts.append(time.perf_counter() - w0)
+        t_e2e = float(np.mean(ts))
+        if dist:
+            t_e2e = max_over_ranks(t_e2e, device=raw.device)
+        part = int(rawh.numel() * 4)
+        e2e = {"value": rows_all / t_e2e, "unit": "rows/s", "ms_per_step": t_e2e * 1e3,
+               "h2d_bytes_per_step": int(n * cfg.n_features * 4) + part,
+               "d2h_bytes_per_step": part + int(oh.numel() * oh.element_size()),
+               "steps": args.e2e_steps,
+               "api": "hb_predict_host(raw) per tree shard -> NCCL reduce of the partials -> "
+                      "hb_finalize on rank 0 -> D2H"}
+        del Xh, oh, rawh
 
     cpu = None
     if rank == 0 and not args.no_cpu:
