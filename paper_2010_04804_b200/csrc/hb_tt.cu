@@ -209,21 +209,20 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // parallelism) and the walk stops early once every lane of the warp sits on a
 // leaf (the self-loop makes further iterations no-ops). Per-row sums
 // are combined with warp shuffles and one SMEM pass in a fixed order.
-// X tile swizzle: row rr of feature f sits at f*R + (rr ^ h(f)), h(f) =
-// (f >> log2(32/R)) & (R-1), so a warp storing 32 consecutive features of one
-// row hits 32 distinct banks (the plain f*R + rr layout is R-way conflicted).
-template <int R>
-__device__ __forceinline__ int xw_swz(int f) {
-  constexpr int S = R == 32 ? 0 : (R == 16 ? 1 : 2);
-  return (f >> S) & (R - 1);
-}
+// X tile layout: plain xs[f*R + r], so the R lanes of one tree slot (distinct
+// rows) always read distinct banks whatever features their walks test; only
+// lanes of different tree slots on the same row can meet (<= 32/R-way). The
+// fill gives the 32/R row groups of a warp different 4-feature chunks and
+// rotates their store order so a warp's 32 stores hit 32 distinct banks.
+// (The previous XOR swizzle made the tile fill's stores conflict-free only for
+// scalar stores of consecutive features and cost 2.4 wavefronts per read.)
 
 template <bool LE, int R, bool SEC>
 __device__ __forceinline__ void wide_step(const uint2 *n, uint32_t &i, const float *xs, int r,
                                           bool &done) {
   const uint2 d = __ldg(n + i);
   const int f = (int)(d.x & (SEC ? 0x7FFFu : 0xFFFFu));
-  const float x = xs[f * R + (r ^ xw_swz<R>(f))];
+  const float x = xs[f * R + r];
   const float t = __uint_as_float(d.y);
   const bool pr = LE ? (x <= t) : (x < t);
   // left child = N_R - 1 (BFS; sector roots) or N_R - 4 (sector layout, flag bit 15)
@@ -248,25 +247,40 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   const int noff = SEC ? node_off<true>() : p.node_off;
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row0 = (int64_t)tile * R;
-    // coalesced X tile load: consecutive threads -> consecutive features of a row
-    if (!p.fmap && p.vec4 && (p.F & 3) == 0) {
-      const int F4 = p.F >> 2;
-      for (int idx = threadIdx.x; idx < R * F4; idx += blockDim.x) {
-        const int rr = idx / F4, f = 4 * (idx - rr * F4);
+    // X tile load: lane = (row group sub, row rr); each lane loads one
+    // 4-feature chunk of its row (16 B, float4 when aligned) and stores it
+    // feature-major, the store order rotated by sub (bank = chunk position)
+    {
+      constexpr int SUBS = 32 / R;
+      const int F4 = (p.F + 3) >> 2;
+      const int nblk = (F4 + SUBS - 1) / SUBS;
+      const bool v4 = !p.fmap && p.vec4 && (p.F & 3) == 0;
+      for (int idx = threadIdx.x; idx < nblk * 32; idx += blockDim.x) {
+        const int q = idx & 31, rr = q % R, sub = q / R;
+        const int c = (idx >> 5) * SUBS + sub;
+        if (c >= F4) continue;
+        const int f = 4 * c;
         const int64_t gr = row0 + rr;
-        const float4 v = gr < p.n ? __ldg(reinterpret_cast<const float4 *>(p.X + gr * p.ldx + f))
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-        xs[(f + 0) * R + (rr ^ xw_swz<R>(f + 0))] = v.x;
-        xs[(f + 1) * R + (rr ^ xw_swz<R>(f + 1))] = v.y;
-        xs[(f + 2) * R + (rr ^ xw_swz<R>(f + 2))] = v.z;
-        xs[(f + 3) * R + (rr ^ xw_swz<R>(f + 3))] = v.w;
-      }
-    } else {
-      for (int idx = threadIdx.x; idx < R * p.F; idx += blockDim.x) {
-        const int rr = idx / p.F, f = idx - rr * p.F;
-        const int64_t gr = row0 + rr;
-        const int fo = p.fmap ? __ldg(p.fmap + f) : f;
-        xs[f * R + (rr ^ xw_swz<R>(f))] = gr < p.n ? __ldg(p.X + gr * p.ldx + fo) : 0.f;
+        float v0, v1, v2, v3;
+        if (v4) {
+          const float4 v = gr < p.n ? __ldg(reinterpret_cast<const float4 *>(p.X + gr * p.ldx + f))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+        } else {
+          float t[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int fj = f + j;
+            t[j] = (gr < p.n && fj < p.F) ? __ldg(p.X + gr * p.ldx + (p.fmap ? __ldg(p.fmap + fj) : fj)) : 0.f;
+          }
+          v0 = t[0]; v1 = t[1]; v2 = t[2]; v3 = t[3];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int jj = (j + sub) & 3;
+          const float val = jj == 0 ? v0 : (jj == 1 ? v1 : (jj == 2 ? v2 : v3));
+          if (f + jj < p.F) xs[(f + jj) * R + rr] = val;
+        }
       }
     }
     // warm L2 with the next tile's rows while this one is walked (the fill
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
             const uint32_t pb = rr == 0 ? 1u : ((rr - 1u) | 1u);
             const uint4 c = __ldg(reinterpret_cast<const uint4 *>(nd[g] + pb));
             const int f = (int)(dc[g].x & 0xFFFFu);
-            const float x = xs[f * R + (r ^ xw_swz<R>(f))];
+            const float x = xs[f * R + r];
             const float t = __uint_as_float(dc[g].y);
             const bool pr = LE ? (x <= t) : (x < t);
             const uint32_t nx = rr - (pr ? 1u : 0u);
