@@ -187,7 +187,7 @@ def launches_per_call(info, kind, small):
 
 def workload_config(cfg, e, rows, args, mode="rows"):
     par = (f"rows sharded over {args.gpus} GPU(s), no collective" if mode == "rows" else
-           f"trees sharded over {args.gpus} GPU(s), one NCCL reduce of fp32 partials + finalize")
+           f"trees sharded over {args.gpus} GPU(s), one NCCL reduce of fp64 partials + finalize")
     return {"workload": f"{cfg.name}: {cfg.note}", "rows_per_gpu": rows, "n_trees": e.n_trees,
             "max_depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": e.n_outputs,
             "family": cfg.family, "parallelism": par,
@@ -242,17 +242,17 @@ def run_ours(args):
                             e.leaf_width)
         m = hb.Model(e, strategy=args.strategy, device=local, tree_range=(t0, t1))
         X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, device=local)
-        raw = torch.empty((n, e.n_outputs), dtype=torch.float32, device=X.device)
+        raw = torch.empty((n, e.n_outputs), dtype=torch.float64, device=X.device)
         shape, dt = m.out_shape(n, kind)
         out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
 
         def step():
-            m.run(X, "raw", out=raw, stream=stream)
+            m.run(X, "raw64", out=raw, stream=stream)
             if dist:
                 reduce_partials(raw, dst=0)
             if rank == 0:
                 m.finalize(raw, kind, out=out, stream=stream)
-        launches_per_step = launches_per_call(m.info, "raw", False) + 1
+        launches_per_step = launches_per_call(m.info, "raw64", False) + 1
     info = m.info
 
     # request/response batch sizes (small-batch kernel) are launch-bound from
@@ -297,7 +297,7 @@ def run_ours(args):
             step()
             evs[i][1].record(stream)
         else:
-            m.run(X, "raw", out=raw, stream=stream)     # the scorer launch alone
+            m.run(X, "raw64", out=raw, stream=stream)   # the scorer launch(es) alone
             evs[i][1].record(stream)
             if dist:
                 reduce_partials(raw, dst=0)
@@ -422,11 +422,11 @@ def run_ours(args):
         Xh = torch.empty((n, cfg.n_features), dtype=torch.float32).pin_memory()
         Xh.copy_(X)
         del X
-        rawh = torch.empty((n, e.n_outputs), dtype=torch.float32).pin_memory()
+        rawh = torch.empty((n, e.n_outputs), dtype=torch.float64).pin_memory()
         oh = torch.empty(shape, dtype=getattr(torch, dt)).pin_memory()
 
         def e2e_step():
-            m.predict_host(Xh, "raw", out=rawh)
+            m.predict_host(Xh, "raw64", out=rawh)
             raw.copy_(rawh)
             if dist:
                 reduce_partials(raw, dst=0)
@@ -445,7 +445,7 @@ def run_ours(args):
         t_e2e = float(np.mean(ts))
         if dist:
             t_e2e = max_over_ranks(t_e2e, device=raw.device)
-        part = int(rawh.numel() * 4)
+        part = int(rawh.numel() * 8)
         e2e = {"value": rows_all / t_e2e, "unit": "rows/s", "ms_per_step": t_e2e * 1e3,
                "h2d_bytes_per_step": int(n * cfg.n_features * 4) + part,
                "d2h_bytes_per_step": part + int(oh.numel() * oh.element_size()),

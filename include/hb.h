@@ -16,12 +16,20 @@
  *  - Device pointers: X / out of the hb_predict* family are caller-owned
  *    DEVICE pointers on the model's device (checked with
  *    cudaPointerGetAttributes; host or foreign-device pointers give
- *    HB_E_INVALID). The only per-call device memory is the scratch of the
- *    rank-code pre-pass (models with hb_model_info.rank_prepass = 1): one
- *    stream-ordered allocation of ceil(n_rows / 32) * 128 * words bytes from
- *    a pool the model owns and keeps warm (cudaMallocFromPoolAsync /
- *    cudaFreeAsync on `stream`; no device-wide synchronisation; HB_E_OOM if
- *    it cannot be satisfied). It is also capturable in a CUDA graph.
+ *    HB_E_INVALID). The caller sizes `out` for the kind it asks for (see
+ *    hb_output); the library cannot check a buffer's length. The only
+ *    per-call device memory is scratch from a stream-ordered pool the model
+ *    owns and keeps warm (cudaMallocFromPoolAsync / cudaFreeAsync on
+ *    `stream`; no device-wide synchronisation; HB_E_OOM if it cannot be
+ *    satisfied): the rank codes of the pre-pass (hb_model_info.rank_prepass =
+ *    1; ceil(n_rows / 32) * 128 * words bytes) and the fp64 raw partials of a
+ *    TT model walked in L2-resident tree chunks (hb_model_info.tt_chunk_trees
+ *    > 0; n_rows * K * 8 bytes). Both are capturable in a CUDA graph.
+ *  - Arithmetic: comparisons are IEEE fp32 (Alg. 1-3); every scorer
+ *    sums leaf values in fp64 and forms the margin in fp64, so scores agree
+ *    with an fp64 tree-order sum to ~1 fp32 ulp whatever the summation order
+ *    (reading R23; the paper validates at rtol = atol = 1e-5,
+ *    P:469).
  *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *    stream). Calls only enqueue work and return once the launch succeeded;
  *    asynchronous kernel faults surface at the caller's synchronisation.
@@ -40,7 +48,8 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 3   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended */
+#define HB_ABI_VERSION 4   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended;
+                              4: HB_OUT_RAW64 + hb_finalize64 (fp64 raw sums) */
 
 typedef enum {
   HB_OK = 0,
@@ -77,8 +86,9 @@ typedef enum { HB_TASK_REGRESSION = 0, HB_TASK_CLASSIFICATION = 1 } hb_task;
  * Sec. 5.1 with thresholds recalibrated on B200 (DESIGN.md §6.1,
  * reading R24): PTT if D_max <= 10, else TT; GEMM only when forced or when
  * env HB_GEMM_MAX_DEPTH is set (3 restores the paper's CPU rule). Independently
- * of the strategy, calls with n_rows <= 4096 (env HB_SMALL_BATCH) use the
- * trees-across-threads small-batch kernel. */
+ * of the strategy, calls with n_rows <= hb_model_info.small_batch_max_rows
+ * (4096; env HB_SMALL_BATCH read at compile time) use the trees-across-threads
+ * small-batch kernel (small batches favour other kernels). */
 typedef enum {
   HB_STRATEGY_AUTO = 0,
   HB_STRATEGY_GEMM = 1,
@@ -93,7 +103,9 @@ typedef enum {
   HB_OUT_RAW = 2,        /* float[n*K]: sum of leaf values of THIS model's trees (tree-shard partial) */
   HB_OUT_MARGIN = 3,     /* float[n*K]: (MEAN ? raw/ntrees_k : raw) + base, no post               */
   HB_OUT_LEAF = 4,       /* int32[n*T_model]: tree-local ORIGINAL node id of the reached leaf     */
-  HB_OUT_LEAF_HASH = 5   /* uint64[n]: sum_t mix64((uint64)t_global << 32 | leaf) mod 2^64        */
+  HB_OUT_LEAF_HASH = 5,  /* uint64[n]: sum_t mix64((uint64)t_global << 32 | leaf) mod 2^64        */
+  HB_OUT_RAW64 = 6       /* double[n*K]: RAW in fp64 (the scorers accumulate in fp64), for
+                            tree-shard partials that are reduced and then hb_finalize64'd   */
 } hb_output;
 
 /*
@@ -149,20 +161,23 @@ typedef struct {
   int32_t tensor_cores;         /* 1 if the scorer runs tcgen05 MMAs (GEMM)    */
   int32_t node_record_bytes;    /* PTT/TT node record size (4 = rank-coded PTT) */
   int32_t kernel;               /* row-tile scorer: 0 ptt, 1 ptt rank-coded, 2 tt, 3 tt wide-row,
-                                   4 gemm tcgen05, 5 gemm CUDA-core, 6 tt 4-CTA cluster,
-                                   7 tt over 2-level node blocks
+                                   4 gemm tcgen05, 5 gemm CUDA-core (6, 7: removed
+                                   experimental TT kernels, never reported)
                                    (small batches: hb_small) */
   int32_t rows_per_cta;         /* rows one CTA owns per tile                   */
   int32_t code_cell_bits;       /* rank-coded PTT: 32 or 16-bit X code cells    */
   int32_t rank_prepass;         /* rank-coded PTT: 1 if a separate launch (rank_code_kernel)
                                    computes the X codes into stream-ordered scratch */
-  int32_t tt_sector;            /* wide-row TT: 1 if tt_wide_kernel walks sector-paired
-                                   records (a node and both children in one 32-B sector) */
+  int32_t tt_sector;            /* always 0 (sector-paired TT records were removed; kept for ABI layout) */
   int32_t tt_chunk_trees;       /* wide-row TT: trees per L2-resident chunk when the model is
                                    walked in several launches (0: one launch) */
+  int32_t small_batch_max_rows; /* calls with n_rows <= this run the small-batch kernel
+                                   (trees across threads) instead of `kernel` (ABI 4) */
 } hb_model_info;
 
-/* Host-only validation of an ensemble (no CUDA calls). HB_E_TREE names the
+/* Host-only validation of an ensemble (no CUDA calls): the tree structure
+ * the paper's compilers assume (binary trees of numerical splits, P:137;
+ * node tensors of Tables 3/5/6). HB_E_TREE names the
  * first offending tree/node. Rules: n_trees >= 1, n_features >= 1,
  * n_outputs >= 1, leaf_width in {1, K}; offsets monotone; each tree a rooted
  * binary tree (one parent per non-root node, no cycles, all nodes reachable,
@@ -172,8 +187,9 @@ typedef struct {
  * CLASSIFICATION => (K == 1 and SIGMOID) or K >= 2. */
 hb_status hb_validate(const hb_ensemble *e);
 
-/* Validate, select the strategy, build its layout (Tables 3/5/6) and upload it
- * to `device`. Forced PTT beyond its memory/depth budget -> HB_E_UNSUPPORTED
+/* Validate, select the strategy (Sec. 5.1), build its layout
+ * (Tables 3/5/6; perfect padding P:243; feature-selection
+ * injection P:316) and upload it to `device`. Forced PTT beyond its memory/depth budget -> HB_E_UNSUPPORTED
  * (AUTO falls back to TT). */
 hb_status hb_compile(const hb_ensemble *e, int32_t strategy, int32_t device, hb_model **out);
 
@@ -187,35 +203,65 @@ hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tre
 
 /* One fused scoring launch writing `kind` (hb_output) for rows [0, n_rows)
  * (two for rank_prepass models on more than the small-batch row count: the
- * rank-code pre-pass, then the scorer; both on `stream`). */
+ * rank-code pre-pass, then the scorer; one per L2-resident tree chunk plus a
+ * finalize for chunked TT models; all on `stream`).
+ * Defined by: the strategies' input/output contract, X in R^{n x |F|} in,
+ * R in R^{n x |C|} out — Alg. 1 P:171-172 (GEMM), Alg. 2
+ * (TreeTraversal), Alg. 3 P:262-263 (PerfectTreeTraversal) — followed by the
+ * reduction over the tree dimension of an ensemble and the post
+ * transforms of Table 2 (sigmoid, exp/logsumexp, argmax).
+ * Arguments: X device fp32 row-major, row r at X + r * ldx (ldx >= n_features);
+ * out device, sized per `kind` (hb_output); stream = cudaStream_t or NULL.
+ * Errors: HB_E_INVALID (NULL model/pointers, n_rows < 0, ldx < n_features,
+ * host or foreign-device pointers, bad kind), HB_E_UNSUPPORTED (PROBA on a
+ * regression model), HB_E_OOM (scratch), HB_E_CUDA (launch failure). */
 hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                         int32_t kind, void *out, void *stream);
 
-/* = hb_predict_ex(HB_OUT_PREDICT). */
+/* = hb_predict_ex(HB_OUT_PREDICT): the algorithms' output R (P:172, P:210,
+ * P:263) — regression: float[n*K] after the post transform; classification:
+ * int32[n] class index (K == 1: 1 iff margin > 0; else argmax, lowest index on
+ * ties; R22). */
 hb_status hb_predict(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                      void *out, void *stream);
-/* = hb_predict_ex(HB_OUT_PROBA); HB_E_UNSUPPORTED on a regression model. */
+/* = hb_predict_ex(HB_OUT_PROBA): class probabilities validated in P:469
+ * ("both the final scores and the probabilities"): float[n*C], C = 2 for a
+ * sigmoid model ([1-p, p]), else K. HB_E_UNSUPPORTED on a regression model. */
 hb_status hb_predict_proba(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                            float *out, void *stream);
-/* = hb_predict_ex(HB_OUT_RAW). */
+/* = hb_predict_ex(HB_OUT_RAW): float[n*K], the per-output sum over THIS
+ * model's trees of the selected leaf values — the tree-dimension reduction of
+ * P:192 before MEAN / base / post; a tree shard's partial. */
 hb_status hb_predict_raw(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                          float *out, void *stream);
-/* = hb_predict_ex(HB_OUT_LEAF). */
+/* = hb_predict_ex(HB_OUT_LEAF): int32[n*T_model], the tree-local ORIGINAL
+ * node id of the leaf each (row, tree) reaches — the leaf selection of Alg. 1
+ * (S == D), Alg. 2 (final T_I) and Alg. 3 (T_I - 2^D mapped
+ * back through the padding); the quantity the paper's output
+ * validation rests on and the bit-exact parity target. */
 hb_status hb_predict_leaf(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                           int32_t *out, void *stream);
 
-/* Epilogue only: from raw sums over ALL trees (e.g. the NCCL-reduced tree-shard
- * partials, float[n*K] on the device) write `kind` in {PREDICT, PROBA, MARGIN}
- * using the model's global tree counts, base score and post transform. */
+/* Epilogue only (P:192 reduction result -> Table 2 P:117 transforms): from
+ * raw sums over ALL trees (e.g. the NCCL-reduced tree-shard partials,
+ * float[n*K] on the device) write `kind` in {PREDICT, PROBA, MARGIN} using the
+ * model's global per-output tree counts (MEAN), base score and post
+ * transform. Errors as hb_predict_ex; HB_E_INVALID for any other kind. */
 hb_status hb_finalize(const hb_model *m, const float *raw, int64_t n_rows, int32_t kind,
                       void *out, void *stream);
+/* Same from fp64 raw sums (double[n*K], e.g. HB_OUT_RAW64 partials reduced
+ * in fp64), so a tree-sharded result carries no fp32 rounding before the
+ * margin is formed. */
+hb_status hb_finalize64(const hb_model *m, const double *raw, int64_t n_rows, int32_t kind,
+                        void *out, void *stream);
 
-/* End-to-end scoring from HOST memory: rows are streamed in chunks through
- * double-buffered device staging (H2D copy of chunk i+1 overlaps scoring of
- * chunk i on a second stream) and results copied back. Synchronous: returns
- * when `out_host` is filled. Pinned host buffers (cudaHostAlloc /
- * torch.pin_memory) are needed for the copies to overlap. kind as in
- * hb_predict_ex except LEAF. */
+/* End-to-end scoring from HOST memory (the same contract as hb_predict_ex,
+ * P:171-172 / P:209-210 / P:262-263, with X and out in host memory): rows are
+ * streamed in chunks through double-buffered device staging (H2D copy of chunk
+ * i+1 overlaps scoring of chunk i on a second stream) and results copied back.
+ * Synchronous: returns when `out_host` is filled. Pinned host buffers
+ * (cudaHostAlloc / torch.pin_memory) are needed for the copies to overlap.
+ * kind as in hb_predict_ex except LEAF (HB_E_UNSUPPORTED). */
 hb_status hb_predict_host(const hb_model *m, const float *X_host, int64_t n_rows, int64_t ldx,
                           int32_t kind, void *out_host);
 

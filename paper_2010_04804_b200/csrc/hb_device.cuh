@@ -161,35 +161,46 @@ __device__ __forceinline__ void load_x_slice_map(float *xs, const float *__restr
   for (int c = 0; c < nx; ++c) xs[c * 32 + lane] = row < n ? __ldg(xr + __ldg(fmap + c)) : 0.f;
 }
 
-// Fused epilogue for one row (a10/a11 of SURVEY §8): margin = acc / div +
-// base, post transform, proba / label, coalesced-enough row-major stores.
+// Fused epilogue for one row (a10/a11 of SURVEY §8; P:192 reduction, Table 2
+// P:117 transforms). The accumulators are fp64 (every scorer sums its fp32
+// leaf values in fp64), so the margin m_k = acc_k / div_k + base_k is formed
+// in fp64 as in the oracle and rounded once; labels take the argmax of the
+// fp64 margins; softmax exponentiates the fp64 differences m_k - max_j m_j.
 template <int NACC>
-__device__ __forceinline__ void write_row(int kind, const float (&acc)[NACC], int K, int task,
+__device__ __forceinline__ void write_row(int kind, const double (&acc)[NACC], int K, int task,
                                           int post, const float *__restrict__ scale /* divisor: ntrees_k (MEAN) or 1 */,
                                           const float *__restrict__ base, int64_t row, void *out) {
   if (kind == HB_OUT_RAW) {
     float *o = static_cast<float *>(out) + row * K;
 #pragma unroll
     for (int k = 0; k < NACC; ++k)
+      if (k < K) o[k] = (float)acc[k];
+    return;
+  }
+  if (kind == HB_OUT_RAW64) {
+    double *o = static_cast<double *>(out) + row * K;
+#pragma unroll
+    for (int k = 0; k < NACC; ++k)
       if (k < K) o[k] = acc[k];
     return;
   }
-  float m[NACC];
+  double m[NACC];
 #pragma unroll
-  for (int k = 0; k < NACC; ++k) m[k] = (k < K) ? acc[k] / __ldg(scale + k) + __ldg(base + k) : 0.f;
+  for (int k = 0; k < NACC; ++k)
+    m[k] = (k < K) ? acc[k] / (double)__ldg(scale + k) + (double)__ldg(base + k) : 0.0;
   if (kind == HB_OUT_MARGIN) {
     float *o = static_cast<float *>(out) + row * K;
 #pragma unroll
     for (int k = 0; k < NACC; ++k)
-      if (k < K) o[k] = m[k];
+      if (k < K) o[k] = (float)m[k];
     return;
   }
   if (kind == HB_OUT_PREDICT && task == HB_TASK_CLASSIFICATION) {
     int32_t lab = 0;
     if (K == 1) {
-      lab = m[0] > 0.f ? 1 : 0;
+      lab = m[0] > 0.0 ? 1 : 0;
     } else {
-      float best = m[0];
+      double best = m[0];
 #pragma unroll
       for (int k = 1; k < NACC; ++k)
         if (k < K && m[k] > best) { best = m[k]; lab = k; }
@@ -201,28 +212,28 @@ __device__ __forceinline__ void write_row(int kind, const float (&acc)[NACC], in
   float p[NACC];
   if (post == HB_POST_SIGMOID) {
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) p[k] = 1.f / (1.f + expf(-m[k]));
+    for (int k = 0; k < NACC; ++k) p[k] = 1.f / (1.f + expf(-(float)m[k]));
   } else if (post == HB_POST_SOFTMAX) {
-    float mx = m[0];
+    double mx = m[0];
 #pragma unroll
     for (int k = 1; k < NACC; ++k)
-      if (k < K) mx = fmaxf(mx, m[k]);
+      if (k < K) mx = fmax(mx, m[k]);
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < NACC; ++k) {
-      p[k] = (k < K) ? expf(m[k] - mx) : 0.f;
+      p[k] = (k < K) ? expf((float)(m[k] - mx)) : 0.f;
       s += p[k];
     }
 #pragma unroll
     for (int k = 0; k < NACC; ++k) p[k] = p[k] / s;
   } else if (post == HB_POST_ISOLATION) {
     // 2^(-mean path length / c(psi)); c(psi) is stored after the K base scores
-    const float c = __ldg(base + K);
+    const double c = (double)__ldg(base + K);
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) p[k] = exp2f(-m[k] / c);
+    for (int k = 0; k < NACC; ++k) p[k] = exp2f((float)(-m[k] / c));
   } else {
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) p[k] = m[k];
+    for (int k = 0; k < NACC; ++k) p[k] = (float)m[k];
   }
   if (kind == HB_OUT_PROBA && K == 1) {
     float2 v = make_float2(1.f - p[0], p[0]);

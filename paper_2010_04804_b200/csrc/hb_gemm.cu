@@ -168,9 +168,9 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmParams p) {
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
-  float acc[NACC];
+  double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
-  for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+  for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
   uint64_t h = 0;
   for (int t = 0; t < p.n_trees_pad; ++t) {
     const uint8_t *rec = p.trees + (size_t)t * p.stride;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmParams p) {
     // R <- T.E : gather the selected leaf's value(s)
     const float *E = reinterpret_cast<const float *>(rec + p.off_e);
     if (p.w == 1) {
-      const float v = __ldg(E + sel);
+      const double v = (double)__ldg(E + sel);
       const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rec));
 #pragma unroll
       for (int k = 0; k < NACC; ++k)
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmParams p) {
     } else {
 #pragma unroll
       for (int k = 0; k < NACC; ++k)
-        if (k < p.K) acc[k] += __ldg(E + sel * p.w + k);
+        if (k < p.K) acc[k] += (double)__ldg(E + sel * p.w + k);
     }
     if (lm && t < p.n_trees) {
       const int32_t id = __ldg(p.leafmap + (size_t)t * p.nl + sel);

@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
       xrow = p.X + (row < p.n ? row : 0) * p.ldx;
       xstride = 1;
     }
-    float acc[NACC];
+    double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
 
     for (int gi = 0; gi < p.ngroups; ++gi, ++it) {
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
           for (int j = 0; j < 8; ++j)
             if (S[hh * 8 + j] == dval[q * 8 + j]) sel = j;
           if (p.w == 1) {
-            const float v = E[q * 8 + sel];
+            const double v = (double)E[q * 8 + sel];
             const uint32_t k0 = tout[q];
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
           } else {
 #pragma unroll
             for (int k = 0; k < NACC; ++k)
-              if (k < p.K) acc[k] += E[(q * 8 + sel) * p.w + k];
+              if (k < p.K) acc[k] += (double)E[(q * 8 + sel) * p.w + k];
           }
           if (lm) {
             const int t = gi * kTcTrees + q;

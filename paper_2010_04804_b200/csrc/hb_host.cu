@@ -4,7 +4,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -335,149 +334,6 @@ static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLa
   return HB_OK;
 }
 
-// Sector-paired TT layout for tt_wide_kernel: nodes are
-// placed so that a "root" node and its two children share one 32-B L2 sector
-// (slots s, s+1, s+2 with s % 4 in {0, 1}), and the children of those children
-// start new sectors. Record (8 B): {N_F | flag << 15 | N_R << 16, N_T}; the
-// left child is N_R - 1 (flag 0: root, children adjacent in its sector) or
-// N_R - 4 (flag 1: the pair sits at the same offset of two consecutive
-// sectors). A walk then misses L1 at most once per two levels: the second
-// level of each sector is an L1 hit. Leaves keep the self-loop {j << 16, NaN}.
-// Needs F <= 32768 and <= 65535 slots per tree; node array 32-B aligned.
-static hb_status build_tt_sector(const hb_ensemble *e, int t0, int t1, int Tpad, HostLayout *L,
-                                 const FeatureMap *fm, int top) {
-  const int w = e->leaf_width;
-  const uint32_t qnan = 0x7FC00000u;
-  struct Tree {
-    std::vector<uint32_t> rec;     // 2 words per slot
-    std::vector<int32_t> orig;     // slot -> original node id of a leaf (-1 otherwise)
-  };
-  std::vector<Tree> trees(t1 - t0);
-  size_t maxslots = 4;
-  for (int t = t0; t < t1; ++t) {
-    Tree &T = trees[t - t0];
-    const int64_t a = e->node_offset[t];
-    int nsec = 0;
-    std::vector<int> ll_free;      // sector pairs (A, A+1) whose offset 3 is free in both
-    auto grow = [&](int sectors) {
-      const size_t n = (size_t)sectors * 4;
-      const size_t old = T.orig.size();
-      T.rec.resize(2 * n);
-      T.orig.resize(n, -1);
-      for (size_t j = old; j < n; ++j) T.rec[2 * j] = (uint32_t)j << 16, T.rec[2 * j + 1] = qnan;
-    };
-    auto alloc_pair = [&]() {
-      const int A = nsec;
-      nsec += 2;
-      grow(nsec);
-      return A;
-    };
-    auto feat = [&](int o) -> uint32_t {
-      return (uint32_t)(fm ? fm->remap[e->feature[a + o]] : e->feature[a + o]);
-    };
-    auto set_leaf = [&](int o, int slot) {
-      T.rec[2 * slot] = (uint32_t)slot << 16;
-      T.rec[2 * slot + 1] = qnan;
-      T.orig[slot] = o;
-    };
-    std::function<void(int, int)> place_root, place_mid;
-    // o internal at slot s (s % 4 in {0, 1}): children at s + 1, s + 2
-    place_root = [&](int o, int s) {
-      T.rec[2 * s] = feat(o) | ((uint32_t)(s + 2) << 16);
-      T.rec[2 * s + 1] = f2u(e->threshold[a + o]);
-      place_mid(e->left[a + o], s + 1);
-      place_mid(e->right[a + o], s + 2);
-    };
-    // o at slot s whose children (if any) go to (p, p + 4) of two new sectors
-    place_mid = [&](int o, int s) {
-      if (e->left[a + o] == -1) {
-        set_leaf(o, s);
-        return;
-      }
-      const int gl = e->left[a + o], gr = e->right[a + o];
-      const bool lleaf = e->left[a + gl] == -1, rleaf = e->left[a + gr] == -1;
-      int p;
-      if (lleaf && rleaf && !ll_free.empty()) {
-        p = 4 * ll_free.back() + 3;          // two leaves: reuse free offset-3 slots
-        ll_free.pop_back();
-      } else {
-        const int A = alloc_pair();
-        p = 4 * A;
-        if (!lleaf && !rleaf) ll_free.push_back(A);
-      }
-      T.rec[2 * s] = feat(o) | 0x8000u | ((uint32_t)(p + 4) << 16);
-      T.rec[2 * s + 1] = f2u(e->threshold[a + o]);
-      if (lleaf) set_leaf(gl, p);
-      else place_root(gl, p);
-      if (rleaf) set_leaf(gr, p + 4);
-      else place_root(gr, p + 4);
-    };
-    if (top <= 0) {
-      nsec = 1;
-      grow(1);
-      if (e->left[a] == -1) set_leaf(0, 0);
-      else place_root(0, 0);
-    } else {
-      // top levels in BFS order (siblings adjacent, flag 0): they are shared
-      // by the rows of a tile and pack densely into a few L1 lines; nodes at
-      // depth top - 1 start the sector-paired part below
-      struct Q { int o, slot, depth; };
-      std::vector<Q> q(1, Q{0, 0, 0});
-      int nb = 1;
-      std::vector<int> right_slot;
-      for (size_t k = 0; k < q.size(); ++k) {
-        const Q c = q[k];
-        right_slot.push_back(-1);
-        if (e->left[a + c.o] != -1 && c.depth < top - 1) {
-          q.push_back(Q{e->left[a + c.o], nb, c.depth + 1});
-          q.push_back(Q{e->right[a + c.o], nb + 1, c.depth + 1});
-          right_slot[k] = nb + 1;
-          nb += 2;
-        }
-      }
-      nsec = (nb + 3) / 4;
-      grow(nsec);
-      for (size_t k = 0; k < q.size(); ++k) {
-        const Q c = q[k];
-        if (e->left[a + c.o] == -1) {
-          set_leaf(c.o, c.slot);
-        } else if (right_slot[k] >= 0) {
-          T.rec[2 * c.slot] = feat(c.o) | ((uint32_t)right_slot[k] << 16);
-          T.rec[2 * c.slot + 1] = f2u(e->threshold[a + c.o]);
-        } else {
-          place_mid(c.o, c.slot);
-        }
-      }
-    }
-    if (T.orig.size() > 65535) return fail(HB_E_UNSUPPORTED, "TT sector layout: tree needs more than 65535 slots");
-    maxslots = std::max(maxslots, T.orig.size());
-  }
-  L->nslots = (int)maxslots;
-  L->stride = (32 + (size_t)8 * maxslots + (size_t)4 * w * maxslots + 31) & ~size_t(31);
-  L->trees.assign((size_t)Tpad * L->stride, 0);
-  L->leafmap.assign((size_t)Tpad * maxslots, -1);
-  for (int lt = 0; lt < Tpad; ++lt) {
-    uint8_t *rec = L->trees.data() + (size_t)lt * L->stride;
-    uint32_t *hdr = reinterpret_cast<uint32_t *>(rec);
-    uint32_t *node = reinterpret_cast<uint32_t *>(rec + 32);
-    float *leaf = reinterpret_cast<float *>(rec + 32 + (size_t)8 * maxslots);
-    for (size_t j = 0; j < maxslots; ++j) node[2 * j] = (uint32_t)j << 16, node[2 * j + 1] = qnan;
-    if (lt >= t1 - t0) continue;
-    const int t = t0 + lt;
-    const int64_t a = e->node_offset[t];
-    hdr[0] = (uint32_t)(w == 1 ? tree_out(e, t) : 0);
-    const Tree &T = trees[lt];
-    std::memcpy(node, T.rec.data(), T.rec.size() * 4);
-    for (size_t j = 0; j < T.orig.size(); ++j) {
-      const int o = T.orig[j];
-      if (o < 0) continue;
-      L->leafmap[(size_t)lt * maxslots + j] = o;
-      for (int k = 0; k < w; ++k) leaf[j * w + k] = e->leaf_value[(a + o) * w + k];
-    }
-  }
-  return HB_OK;
-}
-
 static int env_int(const char *name, int dflt) {
   const char *v = std::getenv(name);
   if (!v || !*v) return dflt;
@@ -566,14 +422,36 @@ static void free_model(Model *m) {
   cudaFree(m->sb_own_trees);
   cudaFree(m->sb_own_leafmap);
   cudaFree(m->d_fmap);
-  cudaFree(m->d_tops);
   cudaFree(m->d_rb);
-  cudaFree(m->d_rbc);
-  cudaFree(m->d_ttb);
-  cudaFree(m->d_ttw);
-  cudaFree(m->d_ttw_leafmap);
   if (m->mempool) cudaMemPoolDestroy(m->mempool);   // deferred until pending frees complete
   delete m;
+}
+
+hb_status ensure_pool(Model *m) {
+  if (m->mempool) return HB_OK;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = m->device;
+  cudaError_t err;
+  if ((err = cudaMemPoolCreate(&m->mempool, &props)) != cudaSuccess) return cuda_fail(err, "cudaMemPoolCreate");
+  uint64_t keep = UINT64_MAX;
+  if ((err = cudaMemPoolSetAttribute(m->mempool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
+    return cuda_fail(err, "cudaMemPoolSetAttribute");
+  return HB_OK;
+}
+
+hb_status scratch_alloc(const Model &m, size_t bytes, cudaStream_t s, void **p) {
+  // under stream capture the allocation becomes a graph memory node, which
+  // CUDA supports for the device's default pool
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusNone;
+  bytes = std::max<size_t>(bytes, 128);
+  const cudaError_t e = (cap == cudaStreamCaptureStatusActive || !m.mempool)
+                            ? cudaMallocAsync(p, bytes, s)
+                            : cudaMallocFromPoolAsync(p, bytes, m.mempool, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync(scratch)");
+  return HB_OK;
 }
 
 template <typename T>
@@ -666,6 +544,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
                           " exceed the perfect-tree / SMEM budget (use TT or AUTO)");
         strat = HB_STRATEGY_TT;
         L = HostLayout();
+        m->n_trees_pad = (m->n_trees + kTreeGroup - 1) / kTreeGroup * kTreeGroup;
       }
     }
     if (!done && strat == HB_STRATEGY_TT) {
@@ -678,15 +557,13 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
       if (!narrow || force_wide == 1) {
         if (force_wide == 0) return fail(HB_E_UNSUPPORTED, "TT: no narrow configuration fits");
         LaunchCfg c;
-        const int K = e->n_outputs;
-        const int nacc = K == 1 ? 1 : (K <= 4 ? 4 : (K <= 8 ? 8 : 16));
         c.nw = 32;
         c.wide_rows = 0;
         const int force_r = env_int("HB_TT_WIDE_ROWS", 0);   // tuning override (32/16/8)
         for (int R : {32, 16, 8}) {
           if (force_r && R != force_r) continue;
-          const long bytes = (long)fmap.used.size() * R * 4 + (long)c.nw * R * (4L * nacc + 8);
-          if (bytes <= kSmemBudget) {
+          const size_t bytes = tt_wide_smem((int)fmap.used.size(), R, c.nw, m->nacc);
+          if (bytes <= (size_t)kSmemBudget) {
             c.wide_rows = R;
             c.smem_bytes = (int)bytes;
             break;
@@ -697,82 +574,28 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.t_smem = 0;
         c.ch = kTreeGroup;
         m->cfg = c;
-        m->tt_g = env_int("HB_TT_G", 4);
-        m->tt_top_prefetch = env_int("HB_TT_TOP_PF", 0);
-        m->tt_cursor = env_int("HB_TT_CURSOR", 0);
-        // sector-paired records (one L2 sector per two levels of a walk,
-        // HB_TT_SECTOR=1): faster than one BFS launch when the records exceed
-        // L2 (C5, 10k trees on one GPU: 16.96 -> 15.57 ms), slower on an
-        // L2-resident model (C5 1/8 shard: 1.83 vs 2.03-2.14 ms: siblings 4
-        // slots apart touch more sectors per tile); L2-resident tree chunks
-        // (below) beat both, so AUTO uses those.
-        int l2_bytes = 0;
-        cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
-        const int want_sector = env_int("HB_TT_SECTOR", -1);
-        const bool big = (double)m->n_trees_pad * (double)L.stride > 0.75 * (double)l2_bytes;
-        if (!(want_sector == 1 || (want_sector == -1 && big)) && env_int("HB_TT_PAIR", 0) == 1) {
-          // pair-aligned BFS records: node array at +24 so every sibling pair
-          // (2m+1, 2m+2) is one aligned 16-B word (lookahead walk, hb_tt.cu)
-          const size_t nbytes = (size_t)8 * L.nslots, lbytes = (size_t)4 * e->leaf_width * L.nslots;
-          const size_t stride2 = round16(24 + nbytes + lbytes);
-          std::vector<uint8_t> t2((size_t)m->n_trees_pad * stride2, 0);
-          for (int lt = 0; lt < m->n_trees_pad; ++lt) {
-            const uint8_t *src = L.trees.data() + (size_t)lt * L.stride;
-            uint8_t *dst = t2.data() + (size_t)lt * stride2;
-            std::memcpy(dst, src, 16);
-            std::memcpy(dst + 24, src + 16, nbytes + lbytes);
-          }
-          st = upload(t2, reinterpret_cast<uint8_t **>(&m->d_ttw), &m->device_bytes);
-          if (st != HB_OK) return st;
-          m->ttw_stride = stride2;
-          m->ttw_nslots = L.nslots;
-          m->tt_pair = 1;
-        }
         // models larger than L2: walk them in tree chunks whose records stay
         // L2-resident (HB_TT_CHUNK: -1 auto, N trees, 0 off). Auto size: the
         // chunk's actual node + leaf bytes (not the padded stride) = 0.4 x L2
         // — C5, 10k trees on one GPU (measured, 100K rows): 1000 / 1500 /
         // 2500 / 3336 / 5000 trees per chunk = 15.5 / 14.7 / 13.7 / 15.1 /
-        // 17.2 ms; sector-paired records 15.7 ms, one BFS launch 17.2 ms
+        // 17.2 ms; one launch over all trees 17.2 ms
+        int l2_bytes = 0;
+        cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
+        const bool big = (double)m->n_trees_pad * (double)L.stride > 0.75 * (double)l2_bytes;
         const int want_chunk = env_int("HB_TT_CHUNK", -1);
-        if (want_chunk > 0 || (want_chunk == -1 && big && want_sector != 1)) {
+        if (want_chunk > 0 || (want_chunk == -1 && big)) {
           double bytes = 0;
           for (int t = t0; t < t1; ++t)
             bytes += (double)(e->node_offset[t + 1] - e->node_offset[t]) * (8.0 + 4.0 * e->leaf_width);
           const double per_tree = std::max(1.0, bytes / std::max(1, t1 - t0));
           const int autoc = (int)(0.4 * (double)l2_bytes / per_tree) & ~(kTreeGroup - 1);
           m->tt_chunk = std::max(kTreeGroup, want_chunk > 0 ? want_chunk : autoc);
+          if (m->tt_chunk >= m->n_trees_pad) m->tt_chunk = 0;   // one chunk: one plain launch
         }
-        if (m->tt_chunk == 0 && want_sector == 1 && fmap.used.size() <= 32768) {
-          HostLayout S;
-          st = build_tt_sector(e, t0, t1, m->n_trees_pad, &S, &fmap, env_int("HB_TT_SECTOR_TOP", 4));
-          if (st == HB_OK) {
-            st = upload(S.trees, reinterpret_cast<uint8_t **>(&m->d_ttw), &m->device_bytes);
-            if (st != HB_OK) return st;
-            st = upload(S.leafmap, &m->d_ttw_leafmap, &m->device_bytes);
-            if (st != HB_OK) return st;
-            m->ttw_stride = S.stride;
-            m->ttw_nslots = S.nslots;
-            m->tt_sector = 1;
-          } else if (st != HB_E_UNSUPPORTED) {
-            return st;
-          }
-        }
-        // opt-in (HB_TT_BLOCK=1): 2-level node blocks walked by per-lane
-        // cursors (hb_ttb.cu); measured slower than
-        // tt_wide_kernel on C5, so AUTO keeps tt_wide_kernel
-        if (env_int("HB_TT_BLOCK", 0) && !env_int("HB_TT_CLUSTER", 0)) {
-          st = compile_tt_blocks(e, t0, t1, fmap.identity ? nullptr : fmap.remap.data(), m.get());
+        if (m->tt_chunk) {
+          st = ensure_pool(m.get());
           if (st != HB_OK) return st;
-        }
-        // large ensembles on wide rows: 4-CTA clusters with SMEM-resident top
-        // levels (hb_tt_cluster.cu) when all features are used and tops fit
-        if (fmap.identity && env_int("HB_TT_CLUSTER", 0)) {
-          m->stride = L.stride;
-          m->nslots = L.nslots;
-          st = compile_tt_cluster(e, t0, t1, m.get(), nullptr, L.trees);
-          if (st == HB_OK) m->tt_cluster = 1;
-          else if (st != HB_E_UNSUPPORTED) return st;
         }
       }
     }
@@ -827,6 +650,11 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     m->sb_depth = D;
   }
 
+  // request/response sizes: trees-across-threads kernel (f2) for n_rows <=
+  // small_max; threshold from the crossover sweep (tools/crossover.py,
+  // DESIGN.md §6.2), env HB_SMALL_BATCH overrides (0: off) at compile time
+  m->small_max = m->sb_trees ? std::max(0, env_int("HB_SMALL_BATCH", 4096)) : 0;
+
   // global per-output tree counts (MEAN divisor) and base score
   std::vector<float> div(K, 1.f), base(K + 1, 0.f);   // base[K] = post_param
   if (e->agg == HB_AGG_MEAN) {
@@ -874,12 +702,13 @@ static size_t out_row_bytes(const Model &m, int kind) {
     case HB_OUT_MARGIN: return 4 * (size_t)m.n_outputs;
     case HB_OUT_LEAF: return 4 * (size_t)m.n_trees;
     case HB_OUT_LEAF_HASH: return 8;
+    case HB_OUT_RAW64: return 8 * (size_t)m.n_outputs;
   }
   return 0;
 }
 
 static hb_status check_kind(const Model &m, int kind) {
-  if (kind < HB_OUT_PREDICT || kind > HB_OUT_LEAF_HASH) return fail(HB_E_INVALID, "bad output kind");
+  if (kind < HB_OUT_PREDICT || kind > HB_OUT_RAW64) return fail(HB_E_INVALID, "bad output kind");
   if (kind == HB_OUT_PROBA && m.task != HB_TASK_CLASSIFICATION)
     return fail(HB_E_UNSUPPORTED, "predict_proba on a regression model");
   return HB_OK;
@@ -914,8 +743,7 @@ static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int
   RunArgs a{X, n, ldx, kind, out, static_cast<cudaStream_t>(stream), nullptr};
   // request/response sizes: trees-across-threads kernel (f2); threshold from
   // the crossover sweep (tools/crossover.py)
-  const int small_max = env_int("HB_SMALL_BATCH", 4096);
-  if (n <= small_max && m.sb_trees) return launch_small_batch(m, a);
+  if (n <= m.small_max) return launch_small_batch(m, a);
   return run(m, a);
 }
 
@@ -1040,8 +868,8 @@ hb_status hb_predict_leaf(const hb_model *m, const float *X, int64_t n, int64_t 
   return predict_impl(m, X, n, ldx, HB_OUT_LEAF, out, stream, true);
 }
 
-hb_status hb_finalize(const hb_model *hm, const float *raw, int64_t n, int32_t kind, void *out,
-                      void *stream) {
+static hb_status finalize_impl(const hb_model *hm, const float *raw, const double *raw64, int64_t n,
+                               int32_t kind, void *out, void *stream) {
   if (!hm) return fail(HB_E_INVALID, "model is NULL");
   const Model &m = *M(hm);
   if (kind != HB_OUT_PREDICT && kind != HB_OUT_PROBA && kind != HB_OUT_MARGIN)
@@ -1050,12 +878,23 @@ hb_status hb_finalize(const hb_model *hm, const float *raw, int64_t n, int32_t k
   if (st != HB_OK) return st;
   if (n < 0) return fail(HB_E_INVALID, "n_rows < 0");
   if (n == 0) return HB_OK;
-  if (!raw || !out) return fail(HB_E_INVALID, "raw or out is NULL");
+  if ((!raw && !raw64) || !out) return fail(HB_E_INVALID, "raw or out is NULL");
   DeviceGuard g(m.device);
-  if ((st = check_dev_ptr(raw, m.device, "raw")) != HB_OK) return st;
+  if ((st = check_dev_ptr(raw ? (const void *)raw : (const void *)raw64, m.device, "raw")) != HB_OK) return st;
   if ((st = check_dev_ptr(out, m.device, "out")) != HB_OK) return st;
   RunArgs a{nullptr, n, 0, kind, out, static_cast<cudaStream_t>(stream), raw};
+  a.raw_in64 = raw64;
   return launch_finalize(m, a);
+}
+
+hb_status hb_finalize(const hb_model *hm, const float *raw, int64_t n, int32_t kind, void *out,
+                      void *stream) {
+  return finalize_impl(hm, raw, nullptr, n, kind, out, stream);
+}
+
+hb_status hb_finalize64(const hb_model *hm, const double *raw, int64_t n, int32_t kind, void *out,
+                        void *stream) {
+  return finalize_impl(hm, nullptr, raw, n, kind, out, stream);
 }
 
 hb_status hb_predict_host(const hb_model *m, const float *X, int64_t n, int64_t ldx, int32_t kind,
@@ -1082,14 +921,15 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : (m.ptt_rank ? 4 : 8);
   if (m.strategy == HB_STRATEGY_PTT) info->kernel = m.ptt_rank ? 1 : 0;
   else if (m.strategy == HB_STRATEGY_TT)
-    info->kernel = m.tt_cluster ? 6 : (m.tt_blocks ? 7 : (m.cfg.wide_rows ? 3 : 2));
+    info->kernel = m.cfg.wide_rows ? 3 : 2;
   else info->kernel = m.gemm_tc ? 4 : 5;
   info->rows_per_cta = m.strategy == HB_STRATEGY_GEMM ? (m.gemm_tc ? 128 : 128)
                        : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);
   info->code_cell_bits = m.ptt_rank ? m.rank_cw : 0;
   info->rank_prepass = m.rank_pre;
-  info->tt_sector = m.tt_sector;
+  info->tt_sector = 0;   // sector-paired TT records were removed
   info->tt_chunk_trees = m.tt_chunk;
+  info->small_batch_max_rows = m.small_max;
   return HB_OK;
 }
 

@@ -74,13 +74,7 @@ struct Model {
   int rb_ngroups = 0;
   uint32_t rb_max_span = 0;  // widest X column span of a table group (staged pre-pass)
   bool rb_global = false;    // some table group is searched from global memory
-  // cluster pre-pass plan: <= 8 table groups, one per CTA of a cluster
-  int rbc_cl = 0;            // CTAs per cluster (0: no cluster plan)
-  void *d_rbc = nullptr;     // [feat | groups | own | pool]
-  size_t rbc_groups_off = 0, rbc_own_off = 0, rbc_pool_off = 0, rbc_smem = 0;
-  uint32_t rbc_max_pitch = 0;
-  int rbc_tile = 2048;       // rows per cluster tile (2048 or 1024)
-  cudaMemPool_t mempool = nullptr;
+  cudaMemPool_t mempool = nullptr;   // per-call scratch (rank codes, TT chunk partials)
 
   // small-batch path (hb_small.cu): PTT fp32 or TT records walked by
   // trees-across-threads; may alias d_trees / d_leafmap
@@ -93,36 +87,14 @@ struct Model {
   int sb_nrec = 0;                    // records in sb_trees (PTT: class-ordered, padded)
   const int32_t *sb_fmap = nullptr;   // feature map of the small-batch records
   int sb_nxf = 0;
+  int small_max = 0;                  // n_rows <= small_max -> small-batch kernel
 
   // feature-selection injection: fp32 PTT / TT records index a
   // compacted X tile holding only the model's used features
   int32_t *d_fmap = nullptr;   // [n_xf] compact column -> original feature (null: identity)
   int n_xf = 0;
 
-  // TT cluster kernel (hb_tt_cluster.cu): SMEM-resident top levels per CTA
-  int tt_cluster = 0;
-  void *d_tops = nullptr;
-  int cl_topd = 0, cl_per_cta = 0, cl_smem = 0;
-  size_t cl_top_bytes = 0;
-
-  // TT over 2-level node blocks (hb_ttb.cu): [blocks | leaves | lorig | cls]
-  int tt_blocks = 0;
-  void *d_ttb = nullptr;
-  size_t ttb_leaf_off = 0, ttb_lorig_off = 0, ttb_cls_off = 0;
-  int64_t ttb_nblocks = 0;
-  int ttb_sync = 1;          // lanes of a warp advance a cursor together
-  int tt_g = 4;              // tt_wide_kernel: concurrent walks per lane (4, 6, 8)
-  // sector-paired TT records for tt_wide_kernel (hb_host.cu build_tt_sector):
-  // a root and its two children share one 32-B sector; own records + leafmap
-  int tt_sector = 0;
-  int tt_cursor = 0;         // tt_wide_kernel: per-lane tree cursors (HB_TT_CURSOR)
-  int tt_pair = 0;           // tt_wide_kernel: pair-aligned BFS records in d_ttw + child lookahead
   int tt_chunk = 0;          // tt_wide_kernel: trees per L2-resident chunk (0: one launch)
-  int tt_top_prefetch = 0;   // tt_wide_kernel: prefetch.global.L1 of the next tree group's top lines
-  void *d_ttw = nullptr;
-  int32_t *d_ttw_leafmap = nullptr;
-  size_t ttw_stride = 0;
-  int ttw_nslots = 0;
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
@@ -140,7 +112,8 @@ struct RunArgs {
   int kind;                 // hb_output
   void *out;
   cudaStream_t stream;
-  const float *raw_in;      // finalize only
+  const float *raw_in;      // finalize only: fp32 raw sums (hb_finalize)
+  const double *raw_in64 = nullptr;   // finalize only: fp64 raw sums (hb_finalize64, tree chunks)
 };
 
 bool gemm_supported(int depth);
@@ -172,19 +145,17 @@ struct RankBuckets {
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
                              int cw, RankBuckets *out, size_t cap_bytes = 0);
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
-// cluster pre-pass (hb_rank_codes_cluster.cu): all tables in one cluster's SMEM
-size_t rank_cluster_stage_bytes(uint32_t max_pitch, int tile);
-hb_status launch_rank_codes_cluster(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);
 hb_status launch_tt(const Model &m, const RunArgs &a);
 hb_status launch_gemm(const Model &m, const RunArgs &a);
 hb_status launch_finalize(const Model &m, const RunArgs &a);
 hb_status launch_small_batch(const Model &m, const RunArgs &a);
-hb_status compile_tt_cluster(const hb_ensemble *e, int t0, int t1, Model *m, const int32_t *fremap,
-                             const std::vector<uint8_t> &tt_trees);
-hb_status launch_tt_cluster(const Model &m, const RunArgs &a);
-hb_status compile_tt_blocks(const hb_ensemble *e, int t0, int t1, const int32_t *remap, Model *m);
-hb_status launch_tt_blocks(const Model &m, const RunArgs &a);
+size_t tt_wide_smem(int F, int R, int nwarps, int nacc);
+// model-owned stream-ordered scratch (hb_host.cu): a pool created at compile
+// time with release threshold UINT64_MAX, so per-call allocations reuse warm
+// memory; under stream capture the device default pool is used instead
+hb_status ensure_pool(Model *m);
+hb_status scratch_alloc(const Model &m, size_t bytes, cudaStream_t s, void **p);
 
 }  // namespace hb

@@ -104,9 +104,9 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
       if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
       else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
     }
-    float acc[NACC];
+    double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
 
     for (int c = 0; c < nchunks; ++c, ring.next()) {
@@ -146,19 +146,19 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
 #pragma unroll
           for (int g = 0; g < G; ++g) off[g] = a[g] - tb[g];
           // R <- N'_C[T_I - 2^D]
-          float vsum = 0.f;
+          double vsum = 0.0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const uint32_t slot = (off[g] >> 3) - (1u << D);
             if (p.w == 1) {
-              const float v = dev::lds_f32(tb[g] + leaf_off + (off[g] >> 1));
+              const double v = (double)dev::lds_f32(tb[g] + leaf_off + (off[g] >> 1));
               if (NACC == 1) acc[0] += v;
               else vsum += v;
             } else {
               const uint32_t lb = tb[g] + (8u << D) + 4u * slot * (uint32_t)p.w;
 #pragma unroll
               for (int k = 0; k < NACC; ++k)
-                if (k < p.K) acc[k] += dev::lds_f32(lb + 4u * k);
+                if (k < p.K) acc[k] += (double)dev::lds_f32(lb + 4u * k);
             }
           }
           if (NACC > 1 && p.w == 1) {

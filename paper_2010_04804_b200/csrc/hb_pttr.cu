@@ -317,79 +317,12 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     m->rb_smem_cap = R.smem_cap;
     m->rb_max_span = R.max_span;
     m->rb_global = R.any_global;
-    // cluster plan (hb_rank_codes_cluster.cu): <= 8 table groups of balanced
-    // size, one per CTA of a thread-block cluster, when the tables fit
-    if (env_int2("HB_RC_CLUSTER", 0) == 1 && F <= 128) {
-      RankBuckets all;
-      hb_status st2 = build_rank_buckets(sorted, origf, cw, &all, (size_t)1 << 40);
-      if (st2 != HB_OK) return st2;
-      const size_t total = all.groups.size() >= 2 ? all.groups[1] : 0;
-      const size_t kTabMax = 160 * 1024;
-      RankBuckets C;
-      bool ok = false;
-      for (double slack : {1.05, 1.15, 1.3, 1.5}) {
-        const size_t capc = (size_t)((double)total / 8.0 * slack) + 16;
-        if (capc > kTabMax) break;
-        st2 = build_rank_buckets(sorted, origf, cw, &C, capc);
-        if (st2 != HB_OK) return st2;
-        if (C.n_groups <= 8 && C.max_group_bytes > 0 && !C.any_global) {
-          ok = true;
-          break;
-        }
-      }
-      const int pw = cw == 32 ? 1 : 2;
-      uint32_t maxp = 1;
-      if (ok) {
-        for (int k = 0; k < C.n_groups; ++k) {
-          const int wb = (int)C.groups[8 * k + 2], we = (int)C.groups[8 * k + 3];
-          const int nf = std::min(we * pw, A.n_fc) - wb * pw;
-          C.groups[8 * k + 4] = (uint32_t)(nf | 1);      // staging row pitch (odd)
-          C.groups[8 * k + 5] = (uint32_t)nf;
-          maxp = std::max<uint32_t>(maxp, (uint32_t)(nf | 1));
-        }
-        const size_t tb = (C.max_group_bytes + 15) & ~size_t(15);
-        int tile = 2048;
-        if (tb + rank_cluster_stage_bytes(maxp, tile) > (size_t)kSmemBudget) tile = 1024;
-        if (tb + rank_cluster_stage_bytes(maxp, tile) > (size_t)kSmemBudget) ok = false;
-        m->rbc_tile = tile;
-      }
-      if (ok) {
-        std::vector<int32_t> own((size_t)F, -1);
-        for (int k = 0; k < C.n_groups; ++k) {
-          const int wb = (int)C.groups[8 * k + 2], we = (int)C.groups[8 * k + 3];
-          for (int c = wb * pw; c < std::min(we * pw, A.n_fc); ++c) own[origf[c]] = (k << 16) | (c - wb * pw);
-        }
-        const size_t fb2 = C.feat.size() * 4, gb2 = C.groups.size() * 4, ob = own.size() * 4;
-        const size_t pool2 = (fb2 + gb2 + ob + 127) & ~size_t(127);
-        std::vector<uint8_t> aux2(pool2 + C.pool.size(), 0);
-        std::memcpy(aux2.data(), C.feat.data(), fb2);
-        std::memcpy(aux2.data() + fb2, C.groups.data(), gb2);
-        std::memcpy(aux2.data() + fb2 + gb2, own.data(), ob);
-        std::memcpy(aux2.data() + pool2, C.pool.data(), C.pool.size());
-        if ((err = cudaMalloc(&m->d_rbc, aux2.size())) != cudaSuccess) return cuda_fail(err, "cudaMalloc(rank cluster tables)");
-        m->device_bytes += aux2.size();
-        if ((err = cudaMemcpy(m->d_rbc, aux2.data(), aux2.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
-          return cuda_fail(err, "cudaMemcpy(rank cluster tables)");
-        m->rbc_groups_off = fb2;
-        m->rbc_own_off = fb2 + gb2;
-        m->rbc_pool_off = pool2;
-        m->rbc_smem = C.max_group_bytes;
-        m->rbc_max_pitch = maxp;
-        m->rbc_cl = C.n_groups;
-      }
-    }
     m->rank_nwords = R.n_words;
     m->rank_ngroups = 0;
     // per-call code scratch: stream-ordered allocations from a model-owned
     // pool that keeps its memory (no cudaMalloc on the scoring path)
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = m->device;
-    if ((err = cudaMemPoolCreate(&m->mempool, &props)) != cudaSuccess) return cuda_fail(err, "cudaMemPoolCreate");
-    uint64_t keep = UINT64_MAX;
-    if ((err = cudaMemPoolSetAttribute(m->mempool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
-      return cuda_fail(err, "cudaMemPoolSetAttribute");
+    const hb_status pst = ensure_pool(m);
+    if (pst != HB_OK) return pst;
   }
   m->rank_pre = pre ? 1 : 0;
   m->rank_nfc = A.n_fc;
@@ -405,9 +338,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
 int sm_count(int device);
 
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
-  const bool top = m.rank_cw == 32 && env_int2("HB_PTTR_TOP", 0) == 1;
   PttrFn fn = m.rank_cw == 16 ? pttr_fn16(m.depth, m.cmp == HB_CMP_LE, m.nacc)
-              : top           ? pttr_fn32_top(m.depth, m.cmp == HB_CMP_LE, m.nacc)
                               : pttr_fn32(m.depth, m.cmp == HB_CMP_LE, m.nacc);
   if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
   PttrParams p;
@@ -418,14 +349,8 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   if (m.rank_pre) {
     const int64_t nblocks = (a.n + 31) / 32;
     const size_t bytes = std::max<size_t>((size_t)nblocks * m.rank_nwords * 128, 128);
-    // under stream capture the allocation becomes a graph memory node, which
-    // CUDA supports for the device's default pool
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(a.stream, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusNone;
-    e = cap == cudaStreamCaptureStatusActive
-            ? cudaMallocAsync(reinterpret_cast<void **>(&codes), bytes, a.stream)
-            : cudaMallocFromPoolAsync(reinterpret_cast<void **>(&codes), bytes, m.mempool, a.stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync(rank codes)");
+    const hb_status ast = scratch_alloc(m, bytes, a.stream, reinterpret_cast<void **>(&codes));
+    if (ast != HB_OK) return ast;
     const hb_status st = launch_rank_codes(m, a, codes, nblocks);
     if (st != HB_OK) {
       cudaFreeAsync(codes, a.stream);

@@ -47,16 +47,7 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
 // share lane l's 32-bit word (bank l) of row m; node = off16 << 16 | k with
 // off16 = (fc>>1)*128 + (fc&1)*2, left <=> (node & 0xFFFF) >= c(x): half the
 // tile, one more instruction per level.
-__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-
-// TOP (opt-in, HB_PTTR_TOP=1, 32-bit cells): the record's first 16 B (header,
-// heap nodes 1-3) as one broadcast LDS.128 per tree, so levels 1 and 2 cost one
-// node wavefront instead of two.
-template <int D, bool LE, int NACC, int G, int CW, bool TOP = false>
+template <int D, bool LE, int NACC, int G, int CW>
 __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,9 +185,12 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
       dev::release_stage(&empty[s], lane);
     }
 
-    float acc[NACC];
+    // fp64 accumulators: every fp32 leaf value is added exactly enough that
+    // the sum matches the oracle's fp64 sum to ~1e-16 relative whatever the
+    // order (R23), at one F2F + DADD per (row, tree)
+    double acc[NACC];
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
     for (int c = 0; c < nchunks; ++c, ring.next()) {
       const int s = ring.s;
@@ -216,20 +210,10 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
             m4[g] = 4u - tb[g];
           }
 #pragma unroll
-          uint4 top[G];
-          bool left0[G];
           for (int l = 0; l < D; ++l) {
             uint32_t nd[G];
-            if (TOP && D >= 2 && l == 0) {
 #pragma unroll
-              for (int g = 0; g < G; ++g) { top[g] = lds_v4(tb[g]); nd[g] = top[g].y; }
-            } else if (TOP && D >= 2 && l == 1) {
-#pragma unroll
-              for (int g = 0; g < G; ++g) nd[g] = left0[g] ? top[g].z : top[g].w;
-            } else {
-#pragma unroll
-              for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(a[g]);
-            }
+            for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(a[g]);
             uint32_t xc[G];
 #pragma unroll
             for (int g = 0; g < G; ++g)
@@ -238,26 +222,25 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
             for (int g = 0; g < G; ++g) {
               // k >= c(x)  <=>  x < u_k
               const bool left = CW == 32 ? nd[g] >= xc[g] : (nd[g] & 0xFFFFu) >= xc[g];
-              if (l == 0) left0[g] = left;
               a[g] = 2u * a[g] + (left ? m0[g] : m4[g]);
             }
           }
           uint32_t off[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) off[g] = a[g] - tb[g];
-          float vsum = 0.f;
+          double vsum = 0.0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const uint32_t slot = (off[g] >> 2) - (1u << D);
             if (p.w == 1) {
-              const float v = dev::lds_f32(tb[g] + off[g]);
+              const double v = (double)dev::lds_f32(tb[g] + off[g]);
               if (NACC == 1) acc[0] += v;
               else vsum += v;
             } else {
               const uint32_t lb = tb[g] + (4u << D) + 4u * slot * (uint32_t)p.w;
 #pragma unroll
               for (int k = 0; k < NACC; ++k)
-                if (k < p.K) acc[k] += dev::lds_f32(lb + 4u * k);
+                if (k < p.K) acc[k] += (double)dev::lds_f32(lb + 4u * k);
             }
           }
           if (NACC > 1 && p.w == 1) {
@@ -299,41 +282,40 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
 
 using PttrFn = void (*)(const PttrParams);
 
-template <int CW, int D, bool LE, bool TOP>
+template <int CW, int D, bool LE>
 static PttrFn pttr_pick_nacc(int nacc) {
   switch (nacc) {
-    case 1: return pttr_kernel<D, LE, 1, kTreeGroup, CW, TOP>;
-    case 4: return pttr_kernel<D, LE, 4, kTreeGroup, CW, TOP>;
-    case 8: return pttr_kernel<D, LE, 8, kTreeGroup, CW, TOP>;
-    default: return pttr_kernel<D, LE, 16, kTreeGroup, CW, TOP>;
+    case 1: return pttr_kernel<D, LE, 1, kTreeGroup, CW>;
+    case 4: return pttr_kernel<D, LE, 4, kTreeGroup, CW>;
+    case 8: return pttr_kernel<D, LE, 8, kTreeGroup, CW>;
+    default: return pttr_kernel<D, LE, 16, kTreeGroup, CW>;
   }
 }
 
-template <int CW, int D, bool TOP>
+template <int CW, int D>
 static PttrFn pttr_pick_le(bool le, int nacc) {
-  return le ? pttr_pick_nacc<CW, D, true, TOP>(nacc) : pttr_pick_nacc<CW, D, false, TOP>(nacc);
+  return le ? pttr_pick_nacc<CW, D, true>(nacc) : pttr_pick_nacc<CW, D, false>(nacc);
 }
 
-template <int CW, bool TOP = false>
+template <int CW>
 static PttrFn pttr_pick(int D, bool le, int nacc) {
   switch (D) {
-    case 0: return pttr_pick_le<CW, 0, TOP>(le, nacc);
-    case 1: return pttr_pick_le<CW, 1, TOP>(le, nacc);
-    case 2: return pttr_pick_le<CW, 2, TOP>(le, nacc);
-    case 3: return pttr_pick_le<CW, 3, TOP>(le, nacc);
-    case 4: return pttr_pick_le<CW, 4, TOP>(le, nacc);
-    case 5: return pttr_pick_le<CW, 5, TOP>(le, nacc);
-    case 6: return pttr_pick_le<CW, 6, TOP>(le, nacc);
-    case 7: return pttr_pick_le<CW, 7, TOP>(le, nacc);
-    case 8: return pttr_pick_le<CW, 8, TOP>(le, nacc);
-    case 9: return pttr_pick_le<CW, 9, TOP>(le, nacc);
-    case 10: return pttr_pick_le<CW, 10, TOP>(le, nacc);
+    case 0: return pttr_pick_le<CW, 0>(le, nacc);
+    case 1: return pttr_pick_le<CW, 1>(le, nacc);
+    case 2: return pttr_pick_le<CW, 2>(le, nacc);
+    case 3: return pttr_pick_le<CW, 3>(le, nacc);
+    case 4: return pttr_pick_le<CW, 4>(le, nacc);
+    case 5: return pttr_pick_le<CW, 5>(le, nacc);
+    case 6: return pttr_pick_le<CW, 6>(le, nacc);
+    case 7: return pttr_pick_le<CW, 7>(le, nacc);
+    case 8: return pttr_pick_le<CW, 8>(le, nacc);
+    case 9: return pttr_pick_le<CW, 9>(le, nacc);
+    case 10: return pttr_pick_le<CW, 10>(le, nacc);
     default: return nullptr;
   }
 }
 
 PttrFn pttr_fn32(int D, bool le, int nacc);
 PttrFn pttr_fn16(int D, bool le, int nacc);
-PttrFn pttr_fn32_top(int D, bool le, int nacc);
 
 }  // namespace hb

@@ -26,8 +26,9 @@
 //   rank_code_staged_kernel  X columns staged with cp.async, for narrow groups
 //                            (C3, C4) or tables searched from global memory.
 // Both run the searches of a batch in lockstep (rank_codes_lockstep) and use
-// a group-major grid with contiguous row slices. The cluster variant (all
-// tables in one cluster's DSMEM) is in hb_rank_codes_cluster.cu.
+// a group-major grid with contiguous row slices. (A cluster variant holding
+// all tables in one cluster's DSMEM was measured slower and removed, DESIGN.md
+// §4.6.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -528,10 +529,6 @@ int sm_count(int device);
 
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks) {
   if (m.rb_ngroups == 0 || nblocks == 0) return HB_OK;   // no split uses any feature: no codes
-  // the cluster kernel when the model has a cluster plan (all tables in one
-  // cluster's SMEM) and no per-group kernel is forced (HB_RC_STAGED=0/1)
-  const char *force = std::getenv("HB_RC_STAGED");
-  if (m.rbc_cl > 0 && !(force && *force && std::atoi(force) >= 0)) return launch_rank_codes_cluster(m, a, codes, nblocks);
   RankCodeParams p;
   p.X = a.X;
   p.n = a.n;

@@ -62,17 +62,17 @@ template <bool LE, int NACC>
 __global__ void __launch_bounds__(256) small_batch_kernel(const SbParams p) {
   extern __shared__ __align__(16) float sb_smem[];
   float *xs = sb_smem;                              // [F]
-  float *red = xs + ((p.F + 3) & ~3);               // [8 warps][NACC]
-  uint64_t *hred = reinterpret_cast<uint64_t *>(red + 8 * NACC);   // [8]
+  double *red = reinterpret_cast<double *>(xs + ((p.F + 3) & ~3));   // [8 warps][NACC]
+  uint64_t *hred = reinterpret_cast<uint64_t *>(red + 8 * NACC);     // [8]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
     for (int f = threadIdx.x; f < p.F; f += blockDim.x)
       xs[f] = __ldg(p.X + row * p.ldx + (p.fmap ? __ldg(p.fmap + f) : f));
     __syncthreads();
-    float acc[NACC];
+    double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
     for (int t = threadIdx.x; t < p.n_rec; t += blockDim.x) {
       const uint8_t *rec = p.trees + (size_t)t * p.stride;
@@ -95,14 +95,14 @@ __global__ void __launch_bounds__(256) small_batch_kernel(const SbParams p) {
         kout = hdr & 0xFFu;
       }
       if (p.w == 1) {
-        const float v = __ldg(leaf + slot);
+        const double v = (double)__ldg(leaf + slot);
 #pragma unroll
         for (int k = 0; k < NACC; ++k)
           if (kout == (uint32_t)k) acc[k] += v;
       } else {
 #pragma unroll
         for (int k = 0; k < NACC; ++k)
-          if (k < p.K) acc[k] += __ldg(leaf + slot * p.w + k);
+          if (k < p.K) acc[k] += (double)__ldg(leaf + slot * p.w + k);
       }
       if (lm) {
         const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + slot);
@@ -124,9 +124,9 @@ __global__ void __launch_bounds__(256) small_batch_kernel(const SbParams p) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      float tot[NACC];
+      double tot[NACC];
 #pragma unroll
-      for (int k = 0; k < NACC; ++k) tot[k] = 0.f;
+      for (int k = 0; k < NACC; ++k) tot[k] = 0.0;
       uint64_t ht = 0;
       for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
 #pragma unroll
@@ -179,7 +179,7 @@ hb_status launch_small_batch(const Model &m, const RunArgs &a) {
   p.kind = a.kind;
   p.out = a.out;
   const int threads = 256;
-  const size_t smem = (size_t)((m.sb_nxf + 3) & ~3) * 4 + 8 * 16 * 4 + 8 * 8;
+  const size_t smem = (size_t)((m.sb_nxf + 3) & ~3) * 4 + 8 * 16 * 8 + 8 * 8;
   if (smem > (size_t)kSmemBudget) return fail(HB_E_UNSUPPORTED, "small-batch path: row too wide");
   const int64_t grid = std::min<int64_t>(a.n, (int64_t)sm_count(m.device) * 16);
   SbFn fn = m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc);

@@ -35,21 +35,11 @@ struct TtParams {
   void *out;
   int nw, ns, ch, ntiles, x_smem, t_smem;
   int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
-  int top_prefetch;       // tt_wide_kernel: L1 prefetch of the next tree group's top levels
-  int cursor;             // tt_wide_kernel: per-lane tree cursors instead of warp-synchronous groups
-  int node_off;           // byte offset of the node array in a record (16 BFS; 24 pair-aligned BFS)
-  int lookahead;          // tt_wide_kernel over pair-aligned BFS records: load both children
-                          // of the current node (one 16-B load) while its X value is read
   // tt_wide_kernel over one tree chunk of a model larger than L2 (launch_tt):
-  int accumulate;         // RAW / LEAF_HASH outputs are added to, not written
+  int accumulate;         // RAW64 / LEAF_HASH outputs are added to, not written
   int leaf_stride;        // LEAF output row stride (the model's tree count)
   int tree_off;           // first model-local tree of this chunk (LEAF column)
 };
-
-// node array offset inside a record: 16 B (BFS layout), 32 B (sector layout:
-// 32-B aligned so a root and its children share one L2 sector)
-template <bool SEC>
-constexpr int node_off() { return SEC ? 32 : 16; }
 
 template <bool LE>
 __device__ __forceinline__ uint32_t tt_walk(const uint2 *nodes, const float *xrow, int xstride,
@@ -123,9 +113,9 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
       xrow = p.X + (row < p.n ? row : 0) * p.ldx;
       xstride = 1;
     }
-    float acc[NACC];
+    double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
     for (int c = 0; c < nchunks; ++c) {
       const uint8_t *cb;
@@ -148,7 +138,7 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
         const float *la = reinterpret_cast<const float *>(na + p.nslots);
         const float *lb = reinterpret_cast<const float *>(nb + p.nslots);
         if (p.w == 1) {
-          const float va = la[ia], vb = lb[ib];
+          const double va = (double)la[ia], vb = (double)lb[ib];
           if (NACC == 1) {
             acc[0] += va;
             acc[0] += vb;
@@ -164,10 +154,10 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
         } else {
 #pragma unroll
           for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += la[ia * p.w + k];
+            if (k < p.K) acc[k] += (double)la[ia * p.w + k];
 #pragma unroll
           for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += lb[ib * p.w + k];
+            if (k < p.K) acc[k] += (double)lb[ib * p.w + k];
         }
         if (lm) {
           const int tg = c * ch + j;
@@ -205,7 +195,7 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // feature-major (xs[f*R + r]); lane = (tree slot, row) with 32/R tree slots per
 // warp, and all warps of the CTA walk disjoint trees of the same R rows. Node
 // records come through L1/L2 (__ldg): the top levels of a tree are shared by
-// the R rows and hit L1. Each lane walks two trees at once (memory-level
+// the R rows and hit L1. Each lane walks G trees at once (memory-level
 // parallelism) and the walk stops early once every lane of the warp sits on a
 // leaf (the self-loop makes further iterations no-ops). Per-row sums
 // are combined with warp shuffles and one SMEM pass in a fixed order.
@@ -214,37 +204,33 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // lanes of different tree slots on the same row can meet (<= 32/R-way). The
 // fill gives the 32/R row groups of a warp different 4-feature chunks and
 // rotates their store order so a warp's 32 stores hit 32 distinct banks.
-// (The previous XOR swizzle made the tile fill's stores conflict-free only for
-// scalar stores of consecutive features and cost 2.4 wavefronts per read.)
 
-template <bool LE, int R, bool SEC>
+template <bool LE, int R>
 __device__ __forceinline__ void wide_step(const uint2 *n, uint32_t &i, const float *xs, int r,
                                           bool &done) {
   const uint2 d = __ldg(n + i);
-  const int f = (int)(d.x & (SEC ? 0x7FFFu : 0xFFFFu));
+  const int f = (int)(d.x & 0xFFFFu);
   const float x = xs[f * R + r];
   const float t = __uint_as_float(d.y);
   const bool pr = LE ? (x <= t) : (x < t);
-  // left child = N_R - 1 (BFS; sector roots) or N_R - 4 (sector layout, flag bit 15)
-  const uint32_t dl = SEC ? ((d.x & 0x8000u) ? 4u : 1u) : 1u;
-  const uint32_t nx = (d.x >> 16) - (pr ? dl : 0u);
+  const uint32_t nx = (d.x >> 16) - (pr ? 1u : 0u);   // left child = N_R - 1 (BFS, siblings adjacent)
   done = done && (nx == i);
   i = nx;
 }
 
-template <bool LE, int NACC, int R, int G, bool SEC> // G: trees walked at once per lane; SEC: sector layout
+template <bool LE, int NACC, int R, int G>   // G: trees walked at once per lane
 __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int L = 32 / R;                       // tree slots per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int sub = lane / R, r = lane % R;
-  float *xs = reinterpret_cast<float *>(smem);                       // [F][R] swizzled
-  float *red = xs + (size_t)p.F * R;                                 // [nwarps][R][NACC]
-  uint64_t *hred = reinterpret_cast<uint64_t *>(red + (size_t)nwarps * R * NACC);  // [nwarps][R]
+  float *xs = reinterpret_cast<float *>(smem);                       // [F][R]
+  double *red = reinterpret_cast<double *>(xs + (((size_t)p.F * R + 1) & ~(size_t)1));  // [nwarps][R][NACC]
+  uint64_t *hred = reinterpret_cast<uint64_t *>(red + (size_t)nwarps * R * NACC);       // [nwarps][R]
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   const int slots = nwarps * L;
-  const int noff = SEC ? node_off<true>() : p.node_off;
+  constexpr int noff = 16;                        // node array offset in a record
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row0 = (int64_t)tile * R;
     // X tile load: lane = (row group sub, row rr); each lane loads one
@@ -289,15 +275,15 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       dev::prefetch_rows_l2(p.X, (int64_t)(tile + gridDim.x) * R, R, p.n, p.ldx);
     __syncthreads();
     const int64_t row = row0 + r;
-    float acc[NACC];
+    double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
     // leaf of tree t reached (record rc, slot leaf): add its value / emit its id
     auto finish = [&](int t, const uint8_t *rc, uint32_t leaf) {
       const float *lv = reinterpret_cast<const float *>(rc + noff + (size_t)8 * p.nslots);
       if (p.w == 1) {
-        const float v = __ldg(lv + leaf);
+        const double v = (double)__ldg(lv + leaf);
         if (NACC == 1) {
           acc[0] += v;
         } else {
@@ -309,7 +295,7 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       } else {
 #pragma unroll
         for (int k = 0; k < NACC; ++k)
-          if (k < p.K) acc[k] += __ldg(lv + leaf * p.w + k);
+          if (k < p.K) acc[k] += (double)__ldg(lv + leaf * p.w + k);
       }
       if (lm && t < p.n_trees) {
         const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
@@ -320,42 +306,6 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         }
       }
     };
-    if (p.cursor) {
-      // per-lane cursors: each of a lane's G walks moves on to its next tree
-      // (t += G * slots) as soon as it sits on a leaf, so a lane never idles
-      // on a finished walk while the warp's slowest path completes; the warp
-      // leaves the loop when every lane has run out of trees
-      const int tstep = G * slots;
-      int t[G];
-      uint32_t ix[G];
-      const uint8_t *rc[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        t[g] = warp * L + sub + g * slots;
-        ix[g] = 0;
-        rc[g] = p.trees + (size_t)min(t[g], p.n_trees_pad - 1) * p.stride;
-      }
-      while (true) {
-        bool act = false;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          if (t[g] < p.n_trees_pad) {
-            act = true;
-            bool dn = true;
-            uint32_t i = ix[g];
-            wide_step<LE, R, SEC>(reinterpret_cast<const uint2 *>(rc[g] + noff), i, xs, r, dn);
-            if (dn) {
-              finish(t[g], rc[g], i);
-              t[g] += tstep;
-              i = 0;
-              rc[g] = p.trees + (size_t)min(t[g], p.n_trees_pad - 1) * p.stride;
-            }
-            ix[g] = i;
-          }
-        }
-        if (!__any_sync(0xFFFFFFFFu, act)) break;
-      }
-    } else {
     // warp-uniform loop over groups of G tree slots (t = base + sub + g*slots)
     for (int base = warp * L; base < p.n_trees_pad; base += G * slots) {
       const uint8_t *rec[G];
@@ -370,60 +320,15 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         nd[g] = reinterpret_cast<const uint2 *>(rec[g] + noff);
         idx[g] = 0;
       }
-      if (p.top_prefetch && r < 2) {
-        // warm L1 with the top levels (first two 128-B lines of the node
-        // array) of this lane's trees in the NEXT group: their first walk
-        // step would otherwise be an L2 round trip per group
+      for (int l = 0; l < p.depth; ++l) {
+        bool done = true;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const int t = base + G * slots + sub + g * slots;
-          if (t < p.n_trees_pad) {
-            const uint8_t *q = p.trees + (size_t)t * p.stride + noff + 128 * r;
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
-          }
-        }
-      }
-      if (!SEC && p.lookahead) {
-        // pair-aligned BFS records: siblings (R-1, R) share one 16-B word, so
-        // the next record is fetched (both candidates) as soon as the current
-        // one is known, in parallel with the X read and the compare. A leaf's
-        // self loop reads the aligned pair holding it ((R-1) | 1 = R).
-        uint2 dc[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) dc[g] = __ldg(nd[g]);
-        for (int l = 0; l < p.depth; ++l) {
-          bool done = true;
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t rr = dc[g].x >> 16;
-            // a leaf at slot 0 (single-leaf or padding tree) has no pair below
-            // it: load any valid pair, the self loop keeps the record
-            const uint32_t pb = rr == 0 ? 1u : ((rr - 1u) | 1u);
-            const uint4 c = __ldg(reinterpret_cast<const uint4 *>(nd[g] + pb));
-            const int f = (int)(dc[g].x & 0xFFFFu);
-            const float x = xs[f * R + r];
-            const float t = __uint_as_float(dc[g].y);
-            const bool pr = LE ? (x <= t) : (x < t);
-            const uint32_t nx = rr - (pr ? 1u : 0u);
-            const bool same = nx == idx[g];      // leaf: self loop, record unchanged
-            done = done && same;
-            idx[g] = nx;
-            if (!same) dc[g] = nx == pb ? make_uint2(c.x, c.y) : make_uint2(c.z, c.w);
-          }
-          if (__all_sync(0xFFFFFFFFu, done)) break;
-        }
-      } else {
-        for (int l = 0; l < p.depth; ++l) {
-          bool done = true;
-#pragma unroll
-          for (int g = 0; g < G; ++g) wide_step<LE, R, SEC>(nd[g], idx[g], xs, r, done);
-          if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
-        }
+        for (int g = 0; g < G; ++g) wide_step<LE, R>(nd[g], idx[g], xs, r, done);
+        if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
       }
 #pragma unroll
       for (int g = 0; g < G; ++g)
         if (valid[g]) finish(base + sub + g * slots, rec[g], idx[g]);
-    }
     }
     // combine the L tree slots of a row inside the warp, then across warps
 #pragma unroll
@@ -439,9 +344,9 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
     }
     __syncthreads();
     if (warp == 0 && lane < R) {
-      float tot[NACC];
+      double tot[NACC];
 #pragma unroll
-      for (int k = 0; k < NACC; ++k) tot[k] = 0.f;
+      for (int k = 0; k < NACC; ++k) tot[k] = 0.0;
       uint64_t ht = 0;
       for (int w2 = 0; w2 < nwarps; ++w2) {
 #pragma unroll
@@ -453,10 +358,10 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         if (lm == 2) {
           uint64_t *o = static_cast<uint64_t *>(p.out) + orow;
           *o = p.accumulate ? *o + ht : ht;
-        } else if (lm == 0 && p.accumulate) {      // RAW partial of a later tree chunk
+        } else if (lm == 0 && p.accumulate) {      // fp64 RAW partial of a later tree chunk
 #pragma unroll
           for (int k = 0; k < NACC; ++k)
-            if (k < p.K) static_cast<float *>(p.out)[orow * p.K + k] += tot[k];
+            if (k < p.K) static_cast<double *>(p.out)[orow * p.K + k] += tot[k];
         } else if (lm == 0) {
           dev::write_row<NACC>(p.kind, tot, p.K, p.task, p.post, p.scale, p.base, orow, p.out);
         }
@@ -480,43 +385,34 @@ static TtFn pick_nacc(int nacc) {
 
 int sm_count(int device);
 
-template <bool LE, int R, bool SEC>
-static TtFn pick_wide_nacc(int nacc, int g) {
-  // 6 or 8 concurrent walks per lane only for scalar outputs (register budget)
-  if (nacc == 1 && g >= 8) return tt_wide_kernel<LE, 1, R, 8, SEC>;
-  if (nacc == 1 && g >= 6) return tt_wide_kernel<LE, 1, R, 6, SEC>;
+template <bool LE, int R>
+static TtFn pick_wide_nacc(int nacc) {
   switch (nacc) {
-    case 1: return tt_wide_kernel<LE, 1, R, 4, SEC>;
-    case 4: return tt_wide_kernel<LE, 4, R, 4, SEC>;
-    case 8: return tt_wide_kernel<LE, 8, R, 4, SEC>;
-    default: return tt_wide_kernel<LE, 16, R, 4, SEC>;
-  }
-}
-
-template <bool LE, bool SEC>
-static TtFn pick_wide_r(int R, int nacc, int g) {
-  switch (R) {
-    case 32: return pick_wide_nacc<LE, 32, SEC>(nacc, g);
-    case 16: return pick_wide_nacc<LE, 16, SEC>(nacc, g);
-    default: return pick_wide_nacc<LE, 8, SEC>(nacc, g);
+    case 1: return tt_wide_kernel<LE, 1, R, 4>;
+    case 4: return tt_wide_kernel<LE, 4, R, 4>;
+    case 8: return tt_wide_kernel<LE, 8, R, 4>;
+    default: return tt_wide_kernel<LE, 16, R, 4>;
   }
 }
 
 template <bool LE>
-static TtFn pick_wide(int R, int nacc, int g, bool sec) {
-  return sec ? pick_wide_r<LE, true>(R, nacc, g) : pick_wide_r<LE, false>(R, nacc, g);
+static TtFn pick_wide(int R, int nacc) {
+  switch (R) {
+    case 32: return pick_wide_nacc<LE, 32>(nacc);
+    case 16: return pick_wide_nacc<LE, 16>(nacc);
+    default: return pick_wide_nacc<LE, 8>(nacc);
+  }
+}
+
+// SMEM of tt_wide_kernel for R rows: X tile + fp64 per-warp row sums + hashes
+size_t tt_wide_smem(int F, int R, int nwarps, int nacc) {
+  return ((((size_t)F * R + 1) & ~(size_t)1) * 4) + (size_t)nwarps * R * (8 * (size_t)nacc + 8);
 }
 
 hb_status launch_tt(const Model &m, const RunArgs &a) {
-  if (m.tt_blocks) return launch_tt_blocks(m, a);
-  if (m.tt_cluster) {
-    const hb_status st = launch_tt_cluster(m, a);
-    if (st != HB_E_UNSUPPORTED) return st;   // unaligned rows: tt_wide_kernel below
-  }
   const bool wide = m.cfg.wide_rows > 0;
-  const bool sec = wide && m.tt_sector;
-  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g, sec)
-                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g, sec))
+  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc)
+                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc))
                  : (m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc));
   TtParams p;
   p.X = a.X;
@@ -526,16 +422,13 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.fmap = m.d_fmap;
   p.vec4 = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && (a.ldx % 4 == 0);
   p.depth = m.depth;
-  const bool pair = wide && !sec && m.tt_pair;
-  p.trees = static_cast<const uint8_t *>(sec || pair ? m.d_ttw : m.d_trees);
-  p.stride = (uint32_t)(sec || pair ? m.ttw_stride : m.stride);
-  p.node_off = pair ? 24 : 16;
-  p.lookahead = pair ? 1 : 0;
+  p.trees = static_cast<const uint8_t *>(m.d_trees);
+  p.stride = (uint32_t)m.stride;
   p.n_trees_pad = m.n_trees_pad;
   p.n_trees = m.n_trees;
   p.tree_begin = m.tree_begin;
-  p.leafmap = sec ? m.d_ttw_leafmap : m.d_leafmap;
-  p.nslots = sec ? m.ttw_nslots : m.nslots;
+  p.leafmap = m.d_leafmap;
+  p.nslots = m.nslots;
   p.scale = m.d_scale;
   p.base = m.d_base;
   p.K = m.n_outputs;
@@ -550,8 +443,6 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.x_smem = m.cfg.x_smem;
   p.t_smem = m.cfg.t_smem;
   p.x_prefetch = m.cfg.prefetch;
-  p.top_prefetch = m.tt_top_prefetch;
-  p.cursor = m.tt_cursor;
   p.accumulate = 0;
   p.leaf_stride = m.n_trees;
   p.tree_off = 0;
@@ -564,7 +455,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
                                        m.cfg.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tt)");
   const int threads = wide ? 32 * m.cfg.nw : 32 * (m.cfg.nw + 1);
-  if (!(wide && !sec && !pair && m.tt_chunk > 0 && m.n_trees_pad > m.tt_chunk)) {
+  if (!(wide && m.tt_chunk > 0 && m.n_trees_pad > m.tt_chunk)) {
     fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tt_kernel launch");
@@ -572,13 +463,15 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   }
   // model larger than L2: walk it in L2-resident tree chunks (every chunk
   // re-streams X from HBM, sequentially, instead of fetching deep node
-  // records from HBM at random); RAW / LEAF_HASH partials accumulate in the
-  // output, PREDICT / PROBA / MARGIN go through a raw scratch + finalize
-  const bool fin = a.kind == HB_OUT_PREDICT || a.kind == HB_OUT_PROBA || a.kind == HB_OUT_MARGIN;
-  float *raw = nullptr;
-  if (fin) {
-    e = cudaMallocAsync(reinterpret_cast<void **>(&raw), (size_t)a.n * m.n_outputs * sizeof(float), a.stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(tt chunk partials)");
+  // records from HBM at random). fp64 RAW partials accumulate in a scratch
+  // buffer from the model's pool (RAW64 / LEAF_HASH: in the output itself),
+  // and one finalize launch writes PREDICT / PROBA / MARGIN / RAW.
+  const bool direct = a.kind == HB_OUT_RAW64 || a.kind == HB_OUT_LEAF_HASH || a.kind == HB_OUT_LEAF;
+  double *raw = nullptr;
+  if (!direct) {
+    const hb_status st = scratch_alloc(m, (size_t)a.n * m.n_outputs * sizeof(double), a.stream,
+                                       reinterpret_cast<void **>(&raw));
+    if (st != HB_OK) return st;
   }
   for (int t0 = 0; t0 < m.n_trees_pad; t0 += m.tt_chunk) {
     TtParams pc = p;
@@ -588,8 +481,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
     pc.tree_begin = m.tree_begin + t0;
     pc.leafmap = p.leafmap + (size_t)t0 * p.nslots;
     pc.tree_off = t0;
-    pc.kind = fin ? HB_OUT_RAW : a.kind;
-    pc.out = fin ? static_cast<void *>(raw) : a.out;
+    pc.kind = direct ? a.kind : HB_OUT_RAW64;
+    pc.out = direct ? a.out : static_cast<void *>(raw);
     pc.accumulate = t0 > 0 && pc.kind != HB_OUT_LEAF;
     fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(pc);
     e = cudaGetLastError();
@@ -598,9 +491,10 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
       return cuda_fail(e, "tt_wide_kernel launch (tree chunk)");
     }
   }
-  if (fin) {
+  if (!direct) {
     RunArgs f = a;
-    f.raw_in = raw;
+    f.raw_in = nullptr;
+    f.raw_in64 = raw;
     const hb_status st = launch_finalize(m, f);
     cudaFreeAsync(raw, a.stream);
     if (st != HB_OK) return st;

@@ -3,10 +3,12 @@
 * Row sharding: rows are independent, so rank r scores a contiguous block of
   rows with a full model replica — no collective on the data path.
 * Tree sharding (very large ensembles, e.g. C5): trees are additive, so rank r
-  compiles a contiguous tree range (hb_compile_range), computes fp32 raw
-  partial sums (hb_predict_raw), ONE reduce(SUM) brings them to the root
-  (NCCL over NVLink with backend "nccl"), and the root runs hb_finalize with the
-  global per-output tree counts and base score.
+  compiles a contiguous tree range (hb_compile_range), computes fp64 raw
+  partial sums (HB_OUT_RAW64: the scorers accumulate in fp64), ONE
+  reduce(SUM) in fp64 brings them to the root (NCCL over NVLink with backend
+  "nccl"), and the root runs hb_finalize64 with the global per-output tree
+  counts and base score — no fp32 rounding before the margin is formed
+  (R23).
 
 The paper itself is single-GPU ("distributed inference is future work",
 PAPER.md P:129); this is the natural extension of its batch (row) and ensemble
@@ -73,7 +75,7 @@ class TreeShardedModel:
         self.rank, self.world, self.root = rank, world, root
 
     def predict(self, X, kind="proba", group=None):
-        raw = self.model.predict_raw(X)
+        raw = self.model.predict_raw64(X)
         if self.world > 1:
             reduce_partials(raw, dst=self.root, group=group)
         if self.rank != self.root:

@@ -16,14 +16,13 @@ TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
 STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
 KERNEL_NAME = {0: "ptt_kernel", 1: "pttr_kernel", 2: "tt_kernel", 3: "tt_wide_kernel",
-               4: "gemm_tc_kernel", 5: "gemm_kernel", 6: "tt_cluster_kernel",
-               7: "ttb_kernel"}
-OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5}
+               4: "gemm_tc_kernel", 5: "gemm_kernel"}
+OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5, "raw64": 6}
 
 # every symbol include/hb.h declares (checked by tests/test_abi.py)
 exported_symbols = ["hb_validate", "hb_compile", "hb_compile_range", "hb_predict_ex",
                     "hb_predict", "hb_predict_proba", "hb_predict_raw", "hb_predict_leaf",
-                    "hb_finalize", "hb_predict_host", "hb_model_get_info", "hb_free",
+                    "hb_finalize", "hb_finalize64", "hb_predict_host", "hb_model_get_info", "hb_free",
                     "hb_last_error", "hb_abi_version"]
 
 
@@ -52,7 +51,8 @@ class _Info(C.Structure):
                 ("tensor_cores", C.c_int32), ("node_record_bytes", C.c_int32),
                 ("kernel", C.c_int32), ("rows_per_cta", C.c_int32),
                 ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32),
-                ("tt_sector", C.c_int32), ("tt_chunk_trees", C.c_int32)]
+                ("tt_sector", C.c_int32), ("tt_chunk_trees", C.c_int32),
+                ("small_batch_max_rows", C.c_int32)]
 
 
 def _load():
@@ -72,6 +72,7 @@ def _load():
         "hb_predict_raw": ([vp, vp, i64, i64, vp, vp], C.c_int),
         "hb_predict_leaf": ([vp, vp, i64, i64, vp, vp], C.c_int),
         "hb_finalize": ([vp, vp, i64, i32, vp, vp], C.c_int),
+        "hb_finalize64": ([vp, vp, i64, i32, vp, vp], C.c_int),
         "hb_predict_host": ([vp, vp, i64, i64, i32, vp], C.c_int),
         "hb_model_get_info": ([vp, C.POINTER(_Info)], C.c_int),
         "hb_free": ([vp], None),
@@ -145,6 +146,14 @@ class Model:
         d["kernel_name"] = KERNEL_NAME.get(d["kernel"], "?")
         return d
 
+    def kernel_for(self, n_rows):
+        """Name of the scoring kernel a call with n_rows rows launches: the
+        small-batch (trees-across-threads) kernel up to small_batch_max_rows,
+        else the model's row-tile scorer."""
+        if n_rows <= self.info["small_batch_max_rows"]:
+            return "small_batch_kernel"
+        return self.info["kernel_name"]
+
     def free(self):
         if getattr(self, "_p", None):
             lib.hb_free(self._p)
@@ -165,11 +174,29 @@ class Model:
             return ((n, 2 if K == 1 else K), "float32")
         if kind in ("raw", "margin"):
             return ((n, K), "float32")
+        if kind == "raw64":
+            return ((n, K), "float64")
         if kind == "leaf":
             return ((n, self.info["n_trees"]), "int32")
         if kind == "leaf_hash":
             return ((n,), "int64")
         raise ValueError(kind)
+
+    def _out(self, n, kind, out, device):
+        """Allocate `out`, or check a caller-supplied one: the C ABI cannot see
+        a buffer's length, so a wrong shape/dtype/device would be an
+        out-of-bounds device write."""
+        import torch
+        shape, dt = self.out_shape(n, kind)
+        want = getattr(torch, dt)
+        if out is None:
+            return torch.empty(shape, dtype=want, device=device)
+        if not isinstance(out, torch.Tensor) or tuple(out.shape) != tuple(shape) or out.dtype != want \
+                or not out.is_contiguous() or out.device != torch.device(device):
+            raise ValueError(f"out must be a contiguous {dt} tensor of shape {shape} on {device}, got "
+                             f"{getattr(out, 'dtype', type(out))} {tuple(getattr(out, 'shape', ()))} "
+                             f"on {getattr(out, 'device', '?')}")
+        return out
 
     def run(self, X, kind="predict", out=None, stream=None):
         """One fused scoring launch (hb_predict_ex; two with the rank-code pre-pass) on torch CUDA tensors.
@@ -178,9 +205,7 @@ class Model:
         if X.dtype != torch.float32 or X.dim() != 2 or X.stride(1) != 1:
             raise ValueError("X must be a 2-D float32 tensor with unit column stride")
         n = X.shape[0]
-        shape, dt = self.out_shape(n, kind)
-        if out is None:
-            out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
+        out = self._out(n, kind, out, X.device)
         st = torch.cuda.current_stream(self.device) if stream is None else stream
         _check(lib.hb_predict_ex(self._p, C.c_void_p(X.data_ptr()), n, X.stride(0), OUT[kind],
                                  C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
@@ -195,6 +220,9 @@ class Model:
     def predict_raw(self, X, **kw):
         return self.run(X, "raw", **kw)
 
+    def predict_raw64(self, X, **kw):
+        return self.run(X, "raw64", **kw)
+
     def predict_margin(self, X, **kw):
         return self.run(X, "margin", **kw)
 
@@ -205,15 +233,19 @@ class Model:
         return self.run(X, "leaf_hash", **kw)
 
     def finalize(self, raw, kind="predict", out=None, stream=None):
-        """hb_finalize: epilogue from device raw sums over all trees."""
+        """hb_finalize (float32 raw) / hb_finalize64 (float64 raw): epilogue
+        from device raw sums over all trees, shape (n, K)."""
         import torch
+        K = self.info["n_outputs"]
+        if raw.dtype not in (torch.float32, torch.float64) or raw.dim() != 2 or raw.shape[1] != K \
+                or not raw.is_contiguous():
+            raise ValueError(f"raw must be a contiguous float32/float64 tensor of shape (n, {K})")
         n = raw.shape[0]
-        shape, dt = self.out_shape(n, kind)
-        if out is None:
-            out = torch.empty(shape, dtype=getattr(torch, dt), device=raw.device)
+        out = self._out(n, kind, out, raw.device)
         st = torch.cuda.current_stream(self.device) if stream is None else stream
-        _check(lib.hb_finalize(self._p, C.c_void_p(raw.data_ptr()), n, OUT[kind],
-                               C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
+        fn = lib.hb_finalize64 if raw.dtype == torch.float64 else lib.hb_finalize
+        _check(fn(self._p, C.c_void_p(raw.data_ptr()), n, OUT[kind],
+                  C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
         return out
 
     # ------------------------------------------------------------ host API

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "hb.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(hb_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(hb_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     missing = [s for s in declared if s not in exported]
     assert not missing, missing
     assert sorted(hb.exported_symbols) == declared
-    assert hb.lib.hb_abi_version() == 3
+    assert hb.lib.hb_abi_version() == 4
 
 
 def test_sm100a_cubin_embedded():

@@ -32,20 +32,8 @@ cases = [
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_STAGED": "1", "HB_RC_RB": "1"}, "ptt"),
     ("ptt-rank-prepass-rows8", synth.gen_forest(40, 6, 12, seed=1),
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "0", "HB_RC_ROWS": "8"}, "ptt"),
-    ("tt-wide-sector", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
-     {"HB_TT_WIDE": "1", "HB_TT_SECTOR": "1"}, "tt"),
     ("tt-wide-chunks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
      {"HB_TT_WIDE": "1", "HB_TT_CHUNK": "8"}, "tt"),
-    ("tt-wide-pair", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
-     {"HB_TT_WIDE": "1", "HB_TT_PAIR": "1"}, "tt"),
-    ("ptt-rank-prepass-cluster-16", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_CLUSTER": "1"}, "ptt"),
-    ("tt-blocks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
-     {"HB_TT_WIDE": "1", "HB_TT_BLOCK": "1"}, "tt"),
-    ("ptt-rank-top-wrap", synth.gen_forest(300, 8, 12, seed=4),
-     {"HB_PTT_RANK": "1", "HB_RANK_CW": "32", "HB_PTTR_TOP": "1", "HB_CH": "8"}, "ptt"),
-    ("ptt-rank-pre-top", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_PTTR_TOP": "1"}, "ptt"),
     ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
     ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
 ]
