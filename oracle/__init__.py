@@ -58,6 +58,8 @@ def _L():
         _lib.oracle_leaf_hash.argtypes = [P, vp, i64, i64, i32, i32, vp]
         _lib.oracle_raw_mt.argtypes = [P, vp, i64, i64, i32, i32, vp, C.c_int]
         _lib.oracle_raw_mt.restype = C.c_int
+        _lib.oracle_raw_hash_mt.argtypes = [P, vp, i64, i64, i32, i32, vp, vp, C.c_int]
+        _lib.oracle_raw_hash_mt.restype = C.c_int
         _lib.oracle_predict_mt.argtypes = [P, vp, i64, i64, vp, C.c_int]
         _lib.oracle_predict_mt.restype = C.c_int
     return _lib
@@ -149,6 +151,20 @@ def leaf_hash(e, X, t0=0, t1=None):
     out = np.empty(X.shape[0], np.uint64)
     _L().oracle_leaf_hash(C.byref(h.s), X.ctypes.data, X.shape[0], ldx, t0, t1, out.ctypes.data)
     return out
+
+
+def raw_and_hash(e, X, t0=0, t1=None, threads=0):
+    """(raw fp64 [n, K], leaf hash uint64 [n]) over trees [t0, t1) with one
+    walk per (row, tree) on `threads` pthreads (0: all cores) — the same values
+    as raw() and leaf_hash(); for every-row parity at full size."""
+    h = _Handle(e)
+    t1 = h.T if t1 is None else t1
+    X, ldx = _X(X)
+    out = np.empty((X.shape[0], h.K), np.float64)
+    hs = np.empty(X.shape[0], np.uint64)
+    _L().oracle_raw_hash_mt(C.byref(h.s), X.ctypes.data, X.shape[0], ldx, t0, t1,
+                            out.ctypes.data, hs.ctypes.data, threads)
+    return out, hs
 
 
 def scores(e, X, threads=1):

@@ -183,6 +183,61 @@ int oracle_raw_mt(const oracle_ensemble *e, const float *X, int64_t n, int64_t l
   return nthreads;
 }
 
+/* raw sums and leaf hashes of rows [r0, r1) in one walk per (row, tree):
+ * exactly raw_rows() and oracle_leaf_hash() above, fused so the full-size
+ * parity checks (every row of C3 / the C5 shard) walk each pair once. */
+static void raw_hash_rows(const oracle_ensemble *e, const float *X, int64_t r0, int64_t r1,
+                          int64_t ldx, int32_t t0, int32_t t1, double *out, uint64_t *hash) {
+  int32_t K = e->n_outputs, w = e->leaf_width;
+  for (int64_t r = r0; r < r1; ++r) {
+    double *o = out + r * K;
+    uint64_t h = 0;
+    for (int32_t k = 0; k < K; ++k) o[k] = 0.0;
+    for (int32_t t = t0; t < t1; ++t) {
+      int32_t leaf = walk(e, t, X + r * ldx);
+      const float *v = e->leaf_value + (e->node_offset[t] + leaf) * w;
+      if (w == 1) {
+        o[tree_out(e, t)] += (double)v[0];
+      } else {
+        for (int32_t k = 0; k < K; ++k) o[k] += (double)v[k];
+      }
+      h += mix64(((uint64_t)(uint32_t)t << 32) | (uint32_t)leaf);
+    }
+    hash[r] = h;
+  }
+}
+
+typedef struct {
+  const oracle_ensemble *e; const float *X; int64_t r0, r1, ldx; int32_t t0, t1;
+  double *out; uint64_t *hash;
+} hjob_t;
+
+static void *hjob_main(void *p) {
+  hjob_t *j = (hjob_t *)p;
+  raw_hash_rows(j->e, j->X, j->r0, j->r1, j->ldx, j->t0, j->t1, j->out, j->hash);
+  return NULL;
+}
+
+int oracle_raw_hash_mt(const oracle_ensemble *e, const float *X, int64_t n, int64_t ldx,
+                       int32_t t0, int32_t t1, double *out, uint64_t *hash, int nthreads) {
+  if (nthreads <= 0) nthreads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 1024) nthreads = 1024;
+  if ((int64_t)nthreads > n) nthreads = n > 0 ? (int)n : 1;
+  pthread_t th[1024];
+  hjob_t jobs[1024];
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i].e = e; jobs[i].X = X; jobs[i].ldx = ldx; jobs[i].t0 = t0; jobs[i].t1 = t1;
+    jobs[i].out = out; jobs[i].hash = hash;
+    jobs[i].r0 = n * i / nthreads; jobs[i].r1 = n * (i + 1) / nthreads;
+    if (nthreads == 1) hjob_main(&jobs[i]);
+    else pthread_create(&th[i], NULL, hjob_main, &jobs[i]);
+  }
+  if (nthreads > 1)
+    for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+  return nthreads;
+}
+
 int oracle_predict_mt(const oracle_ensemble *e, const float *X, int64_t n, int64_t ldx,
                       double *out, int nthreads) {
   int used = oracle_raw_mt(e, X, n, ldx, 0, e->n_trees, out, nthreads);

@@ -73,6 +73,13 @@ void oracle_leaf_hash(const oracle_ensemble *e, const float *X, int64_t n, int64
 int oracle_raw_mt(const oracle_ensemble *e, const float *X, int64_t n, int64_t ldx,
                   int32_t t0, int32_t t1, double *out, int nthreads);
 
+/* raw sums AND leaf hashes over trees [t0, t1) in one walk per (row, tree),
+ * rows split over nthreads pthreads (<= 0: all online cores): the same values
+ * as oracle_raw + oracle_leaf_hash, for parity checks on every row of a
+ * full-size config. Returns the thread count used. */
+int oracle_raw_hash_mt(const oracle_ensemble *e, const float *X, int64_t n, int64_t ldx,
+                       int32_t t0, int32_t t1, double *out, uint64_t *hash, int nthreads);
+
 /* full scoring (raw over all trees -> margin -> post), multi-threaded; the
  * thing bench.py times. out = post-transformed scores [n * K]. */
 int oracle_predict_mt(const oracle_ensemble *e, const float *X, int64_t n, int64_t ldx,

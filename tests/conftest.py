@@ -8,3 +8,18 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """List the near-tie rows the GPU label checks met (labels there are
+    allowed to differ from the oracle's; reading R23)."""
+    try:
+        from tests._common import NEAR_TIES
+    except Exception:
+        return
+    if not NEAR_TIES:
+        return
+    diff = sum(1 for _, _, g, o in NEAR_TIES if g != o)
+    terminalreporter.write_line(f"near-tie rows: {len(NEAR_TIES)} (label differs from the oracle on {diff})")
+    for what, r, g, o in NEAR_TIES[:20]:
+        terminalreporter.write_line(f"  {what}: row {r} gpu label {g} oracle label {o}")

@@ -255,3 +255,23 @@ def test_leaf_hash_consistent_with_leaves():
     with np.errstate(over="ignore"):
         s = oracle.leaf_hash(e, X, 0, 4) + oracle.leaf_hash(e, X, 4, 9)
     assert np.array_equal(s, exp)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_raw_and_hash_mt_equals_single_threaded_definitions(threads):
+    """oracle_raw_hash_mt (one walk per (row, tree), rows split over pthreads;
+    used for every-row parity at full size) returns exactly what the
+    single-threaded oracle_raw (fp64, tree order) and the hash pinned above
+    (Σ mix64 over oracle_leaf) return, for vector leaves, per-class routing,
+    tree shards and NaN / ±Inf cells, and for more threads than rows."""
+    for e in (small_forest(21, T=13, D=5, F=4),
+              small_forest(22, T=12, D=4, F=3, n_outputs=3),
+              small_forest(23, T=7, D=3, F=5, n_outputs=4, leaf_width=4, leaf_kind="dirichlet",
+                           agg=synth.AGG_MEAN)):
+        X = synth.gen_X(31, 257, e.n_features, special_q24=1 << 20)
+        for t0, t1 in ((0, e.n_trees), (2, e.n_trees - 1)):
+            r, h = oracle.raw_and_hash(e, X, t0, t1, threads=threads)
+            assert np.array_equal(r, oracle.raw(e, X, t0, t1))
+            assert np.array_equal(h, oracle.leaf_hash(e, X, t0, t1))
+        r, h = oracle.raw_and_hash(e, X[:2], threads=threads)
+        assert np.array_equal(h, oracle.leaf_hash(e, X[:2]))
