@@ -2,17 +2,33 @@
 """Benchmark: rows/sec scored (500 trees, depth 8) on 1..8 B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
-                    [--impl ours|reference] [--strategy auto] [--no-e2e] [--no-cpu]
+                    [--scaling strong|weak] [--impl ours|reference] [--strategy auto]
+                    [--no-e2e] [--no-cpu]
 
-One "step" is one pass of the whole hot path over one batch: a single fused
-hb_predict_proba (or hb_predict for regression) launch over all rows of the
-rank's shard (X tile staging, the strategy's traversal, ensemble accumulate,
-epilogue, store). Rows are sharded across ranks with no data-path collective
-(weak scaling: every rank scores its own n_rows). Timing: W untimed warm-up
-steps, then K steps bracketed by barrier + cuda synchronize, CUDA events on
-the launching stream, max over ranks. X (> L2) is resident in HBM before the
-timed region. ``e2e`` repeats the metric through hb_predict_host from pinned
-host memory (H2D of X and D2H of the result inside the timed region).
+One "step" is one pass of the whole hot path over one batch: one hb_predict
+(proba for classification, predict for regression) call over all rows of the
+rank's shard — X tile staging, the strategy's traversal, ensemble accumulate,
+epilogue, store; two launches when the model runs the rank-code pre-pass, one
+per L2-resident tree chunk plus a finalize for chunked TT models.
+
+Multi-GPU: row-sharded configs (C1-C4) split the config's
+rows over the ranks with no data-path collective (strong scaling, the
+BASELINE "10M rows, rows sharded over 1/2/4/8 GPUs"; --scaling weak gives
+every rank the full row count instead); C5 shards trees: every rank scores all
+rows with its tree range, fp64 partials go through one NCCL reduce to rank 0,
+which finalizes. Timing: W untimed warm-up steps, then K steps bracketed by
+barrier + cuda synchronize, CUDA events on the launching stream, max over
+ranks. X (> L2) is resident in HBM before the timed region. ``e2e`` repeats the
+metric through hb_predict_host from pinned host memory (H2D of X and D2H of
+the result inside the timed region).
+
+The roofline names the dominant kernel of the call: its duration is measured
+live by CUDA events the library records between its launches
+(hb_predict_ex_events) over the timed steps; its algorithmic bytes are
+SURVEY.md §8(d)'s per-row figure times the rows. ``traffic`` is the DRAM bytes
+of every launch of one call (ncu, profiles/ncu_traffic.json) with the split.
+``parity`` compares the GPU outputs with the oracle on the rows the oracle
+baseline timed (outside the timed region).
 
 --impl reference times the CPU oracle (the only reference this tier has) on a
 bounded sample per step, on the host cores; rank 0 only.
@@ -34,6 +50,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "rows/sec scored (500 trees, depth 8) at 1/2/4/8 B200; % of HBM/tensor roofline"
+TOL = "|gpu - oracle| <= 1e-5 + 1e-5 |oracle| (P:469; DESIGN.md R23)"
 
 
 def parse():
@@ -42,7 +59,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--rows", type=int, default=0, help="override rows per GPU")
+    ap.add_argument("--rows", type=int, default=0, help="override the config's total rows")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="row-sharded configs: strong = the config's rows split over the ranks "
+                         "(default); weak = every rank scores the full row count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--strategy", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
@@ -51,8 +71,8 @@ def parse():
     ap.add_argument("--shard", default=None, choices=["rows", "trees"],
                     help="default: trees for C5, rows otherwise")
     ap.add_argument("--emulate-gpus", type=int, default=0,
-                    help="trees mode on 1 GPU: score only rank 0's tree shard of an "
-                         "N-GPU run (the per-GPU piece of C5 on 8 GPUs)")
+                    help="trees mode on ONE GPU: score only rank 0's tree shard of an "
+                         "N-GPU run (the per-GPU piece of C5 on 8 GPUs); no reduce")
     return ap.parse_args()
 
 
@@ -108,24 +128,47 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- oracle (CPU baseline)
-def time_oracle(e, cfg, budget_s=12.0, max_rows=None, threads=0):
-    """Oracle throughput on a bounded prefix sample of the workload, all host
-    cores (std pthreads over row blocks). Returns (rows/s, cores, sample)."""
+def truncated_mean(xs):
+    """"run all the experiments 5 times and report the truncated mean
+    (by averaging the middle values)"."""
+    s = sorted(xs)
+    mid = s[1:-1] if len(s) >= 3 else s
+    return float(np.mean(mid))
+
+
+def oracle_call(e, X, t0, t1, threads):
+    """What the oracle baseline computes for the line's workload: full scoring
+    (raw -> margin -> post) for a whole model, raw sums for a tree shard."""
     import oracle
+    if t0 == 0 and t1 == e.n_trees:
+        return oracle.predict_mt(e, X, threads=threads)[1]
+    oracle.raw(e, X, t0, t1, threads=threads if threads else 0)
+    return threads or os.cpu_count()
+
+
+def time_oracle(e, cfg, t0, t1, run_s=2.5, runs=5, threads=0, max_rows=None):
+    """Oracle throughput on a bounded prefix of the workload's rows: `runs`
+    timed runs of ~run_s each (5 runs, truncated mean; the min is
+    reported too). Returns a dict (rate from the truncated mean of the run
+    times, rows, cores)."""
     import synth
     max_rows = max_rows or cfg.n_rows
-    probe = min(2000, max_rows)
+    probe = min(1000, max_rows)
     Xp = synth.gen_X(cfg.seed_x, probe, cfg.n_features)
     t = time.perf_counter()
-    _, used = oracle.predict_mt(e, Xp, threads=threads)
-    dt = max(time.perf_counter() - t, 1e-4)
-    rate = probe / dt
-    rows = int(min(max_rows, max(probe, rate * budget_s)))
+    oracle_call(e, Xp, t0, t1, threads)
+    rate = probe / max(time.perf_counter() - t, 1e-4)
+    rows = int(min(max_rows, max(probe, rate * run_s)))
     X = synth.gen_X(cfg.seed_x, rows, cfg.n_features)
-    t = time.perf_counter()
-    _, used = oracle.predict_mt(e, X, threads=threads)
-    dt = time.perf_counter() - t
-    return rows / dt, used, f"first {rows} rows of {cfg.name} (seed {cfg.seed_x:#x}), full model", dt
+    times, used = [], 1
+    for _ in range(runs):
+        t = time.perf_counter()
+        used = oracle_call(e, X, t0, t1, threads)
+        times.append(time.perf_counter() - t)
+    tm = truncated_mean(times)
+    return {"value": rows / tm, "unit": "rows/s", "cores": int(used), "rows": rows,
+            "runs": runs, "seconds_truncated_mean": tm, "seconds_min": min(times),
+            "value_at_min": rows / min(times), "seconds_all": times}
 
 
 def cpu_model():
@@ -142,17 +185,17 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
+    import oracle
     import synth
     cfg, e = synth.make_config(args.config)
     # size each step for ~4 s of CPU work (HB_REF_STEP_S overrides)
     step_s = float(os.environ.get("HB_REF_STEP_S", "4.0"))
-    rate0, used, _, _ = time_oracle(e, cfg, budget_s=min(1.0, step_s))
-    rows = int(min(cfg.n_rows, max(100, rate0 * step_s)))
-    import oracle
+    r0 = time_oracle(e, cfg, 0, e.n_trees, run_s=min(0.5, step_s), runs=1)
+    rows = int(min(cfg.n_rows, max(100, r0["value"] * step_s)))
     X = synth.gen_X(cfg.seed_x, rows, cfg.n_features)
     for _ in range(args.warmup):
         oracle.predict_mt(e, X[: max(1, rows // 8)])
-    times = []
+    times, used = [], 1
     for _ in range(args.steps):
         t = time.perf_counter()
         _, used = oracle.predict_mt(e, X)
@@ -162,7 +205,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(cfg, e, rows, args),
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": used, "kind": "oracle",
                          "sample": f"first {rows} rows of {cfg.name} per step", "cpu": cpu_model()},
@@ -173,28 +216,44 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def launches_per_call(info, kind, small):
-    """Kernels one hb_predict call launches: rank-code pre-pass models two
-    (pre-pass + scorer) except on the small-batch path; a TT model walked in
-    L2-resident tree chunks one per chunk, plus the finalize for outputs that
-    need the post transform."""
-    chunk = info.get("tt_chunk_trees", 0)
-    if chunk and not small:
-        pad = (info["n_trees"] + 3) // 4 * 4
-        return -(-pad // chunk) + (1 if kind in ("predict", "proba", "margin") else 0)
-    return 2 if info.get("rank_prepass") and not small else 1
-
-
-def workload_config(cfg, e, rows, args, mode="rows"):
-    par = (f"rows sharded over {args.gpus} GPU(s), no collective" if mode == "rows" else
-           f"trees sharded over {args.gpus} GPU(s), one NCCL reduce of fp64 partials + finalize")
-    return {"workload": f"{cfg.name}: {cfg.note}", "rows_per_gpu": rows, "n_trees": e.n_trees,
+def workload_config(cfg, e, rows, args, mode="rows", scaling="strong", world=1):
+    if mode == "rows":
+        par = (f"rows sharded over {world} GPU(s), no collective ({scaling} scaling: "
+               + ("the config's rows split over the ranks)" if scaling == "strong"
+                  else "every rank scores the full row count)"))
+    else:
+        par = f"trees sharded over {world} GPU(s), one NCCL reduce of fp64 partials + finalize"
+    return {"workload": f"{cfg.name}: {cfg.note}", "rows_total": rows, "n_trees": e.n_trees,
             "max_depth": cfg.depth, "n_features": cfg.n_features, "n_outputs": e.n_outputs,
             "family": cfg.family, "parallelism": par,
             "l2": ("X larger than L2 (streamed once per step, no flush needed); model (<13 MB) "
                    "L2-resident by design" if cfg.depth <= 10 else
                    "X larger than L2 (streamed once per step, no flush needed); depth-12 node records: "
                    "a 1/8 tree shard (~60 MB) is L2-resident, all 10k trees (~480 MB) are not")}
+
+
+def launch_names(info, n):
+    """Kernel names of one call's launches, in order (hb_predict_ex_events)."""
+    if n <= info["small_batch_max_rows"]:
+        return ["small_batch_kernel"]
+    if info.get("rank_prepass"):
+        return ["rank_code_kernel", "pttr_kernel"]
+    chunk = info.get("tt_chunk_trees", 0)
+    if chunk:
+        pad = (info["n_trees"] + 3) // 4 * 4
+        return [info["kernel_name"]] * (-(-pad // chunk)) + ["finalize_kernel"]
+    return [info["kernel_name"]]
+
+
+def load_traffic(config, layout, rows, trees):
+    """DRAM traffic of one call (every launch) from profiles/ncu_traffic.json,
+    recorded by tools/traffic.py from one ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+    except (OSError, ValueError):
+        return None
+    return d.get(f"{config}:{layout}:{rows}:{trees}")
 
 
 # ----------------------------------------------------------------- ours
@@ -214,52 +273,60 @@ def run_ours(args):
     import paper_2010_04804_b200 as hb
     import synth
     import synth.dev
-    from paper_2010_04804_b200.dist import max_over_ranks, reduce_partials, tree_shard
+    from paper_2010_04804_b200.dist import max_over_ranks, reduce_partials, row_shard, tree_shard
 
     cfg, e = synth.make_config(args.config)
-    n = args.rows or cfg.n_rows
+    n_total = args.rows or cfg.n_rows
     mode = args.shard or ("trees" if cfg.name == "C5" else "rows")
+    if args.emulate_gpus and world > 1 and args.emulate_gpus != world:
+        raise SystemExit("--emulate-gpus N with several ranks needs N == world size")
     cls = e.task == synth.TASK_CLASSIFICATION
     kind = "proba" if cls else "predict"
     stream = torch.cuda.current_stream(local)
+    scaling = args.scaling
     if mode == "rows":
-        # rows sharded, model replicated, no data-path collective (weak scaling)
+        # rows sharded, model replicated, no data-path collective
+        if scaling == "strong":
+            r0, n = row_shard(n_total, rank, world)
+        else:
+            r0, n = rank * n_total, n_total
         t0, t1 = 0, e.n_trees
         m = hb.Model(e, strategy=args.strategy, device=local)
-        X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, row_offset=rank * n,
-                                   device=local)
-        shape, dt = m.out_shape(n, kind)
-        out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
-
-        def step():
-            m.run(X, kind, out=out, stream=stream)
-        small = n <= int(os.environ.get("HB_SMALL_BATCH", "4096"))
-        launches_per_step = launches_per_call(m.info, kind, small)
+        X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, row_offset=r0, device=local)
+        out = m._out(n, kind, None, X.device)
+        call_kind, call_out = kind, out
+        rows_all = n_total if scaling == "strong" else n_total * world
     else:
-        # trees sharded, all rows on every rank; one NCCL reduce of fp32
-        # partials to rank 0, which finalizes (strong scaling)
-        t0, t1 = tree_shard(e.n_trees, rank, max(world, args.emulate_gpus), e.n_outputs,
-                            e.leaf_width)
+        # trees sharded, all rows on every rank; one NCCL reduce of fp64
+        # partials to rank 0, which finalizes (strong scaling over trees)
+        shards = max(world, args.emulate_gpus)
+        t0, t1 = tree_shard(e.n_trees, rank, shards, e.n_outputs, e.leaf_width)
         m = hb.Model(e, strategy=args.strategy, device=local, tree_range=(t0, t1))
+        r0, n = 0, n_total
         X = synth.dev.gen_X_device(cfg.seed_x, n, cfg.n_features, device=local)
         raw = torch.empty((n, e.n_outputs), dtype=torch.float64, device=X.device)
-        shape, dt = m.out_shape(n, kind)
-        out = torch.empty(shape, dtype=getattr(torch, dt), device=X.device)
+        out = m._out(n, kind, None, X.device)
+        call_kind, call_out = "raw64", raw
+        rows_all = n
+        scaling = "strong"
+    info = m.info
+    names = launch_names(info, n)
+    small = n <= info["small_batch_max_rows"]
 
-        def step():
-            m.run(X, "raw64", out=raw, stream=stream)
+    def tail():
+        """The rest of a trees-mode step after the scorer call."""
+        if mode == "trees":
             if dist:
                 reduce_partials(raw, dst=0)
             if rank == 0:
                 m.finalize(raw, kind, out=out, stream=stream)
-        launches_per_step = launches_per_call(m.info, "raw64", False) + 1
-    info = m.info
 
     # request/response batch sizes (small-batch kernel) are launch-bound from
-    # Python: capture REPS calls in one CUDA graph and replay it, so the
+    # Python: capture `calls` calls in one CUDA graph and replay it, so the
     # device time per call is measured instead of the host issue rate
     calls = 1
-    if mode == "rows" and n <= int(os.environ.get("HB_SMALL_BATCH", "4096")):
+    graph = None
+    if mode == "rows" and small:
         calls = int(os.environ.get("HB_BENCH_GRAPH_CALLS", "200"))
         gs = torch.cuda.Stream(local)
         gs.wait_stream(stream)
@@ -273,8 +340,24 @@ def run_ours(args):
                 m.run(X, kind, out=out, stream=gs)
         torch.cuda.synchronize()
 
-        def step():
+    # per-launch events recorded by the library (hb_predict_ex_events)
+    nev = len(names) + 1
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    for row in evs:
+        for ev in row:
+            ev.record(stream)          # creates the CUDA events up front
+
+    def step(i=None):
+        if graph is not None:
             graph.replay()
+            return 1
+        if i is None:
+            m.run(X, call_kind, out=call_out, stream=stream)
+            nl = len(names)
+        else:
+            nl = m.run_events(X, call_kind, call_out, evs[i], stream)
+        tail()
+        return nl
 
     for _ in range(max(args.warmup, 3)):     # timing rule: >= 3 warm-up steps
         step()
@@ -286,38 +369,41 @@ def run_ours(args):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
+    launches = 0
     for i in range(args.steps):
-        evs[i][0].record(stream)
-        if mode == "rows":
-            step()
-            evs[i][1].record(stream)
-        else:
-            m.run(X, "raw64", out=raw, stream=stream)   # the scorer launch(es) alone
-            evs[i][1].record(stream)
-            if dist:
-                reduce_partials(raw, dst=0)
-            if rank == 0:
-                m.finalize(raw, kind, out=out, stream=stream)
+        launches += step(i)
     t_end.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
     total_ms = t_start.elapsed_time(t_end)
-    per_launch = [a.elapsed_time(b) for a, b in evs]
     if dist:
         total_ms = max_over_ranks(total_ms, device=X.device)
         dist.barrier()
     ms_per_step = total_ms / args.steps / calls
-    per_launch = [t / calls for t in per_launch]
-    rows_all = n * world if mode == "rows" else n
     value = rows_all / (ms_per_step * 1e-3)
+    if graph is not None:
+        launches = args.steps * calls
+        names = ["small_batch_kernel"]
 
-    # ---- roofline of the dominant (only) kernel of the step
-    kern_ms = float(np.mean(per_launch))
+    # ---- per-kernel durations (library events), dominant kernel
+    per_kernel = {}
+    if graph is None:
+        for row in evs:
+            for j, nm in enumerate(names):
+                per_kernel.setdefault(nm, []).append(row[j].elapsed_time(row[j + 1]))
+        kern_total = {nm: float(np.sum(v)) / args.steps for nm, v in per_kernel.items()}
+        kern_launch = {nm: float(np.mean(v)) for nm, v in per_kernel.items()}
+        dom = max(kern_total, key=kern_total.get)
+        dom_ms = kern_total[dom]             # per call (all launches of that kernel)
+        call_ms = sum(kern_total.values())
+    else:
+        kern_total = kern_launch = {"small_batch_kernel": ms_per_step}
+        dom, dom_ms, call_ms = "small_batch_kernel", ms_per_step, ms_per_step
+
+    # ---- roofline of the dominant kernel
     D = info["max_depth"]
     w = info["leaf_width"]
     # per (row, tree) and level one 8-B node record + one 4-B X
@@ -328,7 +414,7 @@ def run_ours(args):
     if info["strategy_name"] == "tt":
         levels = mean_path_length(m, e, X[: min(n, 2048)], t0, t1)
     per_row = (t1 - t0) * (levels * 12 + 4 * w)
-    achieved = per_row * n / (kern_ms * 1e-3) / 1e9
+    achieved = per_row * n / (dom_ms * 1e-3) / 1e9
     peaks = {}
     if rank == 0:
         try:
@@ -339,12 +425,10 @@ def run_ours(args):
             peaks = {"error": str(ex)}
     smem_peak = peaks.get("smem_gbs") or 148 * 128 * 1.965
     layout = info["strategy_name"] + ("-rank" if info.get("node_record_bytes") == 4 else "") + \
-        ("-pre" if info.get("rank_prepass") else "") + ("-sector" if info.get("tt_sector") else "") + \
-        ("-chunk" if info.get("tt_chunk_trees") else "")
-    prof = load_profile(args.config, layout)
-    kname = info["kernel_name"]
-    if n <= int(os.environ.get("HB_SMALL_BATCH", "4096")):
-        kname = "small_batch_kernel"      # request/response sizes (hb_small.cu)
+        ("-pre" if info.get("rank_prepass") else "") + ("-chunk" if info.get("tt_chunk_trees") else "")
+    if small:
+        layout = "small-batch"
+    traffic = load_traffic(args.config, layout, n, t1 - t0)
     hbm_bytes = n * (cfg.n_features * 4 + (8 if (cls and e.n_outputs == 1) else 4 * e.n_outputs))
     measured = {}
     try:
@@ -352,47 +436,44 @@ def run_ours(args):
     except OSError:
         pass
     hbm_peak = measured.get("hbm_gbs", 6650.0)
-    same_launch = prof.get("rows") == n and prof.get("trees", t1 - t0) == t1 - t0
-    # nodes staged in SMEM (PTT, narrow TT) -> SMEM roof; tt_wide_kernel and
-    # ttb_kernel read node records through L1/L2 -> the measured L2 read roof
-    l2_wide = info["strategy_name"] == "tt" and kname in ("tt_wide_kernel", "ttb_kernel")
+    # nodes staged in SMEM (PTT, narrow TT) -> SMEM roof; tt_wide_kernel reads
+    # node records through L1/L2 -> the measured L2 read roof
+    l2_wide = info["strategy_name"] == "tt" and dom == "tt_wide_kernel"
     bound, peak = ("l2", peaks.get("l2_gbs") or 12000.0) if l2_wide else ("smem", smem_peak)
     roofline = {
         "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "mean_levels_per_tree": levels,
-        # contract: traffic = dram__bytes_read.sum + dram__bytes_write.sum per
-        # launch (one ncu --set full capture); the kernel is bound on chip, so
-        # the comparable figure for achieved/algorithmic bytes is the SMEM one
-        "traffic": prof.get("dram_bytes_per_launch") if same_launch else None,
-        "traffic_smem": prof.get("smem_ld_bytes_per_launch") if same_launch else None,
-        "traffic_note": "traffic = DRAM bytes per launch (X + output when the model is L2-resident); "
-                        "traffic_smem = SMEM load wavefronts x 128 B per launch, the on-chip "
-                        "counterpart of the algorithmic bytes",
-        "traffic_source": prof.get("source"),
-        # cross-check in bytes the kernel really loads from SMEM (ncu), over the
-        # whole timed call (the pre-pass launch included when there is one)
-        "frac_ncu_smem_bytes": (prof["smem_ld_bytes_per_launch"] / (kern_ms * 1e-3) / 1e9 / smem_peak)
-        if (same_launch and bound == "smem" and prof.get("smem_ld_bytes_per_launch")) else None,
-        "kernel": kname, "layout": layout, "kernel_ms": kern_ms,
-        "kernel_ms_covers": ("rank-code pre-pass + pttr_kernel (both launches of one hb_predict call; "
-                             "their split is in the ncu launch list under profiles/)")
-        if info.get("rank_prepass") and kname != "small_batch_kernel" else
-        (f"{kname} over L2-resident chunks of {info['tt_chunk_trees']} trees (one launch per chunk) + finalize"
-         if info.get("tt_chunk_trees") else kname),
+        "frac": achieved / peak, "kernel": dom, "layout": layout,
+        "kernel_ms": dom_ms, "kernel_ms_per_launch": kern_launch.get(dom),
+        "kernel_ms_source": "CUDA events recorded by libhb between its launches "
+                            "(hb_predict_ex_events) over the timed steps",
+        "kernels_ms_per_call": kern_total,
+        "call_ms": call_ms,
+        "frac_call": per_row * n / (ms_per_step * 1e-3) / 1e9 / peak,
+        "mean_levels_per_tree": levels,
         "algorithmic_bytes_per_row": per_row,
+        "algorithmic_bytes_per_call": per_row * n,
+        "traffic": traffic["dram_bytes_per_call"] if traffic else None,
+        "traffic_split": traffic["launches"] if traffic else None,
+        "traffic_note": ("DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of EVERY launch "
+                         "of one call, from one ncu --set full capture (tools/traffic.py); "
+                         "traffic_split lists them per launch" if traffic else
+                         "no ncu capture recorded for this config/layout/rows"),
+        "traffic_source": traffic.get("source") if traffic else None,
         "peak_source": ("measured L2 read microbenchmark (tools/peaks.cu), this run" if l2_wide else
                         "measured LDS.128 microbenchmark (tools/peaks.cu), this run")
         if (peaks.get("l2_gbs") if l2_wide else peaks.get("smem_gbs"))
         else "spec 148 SM x 128 B/clk x 1.965 GHz",
         "smem_peak_spec_gbs": 148 * 128 * 1.965,
         "l2_peak_gbs": peaks.get("l2_gbs"),
-        "hbm": {"achieved": hbm_bytes / (kern_ms * 1e-3) / 1e9, "peak": hbm_peak,
-                "frac": hbm_bytes / (kern_ms * 1e-3) / 1e9 / hbm_peak,
-                "peak_source": "MEASURED_PEAKS.json" if measured else "fallback 6.65 TB/s"},
+        "hbm": {"achieved": hbm_bytes / (ms_per_step * 1e-3) / 1e9, "peak": hbm_peak,
+                "frac": hbm_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
+                "bytes_per_call": hbm_bytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if measured else "fallback 6.65 TB/s"},
     }
 
     # ---- e2e through the public host API (pinned host buffers)
     e2e = None
+    shape, dt = m.out_shape(n, kind)
     if not args.no_e2e and mode == "rows":
         del out
         Xh = torch.empty((n, cfg.n_features), dtype=torch.float32).pin_memory()
@@ -414,14 +495,14 @@ def run_ours(args):
                "d2h_bytes_per_step": int(oh.numel() * oh.element_size()), "steps": args.e2e_steps,
                "api": "hb_predict_host (chunked H2D / score / D2H on two streams)"}
         del Xh, oh
+        out = m._out(n, kind, None, X.device)
     elif not args.no_e2e and mode == "trees":
         # every rank streams all rows from pinned host memory through
-        # hb_predict_host and gets its shard's raw partials back; the partials
+        # hb_predict_host and gets its shard's fp64 partials back; the partials
         # go to the device for the NCCL reduce, rank 0 finalizes and reads the
-        # result back (the partial round trip is n*K*4 B each way)
+        # result back (the partial round trip is n*K*8 B each way)
         Xh = torch.empty((n, cfg.n_features), dtype=torch.float32).pin_memory()
         Xh.copy_(X)
-        del X
         rawh = torch.empty((n, e.n_outputs), dtype=torch.float64).pin_memory()
         oh = torch.empty(shape, dtype=getattr(torch, dt)).pin_memory()
 
@@ -450,33 +531,52 @@ def run_ours(args):
                "h2d_bytes_per_step": int(n * cfg.n_features * 4) + part,
                "d2h_bytes_per_step": part + int(oh.numel() * oh.element_size()),
                "steps": args.e2e_steps,
-               "api": "hb_predict_host(raw) per tree shard -> NCCL reduce of the partials -> "
-                      "hb_finalize on rank 0 -> D2H"}
+               "api": "hb_predict_host(raw64) per tree shard -> NCCL reduce of the partials -> "
+                      "hb_finalize64 on rank 0 -> D2H"}
         del Xh, oh, rawh
 
-    cpu = None
+    # ---- CPU oracle baseline (P:324 timing) and parity on the same rows
+    cpu = parity = None
     if rank == 0 and not args.no_cpu:
-        rate, used, sample, secs = time_oracle(e, cfg, budget_s=12.0)
-        cpu = {"value": rate, "unit": "rows/s", "cores": used, "kind": "oracle", "sample": sample,
-               "seconds": secs, "cpu": cpu_model()}
+        whole = t0 == 0 and t1 == e.n_trees
+        tm = time_oracle(e, cfg, t0, t1, run_s=2.5, runs=5, max_rows=n)
+        cpu = {"value": tm["value"], "unit": "rows/s", "cores": tm["cores"], "kind": "oracle",
+               "sample": f"first {tm['rows']} rows of {cfg.name} (seed {cfg.seed_x:#x}), "
+                         + ("full model" if whole else f"trees [{t0}, {t1})"),
+               "timing": "5 runs, truncated mean (P:324); min also given",
+               "value_at_min": tm["value_at_min"], "seconds_truncated_mean": tm["seconds_truncated_mean"],
+               "seconds_min": tm["seconds_min"], "cpu": cpu_model()}
         # the oracle on all host cores, plus one core
-        r1, u1, s1, t1_ = time_oracle(e, cfg, budget_s=3.0, threads=1)
-        cpu["single_core"] = {"value": r1, "unit": "rows/s", "cores": u1, "sample": s1,
-                              "seconds": t1_}
+        t1c = time_oracle(e, cfg, t0, t1, run_s=0.6, runs=5, threads=1, max_rows=n)
+        cpu["single_core"] = {"value": t1c["value"], "unit": "rows/s", "cores": 1,
+                              "rows": t1c["rows"], "value_at_min": t1c["value_at_min"]}
+        parity = parity_report(m, e, cfg, X, tm["rows"], t0, t1, kind, cls)
+        if mode == "trees" and whole is False:
+            parity["scope"] = f"tree shard [{t0}, {t1}) raw fp64 partials and leaf hashes"
 
     if rank == 0:
+        cfgd = dict(workload_config(cfg, e, rows_all, args, mode, scaling, world), strategy=info["strategy_name"],
+                    output=kind, rows_per_gpu=n, trees_per_gpu=t1 - t0,
+                    timing=("CUDA graph of %d calls per timed step, value per call" % calls)
+                    if calls > 1 else "one call per timed step")
+        if mode == "trees" and args.emulate_gpus and world == 1:
+            cfgd["emulated_shard_of"] = args.emulate_gpus
+            cfgd["trees_scored"] = t1 - t0
+            cfgd["parallelism"] = (f"ONE GPU scoring rank 0's 1/{args.emulate_gpus} tree shard "
+                                   f"({t1 - t0} of {e.n_trees} trees), no reduce")
+            cfgd["value_note"] = ("rate of one GPU's tree shard = the 8-GPU job rate if the reduce "
+                                  "were free; NOT the full-model single-GPU rate")
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak" if mode == "rows" else "strong",
+            "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32",
+            "dtype_note": "fp32 X and thresholds, IEEE fp32 compares, fp64 leaf-value accumulation",
             "data": f"synthetic (seeded splitmix64 grid X; random {cfg.family} depth-{cfg.depth} forest)",
-            "config": dict(workload_config(cfg, e, n, args, mode), strategy=info["strategy_name"],
-                           output=kind, trees_per_gpu=t1 - t0,
-                           timing=("CUDA graph of %d calls per timed step, value per call" % calls)
-                           if calls > 1 else "one call per timed step"),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": args.steps * calls * launches_per_step,
+            "config": cfgd,
+            "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches,
+            "gpu_launches_per_call": names,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -484,10 +584,58 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def parity_report(m, e, cfg, X, rows, t0, t1, kind, cls):
+    """GPU outputs vs the oracle on the rows the oracle baseline timed
+    (outside the timed region): leaf-hash mismatches (bit-exact bar), max abs
+    / rel error of the margin and of the returned output (R23 bar), labels
+    outside near-ties, near-tie count."""
+    import oracle
+    rows = min(rows, X.shape[0])
+    Xs = X[:rows]
+    import synth
+    Xh = synth.gen_X(cfg.seed_x, rows, cfg.n_features)
+    raw, hsh = oracle.raw_and_hash(e, Xh, t0, t1, threads=0)
+    g_hash = m.predict_leaf_hash(Xs).cpu().numpy().view(np.uint64)
+    rep = {"rows": rows, "tolerance": TOL,
+           "leaf_hash_mismatches": int((g_hash != hsh).sum())}
+
+    def errs(got, ref, tag):
+        got = np.asarray(got, np.float64)
+        d = np.abs(got - ref)
+        rep[f"{tag}_max_abs_err"] = float(d.max())
+        rep[f"{tag}_max_rel_err"] = float((d / np.maximum(np.abs(ref), 1e-30)).max())
+        rep[f"{tag}_outside_tol"] = int((d > 1e-5 + 1e-5 * np.abs(ref)).sum())
+
+    if t0 == 0 and t1 == e.n_trees:
+        mg = oracle.margin(e, raw)
+        errs(m.predict_margin(Xs).cpu().numpy(), mg, "margin")
+        post = oracle.post(e, mg)
+        ref = oracle.proba(e, post) if cls else post
+        errs(m.run(Xs, kind).cpu().numpy(), ref, kind)
+        if cls:
+            lab = m.predict(Xs).cpu().numpy()
+            ref_lab = oracle.label(e, mg)
+            if e.n_outputs == 1:
+                tie = np.abs(mg[:, 0]) < 2 * (1e-5 + 1e-5 * np.abs(mg[:, 0]))
+            else:
+                s = np.sort(mg, 1)
+                tie = s[:, -1] - s[:, -2] < 2 * (1e-5 + 1e-5 * np.abs(s[:, -1]))
+            rep["near_ties"] = int(tie.sum())
+            rep["near_tie_rows"] = [int(r) for r in np.flatnonzero(tie)[:20]]
+            rep["label_mismatches_outside_near_ties"] = int((lab[~tie] != ref_lab[~tie]).sum())
+            rep["label_mismatches_at_near_ties"] = int((lab[tie] != ref_lab[tie]).sum())
+        bad = rep["leaf_hash_mismatches"] + rep["margin_outside_tol"] + rep[f"{kind}_outside_tol"] + \
+            rep.get("label_mismatches_outside_near_ties", 0)
+    else:
+        errs(m.predict_raw64(Xs).cpu().numpy(), raw, "raw")
+        bad = rep["leaf_hash_mismatches"] + rep["raw_outside_tol"]
+    rep["pass"] = bad == 0
+    return rep
+
+
 def mean_path_length(m, e, X, t0, t1):
     """Mean number of levels the walk traverses per (row, tree): leaf depth of
     the reached leaf (leaf ids from the device, depths from the tree arrays)."""
-    import numpy as np
     leaf = m.predict_leaf(X).cpu().numpy()
     tot = 0.0
     for j, t in enumerate(range(t0, t1)):
@@ -501,15 +649,6 @@ def mean_path_length(m, e, X, t0, t1):
                 order += [int(L[i]), int(R[i])]
         tot += depth[leaf[:, j]].mean()
     return tot / max(1, t1 - t0)
-
-
-def load_profile(config, strat):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        d = json.load(open(p))
-        return d.get(f"{config}:{strat}", {})
-    except (OSError, ValueError):
-        return {}
 
 
 def main():

@@ -218,6 +218,18 @@ hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tre
 hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
                         int32_t kind, void *out, void *stream);
 
+/* Profiling form of hb_predict_ex (same arguments, same work): additionally
+ * records the caller-created events `events[i]` (cudaEvent_t passed as void*)
+ * on `stream` at the start of the call's launch i and one after its last
+ * launch, so per-kernel durations of a multi-launch call (rank-code pre-pass
+ * + scorer; tree chunks + finalize) can be read with cudaEventElapsedTime
+ * without any synchronisation. n_events >= 2; at most n_events events are
+ * recorded. *n_launches (if not NULL) receives the number of kernel launches
+ * the call made. Used by bench.py's roofline (dominant kernel duration). */
+hb_status hb_predict_ex_events(const hb_model *m, const float *X, int64_t n_rows, int64_t ldx,
+                               int32_t kind, void *out, void *stream, void **events,
+                               int32_t n_events, int32_t *n_launches);
+
 /* = hb_predict_ex(HB_OUT_PREDICT): the algorithms' output R (P:172, P:210,
  * P:263) — regression: float[n*K] after the post transform; classification:
  * int32[n] class index (K == 1: 1 iff margin > 0; else argmax, lowest index on

@@ -724,7 +724,9 @@ static hb_status run(const Model &m, const RunArgs &a) {
 }
 
 static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int64_t ldx, int kind,
-                              void *out, void *stream, bool check_ptrs) {
+                              void *out, void *stream, bool check_ptrs, void **events = nullptr,
+                              int nev = 0, int32_t *n_launches = nullptr) {
+  if (n_launches) *n_launches = 0;
   if (!hm) return fail(HB_E_INVALID, "model is NULL");
   const Model &m = *M(hm);
   hb_status st = check_kind(m, kind);
@@ -741,10 +743,19 @@ static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int
     if (st != HB_OK) return st;
   }
   RunArgs a{X, n, ldx, kind, out, static_cast<cudaStream_t>(stream), nullptr};
+  int k = 0;
+  if (events && nev > 0) {
+    a.ev = reinterpret_cast<cudaEvent_t *>(events);
+    a.nev = nev;
+    a.ev_k = &k;
+  }
+  mark_launch(a);
   // request/response sizes: trees-across-threads kernel (f2); threshold from
   // the crossover sweep (tools/crossover.py)
-  if (n <= m.small_max) return launch_small_batch(m, a);
-  return run(m, a);
+  st = n <= m.small_max ? launch_small_batch(m, a) : run(m, a);
+  mark_launch(a);
+  if (n_launches) *n_launches = k > 0 ? k - 1 : 0;
+  return st;
 }
 
 // ------------------------------------------------------------------ host streaming
@@ -846,6 +857,13 @@ hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tre
 hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n, int64_t ldx, int32_t kind,
                         void *out, void *stream) {
   return predict_impl(m, X, n, ldx, kind, out, stream, true);
+}
+
+hb_status hb_predict_ex_events(const hb_model *m, const float *X, int64_t n, int64_t ldx,
+                               int32_t kind, void *out, void *stream, void **events, int32_t n_events,
+                               int32_t *n_launches) {
+  if (!events || n_events < 2) return fail(HB_E_INVALID, "hb_predict_ex_events: need >= 2 events");
+  return predict_impl(m, X, n, ldx, kind, out, stream, true, events, n_events, n_launches);
 }
 
 hb_status hb_predict(const hb_model *m, const float *X, int64_t n, int64_t ldx, void *out,

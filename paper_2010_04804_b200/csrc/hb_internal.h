@@ -114,7 +114,17 @@ struct RunArgs {
   cudaStream_t stream;
   const float *raw_in;      // finalize only: fp32 raw sums (hb_finalize)
   const double *raw_in64 = nullptr;   // finalize only: fp64 raw sums (hb_finalize64, tree chunks)
+  // hb_predict_ex_events: caller events recorded on `stream` at the start of
+  // every launch and after the last one (per-kernel durations, no sync)
+  cudaEvent_t *ev = nullptr;
+  int nev = 0;
+  int *ev_k = nullptr;
 };
+
+// record the next profiling event of a call (no-op without events)
+inline void mark_launch(const RunArgs &a) {
+  if (a.ev && a.ev_k && *a.ev_k < a.nev) cudaEventRecord(a.ev[(*a.ev_k)++], a.stream);
+}
 
 bool gemm_supported(int depth);
 hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);

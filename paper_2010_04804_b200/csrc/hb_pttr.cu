@@ -401,6 +401,7 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m.cfg.smem_bytes);
   if (e == cudaSuccess) {
+    if (codes) mark_launch(a);     // scorer starts (the pre-pass was launch 0)
     fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
     e = cudaGetLastError();
   }

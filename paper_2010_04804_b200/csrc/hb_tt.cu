@@ -484,6 +484,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
     pc.kind = direct ? a.kind : HB_OUT_RAW64;
     pc.out = direct ? a.out : static_cast<void *>(raw);
     pc.accumulate = t0 > 0 && pc.kind != HB_OUT_LEAF;
+    if (t0 > 0) mark_launch(a);    // next chunk launch starts
     fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(pc);
     e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -495,6 +496,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
     RunArgs f = a;
     f.raw_in = nullptr;
     f.raw_in64 = raw;
+    mark_launch(a);                // finalize starts
     const hb_status st = launch_finalize(m, f);
     cudaFreeAsync(raw, a.stream);
     if (st != HB_OK) return st;

@@ -21,7 +21,7 @@ OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 
 
 # every symbol include/hb.h declares (checked by tests/test_abi.py)
 exported_symbols = ["hb_validate", "hb_compile", "hb_compile_range", "hb_predict_ex",
-                    "hb_predict", "hb_predict_proba", "hb_predict_raw", "hb_predict_leaf",
+                    "hb_predict_ex_events", "hb_predict", "hb_predict_proba", "hb_predict_raw", "hb_predict_leaf",
                     "hb_finalize", "hb_finalize64", "hb_predict_host", "hb_model_get_info", "hb_free",
                     "hb_last_error", "hb_abi_version"]
 
@@ -67,6 +67,8 @@ def _load():
         "hb_compile": ([P, i32, i32, C.POINTER(vp)], C.c_int),
         "hb_compile_range": ([P, i32, i32, i32, i32, C.POINTER(vp)], C.c_int),
         "hb_predict_ex": ([vp, vp, i64, i64, i32, vp, vp], C.c_int),
+        "hb_predict_ex_events": ([vp, vp, i64, i64, i32, vp, vp, C.POINTER(vp), i32, C.POINTER(i32)],
+                                 C.c_int),
         "hb_predict": ([vp, vp, i64, i64, vp, vp], C.c_int),
         "hb_predict_proba": ([vp, vp, i64, i64, vp, vp], C.c_int),
         "hb_predict_raw": ([vp, vp, i64, i64, vp, vp], C.c_int),
@@ -210,6 +212,19 @@ class Model:
         _check(lib.hb_predict_ex(self._p, C.c_void_p(X.data_ptr()), n, X.stride(0), OUT[kind],
                                  C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)))
         return out
+
+    def run_events(self, X, kind, out, events, stream):
+        """hb_predict_ex_events: the same call as run(), recording torch
+        CUDA events (already created, enable_timing) at the start of every
+        kernel launch and after the last one; returns the launch count."""
+        n = X.shape[0]
+        out = self._out(n, kind, out, X.device)
+        arr = (C.c_void_p * len(events))(*[C.c_void_p(ev.cuda_event) for ev in events])
+        nl = C.c_int32(0)
+        _check(lib.hb_predict_ex_events(self._p, C.c_void_p(X.data_ptr()), n, X.stride(0), OUT[kind],
+                                        C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream),
+                                        arr, len(events), C.byref(nl)))
+        return nl.value
 
     def predict(self, X, **kw):
         return self.run(X, "predict", **kw)

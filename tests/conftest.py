@@ -20,6 +20,6 @@ def pytest_terminal_summary(terminalreporter, exitstatus, config):
     if not NEAR_TIES:
         return
     diff = sum(1 for _, _, g, o in NEAR_TIES if g != o)
-    terminalreporter.write_line(f"near-tie rows: {len(NEAR_TIES)} (label differs from the oracle on {diff})")
-    for what, r, g, o in NEAR_TIES[:20]:
+    terminalreporter.write_line(f"near-tie rows: {len(NEAR_TIES)} checks (label differs from the oracle on {diff})")
+    for what, r, g, o in sorted(set(NEAR_TIES))[:20]:
         terminalreporter.write_line(f"  {what}: row {r} gpu label {g} oracle label {o}")

@@ -43,12 +43,19 @@ def test_gpu_arm_contract():
     assert r["bound"] == "smem" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    assert "truncated mean" in d["cpu_baseline"]["timing"]
     assert d["e2e"]["h2d_bytes_per_step"] == 300000 * 28 * 4
     # one hb_predict call per step: one launch, two when the model runs the
-    # rank-code pre-pass (C3's AUTO layout does)
+    # rank-code pre-pass (C3's AUTO layout does); the dominant kernel's time
+    # comes from the library's per-launch events
     per_call = 2 if d["roofline"]["layout"].endswith("-pre") else 1
-    assert d["gpu_launches"] == 3 * per_call and d["scaling"] == "weak" and d["n_gpus"] == 1
+    assert len(d["gpu_launches_per_call"]) == per_call
+    assert d["gpu_launches"] == 3 * per_call and d["scaling"] == "strong" and d["n_gpus"] == 1
+    assert r["kernel"] == "pttr_kernel" and 0 < r["kernel_ms"] <= r["call_ms"] * 1.001
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    p = d["parity"]
+    assert p["pass"] and p["leaf_hash_mismatches"] == 0 and p["rows"] > 0
+    assert p["label_mismatches_outside_near_ties"] == 0
 
 
 @pytest.mark.gpu
@@ -61,6 +68,7 @@ def test_gpu_arm_small_batch_graph_and_prepass():
     d = _run(["--config", "C1", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e"])
     assert d["gpu_launches"] == 3 * 200 and "CUDA graph" in d["config"]["timing"]
     assert d["roofline"]["kernel"] == "small_batch_kernel" and d["value"] > 0
+    assert d["roofline"]["layout"] == "small-batch"
     d = _run(["--config", "C2", "--steps", "3", "--warmup", "3", "--rows", "200000", "--no-cpu",
               "--no-e2e"])
     assert d["roofline"]["layout"] == "ptt-rank-pre" and d["gpu_launches"] == 6
@@ -82,11 +90,14 @@ def _torchrun(args, timeout=900):
 def test_multi_rank_bench_on_one_device(cfg, extra):
     """The torchrun path of bench.py (2 ranks; both on this box's one GPU,
     gloo for the collectives): row shards with no data-path collective (C3),
-    tree shards + one reduce of fp32 partials + finalize on rank 0 (C5)."""
+    tree shards + one reduce of fp64 partials + finalize on rank 0 (C5). C3
+    is strong-scaled: the 200,000 rows are split over the two ranks."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     d = _torchrun(["--config", cfg, "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e"] + extra)
     assert d["n_gpus"] == 2 and d["value"] > 0
-    assert d["scaling"] == ("weak" if cfg == "C3" else "strong")
+    assert d["scaling"] == "strong"
     assert d["config"]["trees_per_gpu"] == (500 if cfg == "C3" else 5000)
+    if cfg == "C3":
+        assert d["config"]["rows_total"] == 200000 and d["config"]["rows_per_gpu"] == 100000

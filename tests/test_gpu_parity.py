@@ -475,7 +475,7 @@ def test_rejects_host_pointers_and_bad_args():
     # the binding refuses a host / wrong-shape / wrong-dtype out before the
     # call (the C side cannot see a buffer's length) ...
     for bad in (out_host, torch.zeros(10, 2, device="cuda"), torch.zeros(10, 1, dtype=torch.float64, device="cuda"),
-                torch.zeros(1, 10, device="cuda").t()):
+                torch.zeros(10, 2, device="cuda")[:, :1]):
         with pytest.raises(ValueError):
             m.predict(Xd, out=bad)
     with pytest.raises(ValueError):
