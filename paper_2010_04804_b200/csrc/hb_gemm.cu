@@ -21,134 +21,9 @@
 
 #include "hb_device.cuh"
 #include "hb_internal.h"
+#include "hb_layouts.h"
 
 namespace hb {
-
-constexpr int kGemmMaxInternal = 64;   // T fits one 64-bit word
-
-// per-tree record (all fields 8-B aligned):
-//   u32 hdr[2] = {tree_output, 0}
-//   u32 feat[NI]; f32 thr[NI]                 (NI padded to even)
-//   u64 lmask[NL]; u64 rmask[NL]; u32 D[NL] (NL padded to even)
-//   f32 E[NL * w]
-struct GemmGeom {
-  int ni, nl, w;
-  size_t off_feat, off_thr, off_lm, off_rm, off_d, off_e, stride;
-};
-
-static GemmGeom gemm_geom(int ni, int nl, int w) {
-  GemmGeom g;
-  g.ni = (ni + 1) & ~1;
-  g.nl = (nl + 1) & ~1;
-  g.w = w;
-  size_t o = 8;
-  g.off_feat = o; o += 4 * (size_t)g.ni;
-  g.off_thr = o;  o += 4 * (size_t)g.ni;
-  g.off_lm = o;   o += 8 * (size_t)g.nl;
-  g.off_rm = o;   o += 8 * (size_t)g.nl;
-  g.off_d = o;    o += 4 * (size_t)g.nl;
-  g.off_e = o;    o += 4 * (size_t)g.nl * w;
-  g.stride = (o + 15) & ~size_t(15);
-  return g;
-}
-
-bool gemm_supported(int depth) { return depth <= 6; }
-
-hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m) {
-  const int w = e->leaf_width;
-  int ni = 1, nl = 1;
-  for (int t = t0; t < t1; ++t) {
-    const int64_t a = e->node_offset[t], b = e->node_offset[t + 1];
-    int ci = 0, cl = 0;
-    for (int64_t i = a; i < b; ++i) (e->left[i] == -1 ? cl : ci)++;
-    ni = std::max(ni, ci);
-    nl = std::max(nl, cl);
-  }
-  if (ni > kGemmMaxInternal)
-    return fail(HB_E_UNSUPPORTED, "GEMM: trees with more than 64 internal nodes (use PTT/TT)");
-  const GemmGeom g = gemm_geom(ni, nl, w);
-  const int Tpad = m->n_trees_pad;
-  std::vector<uint8_t> buf((size_t)Tpad * g.stride, 0);
-  std::vector<int32_t> leafmap((size_t)Tpad * g.nl, -1);
-  std::vector<int> ipos, lpos, stack;
-  for (int lt = 0; lt < Tpad; ++lt) {
-    uint8_t *rec = buf.data() + (size_t)lt * g.stride;
-    uint32_t *hdr = reinterpret_cast<uint32_t *>(rec);
-    float *thr = reinterpret_cast<float *>(rec + g.off_thr);
-    uint32_t *feat = reinterpret_cast<uint32_t *>(rec + g.off_feat);
-    uint64_t *lm = reinterpret_cast<uint64_t *>(rec + g.off_lm);
-    uint64_t *rm = reinterpret_cast<uint64_t *>(rec + g.off_rm);
-    uint32_t *D = reinterpret_cast<uint32_t *>(rec + g.off_d);
-    float *E = reinterpret_cast<float *>(rec + g.off_e);
-    for (int i = 0; i < g.ni; ++i) thr[i] = INFINITY;  // padded nodes: C rows are 0
-    for (int j = 0; j < g.nl; ++j) D[j] = 0xFFFFu;      // padded leaves: unreachable D
-    if (lt >= t1 - t0) {
-      D[0] = 0;  // zero tree: column 0 (C = 0, D = 0) always matches, E = 0
-      continue;
-    }
-    const int t = t0 + lt;
-    const int64_t a = e->node_offset[t];
-    const int n = (int)(e->node_offset[t + 1] - a);
-    hdr[0] = (uint32_t)(w == 1 ? (e->tree_output ? e->tree_output[t] : t % e->n_outputs) : 0);
-    // ordered lists I and L (node-id order, Table 3)
-    ipos.assign(n, -1);
-    lpos.assign(n, -1);
-    int ci = 0, cl = 0;
-    for (int i = 0; i < n; ++i) {
-      if (e->left[a + i] != -1) ipos[i] = ci++;
-      else lpos[i] = cl++;
-    }
-    for (int i = 0; i < n; ++i) {
-      if (ipos[i] >= 0) {
-        feat[ipos[i]] = (uint32_t)e->feature[a + i];
-        thr[ipos[i]] = e->threshold[a + i];
-      } else {
-        const int j = lpos[i];
-        for (int k = 0; k < w; ++k) E[(size_t)j * w + k] = e->leaf_value[(a + i) * w + k];
-        leafmap[(size_t)lt * g.nl + j] = i;
-      }
-    }
-    // C: +1 for leaves in the left subtree of internal node i, -1 right.
-    for (int i = 0; i < n; ++i) {
-      if (ipos[i] < 0) continue;
-      for (int side = 0; side < 2; ++side) {
-        stack.assign(1, side == 0 ? e->left[a + i] : e->right[a + i]);
-        while (!stack.empty()) {
-          const int k = stack.back();
-          stack.pop_back();
-          if (e->left[a + k] == -1) {
-            (side == 0 ? lm : rm)[lpos[k]] |= 1ull << ipos[i];
-          } else {
-            stack.push_back(e->left[a + k]);
-            stack.push_back(e->right[a + k]);
-          }
-        }
-      }
-    }
-    for (int j = 0; j < cl; ++j) D[j] = (uint32_t)__builtin_popcountll(lm[j]);
-  }
-  m->stride = g.stride;
-  m->nslots = g.nl;
-  m->gemm_ni = g.ni;
-  m->gemm_nl = g.nl;
-  size_t acct = 0;
-  cudaError_t err = cudaMalloc(&m->d_trees, buf.size());
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(gemm)");
-  m->device_bytes += buf.size();
-  err = cudaMemcpy(m->d_trees, buf.data(), buf.size(), cudaMemcpyHostToDevice);
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm)");
-  err = cudaMalloc(&m->d_leafmap, leafmap.size() * 4);
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(gemm leafmap)");
-  m->device_bytes += leafmap.size() * 4;
-  err = cudaMemcpy(m->d_leafmap, leafmap.data(), leafmap.size() * 4, cudaMemcpyHostToDevice);
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm leafmap)");
-  (void)acct;
-  m->cfg = LaunchCfg();
-  m->cfg.nw = 4;
-  m->cfg.x_smem = 0;
-  m->cfg.t_smem = 0;
-  return HB_OK;
-}
 
 struct GemmParams {
   const float *X;

@@ -32,181 +32,9 @@
 
 #include "hb_device.cuh"
 #include "hb_internal.h"
+#include "hb_layouts.h"
 
 namespace hb {
-
-constexpr int kTcPairs = 8;                 // pairs of trees per group
-constexpr int kTcTrees = 2 * kTcPairs;      // 16 trees per group
-constexpr int kTcCols = 16 * kTcPairs;      // TMEM columns per group
-constexpr int kTcRows = 128;                // rows per CTA tile (UMMA M)
-constexpr float kTcDPad = 99.f;             // unreachable D for padded leaf columns
-
-// Group record (SMEM image), all offsets 16-B aligned:
-//   bimg  [kTcPairs][512 B]   B operand: per pair 16 (N) x 16 (K) bf16, K-major
-//                             core matrices (8 rows x 16 B), LBO = 128, SBO = 256
-//   feat  [kTcTrees][8] u32   feature id of internal node i (pads: 0)
-//   thr   [kTcTrees][8] f32   threshold (pads: +Inf)
-//   dval  [kTcTrees][8] f32   D_j (pads: 99)
-//   tout  [kTcTrees]    u32   tree_output
-//   e     [kTcTrees][8][w] f32
-struct TcGeom {
-  int w;
-  size_t off_b, off_feat, off_thr, off_d, off_tout, off_e, stride;
-};
-
-static TcGeom tc_geom(int w) {
-  TcGeom g;
-  g.w = w;
-  size_t o = 0;
-  g.off_b = o;    o += 512 * kTcPairs;
-  g.off_feat = o; o += 4 * 8 * kTcTrees;
-  g.off_thr = o;  o += 4 * 8 * kTcTrees;
-  g.off_d = o;    o += 4 * 8 * kTcTrees;
-  g.off_tout = o; o += 4 * kTcTrees;
-  g.off_e = o;    o += 4 * 8 * (size_t)kTcTrees * w;
-  g.stride = (o + 127) & ~size_t(127);
-  return g;
-}
-
-static inline uint16_t bf16_bits(float f) {  // exact for {-1, 0, 1}
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  return (uint16_t)(u >> 16);
-}
-
-bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1) {
-  for (int t = t0; t < t1; ++t) {
-    const int64_t a = e->node_offset[t], b = e->node_offset[t + 1];
-    int ni = 0, nl = 0;
-    for (int64_t i = a; i < b; ++i) (e->left[i] == -1 ? nl : ni)++;
-    if (ni > 8 || nl > 8) return false;
-  }
-  return true;
-}
-
-hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
-  const int w = e->leaf_width;
-  const TcGeom g = tc_geom(w);
-  const int T = t1 - t0;
-  const int ngroups = (T + kTcTrees - 1) / kTcTrees;
-  // feature-selection injection: the X tile holds used features only
-  std::vector<int32_t> remap(e->n_features, -1), used;
-  for (int t = t0; t < t1; ++t)
-    for (int64_t i = e->node_offset[t]; i < e->node_offset[t + 1]; ++i)
-      if (e->left[i] != -1) remap[e->feature[i]] = 1;
-  for (int f = 0; f < e->n_features; ++f)
-    if (remap[f] == 1) {
-      remap[f] = (int32_t)used.size();
-      used.push_back(f);
-    }
-  if (used.empty()) used.push_back(0), remap[0] = 0;
-  // X slices of 4 warps in SMEM when the used columns fit (else X is read
-  // from global with original feature ids)
-  const bool fits = 4L * (long)used.size() * 128 <= 160L * 1024;
-  const bool compact = fits && (int)used.size() < e->n_features;
-  if (!compact)
-    for (int f = 0; f < e->n_features; ++f) remap[f] = f;
-  std::vector<uint8_t> buf((size_t)ngroups * g.stride, 0);
-  std::vector<int32_t> leafmap((size_t)ngroups * kTcTrees * 8, -1);
-  std::vector<int> ipos, lpos, stack;
-  for (int gi = 0; gi < ngroups; ++gi) {
-    uint8_t *rec = buf.data() + (size_t)gi * g.stride;
-    uint16_t *bimg = reinterpret_cast<uint16_t *>(rec + g.off_b);
-    uint32_t *feat = reinterpret_cast<uint32_t *>(rec + g.off_feat);
-    float *thr = reinterpret_cast<float *>(rec + g.off_thr);
-    float *dval = reinterpret_cast<float *>(rec + g.off_d);
-    uint32_t *tout = reinterpret_cast<uint32_t *>(rec + g.off_tout);
-    float *E = reinterpret_cast<float *>(rec + g.off_e);
-    for (int q = 0; q < kTcTrees; ++q) {
-      for (int i = 0; i < 8; ++i) {
-        thr[q * 8 + i] = INFINITY;
-        dval[q * 8 + i] = kTcDPad;
-      }
-      const int lt = gi * kTcTrees + q;
-      if (lt >= T) {  // zero tree: column 0 (C = 0, D = 0) always matches, E = 0
-        dval[q * 8] = 0.f;
-        continue;
-      }
-      const int t = t0 + lt;
-      const int64_t a = e->node_offset[t];
-      const int n = (int)(e->node_offset[t + 1] - a);
-      tout[q] = (uint32_t)(w == 1 ? (e->tree_output ? e->tree_output[t] : t % e->n_outputs) : 0);
-      ipos.assign(n, -1);
-      lpos.assign(n, -1);
-      int ci = 0, cl = 0;
-      for (int i = 0; i < n; ++i) {
-        if (e->left[a + i] != -1) ipos[i] = ci++;
-        else lpos[i] = cl++;
-      }
-      for (int i = 0; i < n; ++i) {
-        if (ipos[i] >= 0) {
-          feat[q * 8 + ipos[i]] = (uint32_t)remap[e->feature[a + i]];
-          thr[q * 8 + ipos[i]] = e->threshold[a + i];
-        } else {
-          for (int k = 0; k < w; ++k)
-            E[((size_t)q * 8 + lpos[i]) * w + k] = e->leaf_value[(a + i) * w + k];
-          leafmap[(size_t)lt * 8 + lpos[i]] = i;
-        }
-      }
-      // C (Table 3): +1 left subtree, -1 right subtree; D_j = #left edges (R5)
-      int dcount[8] = {0};
-      const int pair = q >> 1, half = q & 1;
-      for (int i = 0; i < n; ++i) {
-        if (ipos[i] < 0) continue;
-        for (int side = 0; side < 2; ++side) {
-          stack.assign(1, side == 0 ? e->left[a + i] : e->right[a + i]);
-          while (!stack.empty()) {
-            const int k = stack.back();
-            stack.pop_back();
-            if (e->left[a + k] == -1) {
-              const int j = lpos[k];
-              // B[nrow][kcol] with nrow = leaf column (half*8 + j), kcol = node (half*8 + i)
-              const int nrow = half * 8 + j, kcol = half * 8 + ipos[i];
-              const int core = (nrow >> 3) * 2 + (kcol >> 3);  // SBO = 256 B = 2 cores, LBO = 128 B
-              bimg[pair * 256 + core * 64 + (nrow & 7) * 8 + (kcol & 7)] =
-                  bf16_bits(side == 0 ? 1.f : -1.f);
-              if (side == 0) dcount[j]++;
-            } else {
-              stack.push_back(e->left[a + k]);
-              stack.push_back(e->right[a + k]);
-            }
-          }
-        }
-      }
-      for (int j = 0; j < cl; ++j) dval[q * 8 + j] = (float)dcount[j];
-    }
-  }
-  m->stride = g.stride;
-  m->nslots = 8;
-  m->n_trees_pad = ngroups * kTcTrees;
-  cudaError_t err = cudaMalloc(&m->d_trees, buf.size());
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(gemm_tc)");
-  m->device_bytes += buf.size();
-  err = cudaMemcpy(m->d_trees, buf.data(), buf.size(), cudaMemcpyHostToDevice);
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm_tc)");
-  err = cudaMalloc(&m->d_leafmap, leafmap.size() * 4);
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMalloc(gemm_tc leafmap)");
-  m->device_bytes += leafmap.size() * 4;
-  err = cudaMemcpy(m->d_leafmap, leafmap.data(), leafmap.size() * 4, cudaMemcpyHostToDevice);
-  if (err != cudaSuccess) return cuda_fail(err, "cudaMemcpy(gemm_tc leafmap)");
-  if (compact) {
-    if ((err = cudaMalloc(&m->d_fmap, used.size() * 4)) != cudaSuccess) return cuda_fail(err, "cudaMalloc(fmap)");
-    m->device_bytes += used.size() * 4;
-    if ((err = cudaMemcpy(m->d_fmap, used.data(), used.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
-      return cuda_fail(err, "cudaMemcpy(fmap)");
-  }
-  m->n_xf = compact ? (int)used.size() : e->n_features;
-  const long xb = 4L * m->n_xf * 128;
-  m->cfg = LaunchCfg();
-  m->cfg.nw = 4;
-  m->cfg.x_smem = fits ? 1 : 0;
-  m->cfg.t_smem = 1;
-  m->cfg.smem_bytes = (int)((m->cfg.x_smem ? xb : 0) + 2 * g.stride + kTcRows * 16 * 2 * kTcPairs + 64);
-  // 4 warps per CTA: fill the SM with up to 4 CTAs (TMEM: 4 x 128 columns = 512)
-  m->cfg.ctas_per_sm = std::max(1, std::min(4, (int)(kSmemBudget / std::max(1, m->cfg.smem_bytes))));
-  m->gemm_tc = 1;
-  return HB_OK;
-}
 
 // ------------------------------------------------------------------ device
 namespace tc {

@@ -1,4 +1,4 @@
-// hb_host.cu — the C ABI (include/hb.h): validation, strategy selection
+// hb_host.cpp — the C ABI (include/hb.h): validation, strategy selection
 // (Sec. 5.1), layout compilation for the three strategies
 // (Tables 3/5/6) and the scoring entry points.
 #include <cuda_runtime.h>
@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "hb_internal.h"
+#include "hb_layouts.h"
 
 namespace hb {
 
@@ -49,6 +50,7 @@ struct DeviceGuard {
   int prev = -1;
   bool ok = true;
   explicit DeviceGuard(int dev) {
+    if (dev < 0) return;           // host-only compile: no CUDA call at all
     if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
     if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
   }
@@ -334,6 +336,108 @@ static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLa
   return HB_OK;
 }
 
+// Wide-row TT records (tt_wide_kernel). Alg. 2's per-node
+// tensors (Table 5: N_F, N_T, N_L, N_R, N_C) folded per INTERNAL node into one
+// 16-B record {N_F | leafL << 16 | leafR << 17, N_T, payload_L, payload_R},
+// in BFS order of the internal nodes. A payload is the child's record index,
+// or, when the child is a leaf (flag set), its value bits (w == 1) or its leaf
+// slot (w > 1; values at vals_off). So a walk ends on the record whose chosen
+// child is a leaf, carrying the value: D_k dependent loads for a leaf at depth
+// D_k instead of D_k + 1 (leaf self-loop) + 1 (N_C gather). Per tree:
+// 16-B header {n_records, ids_off, tree_output, vals_off}, the records, then
+// ids[n_records][2] (original ids of the leaf children, read only by the LEAF /
+// LEAF_HASH outputs) and the leaf values (w > 1). Trees are packed without
+// padding; toff[t] is the tree's offset in 16-B units. A single-leaf tree gets
+// one record {feature 0, +Inf, leaf, leaf}: both children are the leaf, so the
+// compare (true for finite x, false for +Inf / NaN) cannot matter.
+struct WideLayout {
+  std::vector<uint32_t> words;   // the packed trees, 16-B aligned
+  std::vector<uint32_t> toff;    // [Tpad] tree offset in 16-B units
+};
+
+static hb_status build_ttw(const hb_ensemble *e, int t0, int t1, int Tpad, const FeatureMap *fm,
+                           WideLayout *W) {
+  const int w = e->leaf_width;
+  const uint32_t pinf = f2u(INFINITY);
+  std::vector<int> q, recid, slot;
+  W->words.clear();
+  W->toff.assign(Tpad, 0);
+  for (int lt = 0; lt < Tpad; ++lt) {
+    const size_t base = W->words.size();
+    if ((base / 4) > 0xFFFFFFFFull) return fail(HB_E_UNSUPPORTED, "TT: model larger than 64 GB");
+    W->toff[lt] = (uint32_t)(base / 4);
+    if (lt >= t1 - t0) {   // padding tree: one record, both children a zero leaf
+      W->words.insert(W->words.end(), {1u, 32u, 0u, 48u});   // header (byte offsets)
+      W->words.insert(W->words.end(), {0u | 3u << 16, pinf, 0u, 0u});
+      W->words.insert(W->words.end(), {0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u});   // ids (never read)
+      for (int k = 0; k < 4; ++k) W->words.push_back(0u);                  // w <= 4 zero values
+      if (w > 4) W->words.resize(W->words.size() + ((size_t)w - 4 + 3) / 4 * 4, 0u);
+      continue;
+    }
+    const int t = t0 + lt;
+    const int64_t a = e->node_offset[t];
+    const int n = (int)(e->node_offset[t + 1] - a);
+    // BFS over internal nodes; record ids in that order, leaf slots in order
+    // of appearance
+    q.assign(1, 0);
+    recid.assign(n, -1);
+    slot.assign(n, -1);
+    int nrec = 0, nleaf = 0;
+    const bool root_leaf = e->left[a] == -1;
+    if (!root_leaf) recid[0] = nrec++;
+    for (size_t k = 0; k < q.size(); ++k) {
+      const int o = q[k];
+      if (e->left[a + o] == -1) {
+        slot[o] = nleaf++;
+        continue;
+      }
+      for (int c : {e->left[a + o], e->right[a + o]}) {
+        if (e->left[a + c] != -1) recid[c] = nrec++;
+        q.push_back(c);
+      }
+    }
+    if (root_leaf) nrec = 1;
+    const uint32_t ids_off = 4 + 4 * (uint32_t)nrec;                    // words
+    const uint32_t vals_off = ids_off + ((2 * (uint32_t)nrec + 3) & ~3u);
+    const size_t vals_words = w == 1 ? 0 : (((size_t)nleaf * w + 3) & ~(size_t)3);
+    W->words.resize(base + vals_off + vals_words, 0u);
+    uint32_t *T = W->words.data() + base;
+    T[0] = (uint32_t)nrec;
+    T[1] = ids_off * 4;
+    T[2] = (uint32_t)(w == 1 ? tree_out(e, t) : 0);
+    T[3] = vals_off * 4;
+    auto payload = [&](int c) -> uint32_t {
+      if (e->left[a + c] != -1) return (uint32_t)recid[c];
+      return w == 1 ? f2u(e->leaf_value[a + c]) : (uint32_t)slot[c];
+    };
+    if (root_leaf) {
+      uint32_t *r = T + 4;
+      r[0] = 0u | 3u << 16;
+      r[1] = pinf;
+      r[2] = r[3] = payload(0);
+      T[ids_off] = T[ids_off + 1] = 0u;
+    } else {
+      for (int o = 0; o < n; ++o) {
+        if (recid[o] < 0) continue;
+        uint32_t *r = T + 4 + 4 * recid[o];
+        const int L = e->left[a + o], Rc = e->right[a + o];
+        const uint32_t f = (uint32_t)(fm ? fm->remap[e->feature[a + o]] : e->feature[a + o]);
+        r[0] = f | (e->left[a + L] == -1 ? 1u << 16 : 0u) | (e->left[a + Rc] == -1 ? 1u << 17 : 0u);
+        r[1] = f2u(e->threshold[a + o]);
+        r[2] = payload(L);
+        r[3] = payload(Rc);
+        T[ids_off + 2 * recid[o]] = e->left[a + L] == -1 ? (uint32_t)L : 0xFFFFFFFFu;
+        T[ids_off + 2 * recid[o] + 1] = e->left[a + Rc] == -1 ? (uint32_t)Rc : 0xFFFFFFFFu;
+      }
+    }
+    if (w > 1)
+      for (int o = 0; o < n; ++o)
+        if (slot[o] >= 0)
+          for (int k = 0; k < w; ++k) T[vals_off + (size_t)slot[o] * w + k] = f2u(e->leaf_value[(a + o) * w + k]);
+  }
+  return HB_OK;
+}
+
 static int env_int(const char *name, int dflt) {
   const char *v = std::getenv(name);
   if (!v || !*v) return dflt;
@@ -412,23 +516,42 @@ static int select_strategy(int D) {
 
 static void free_model(Model *m) {
   if (!m) return;
-  DeviceGuard g(m->device);
-  cudaFree(m->d_trees);
-  cudaFree(m->d_leafmap);
-  cudaFree(m->d_scale);
-  cudaFree(m->d_base);
-  cudaFree(m->d_gemm);
-  cudaFree(m->d_aux);
-  cudaFree(m->sb_own_trees);
-  cudaFree(m->sb_own_leafmap);
-  cudaFree(m->d_fmap);
-  cudaFree(m->d_rb);
-  if (m->mempool) cudaMemPoolDestroy(m->mempool);   // deferred until pending frees complete
+  void *bufs[] = {m->d_trees, m->d_leafmap, m->d_scale, m->d_base, m->d_gemm, m->d_aux,
+                  m->sb_own_trees, m->sb_own_leafmap, m->d_fmap, m->d_rb, m->d_ttw, m->d_ttw_off};
+  if (m->host_only) {
+    for (void *b : bufs) std::free(b);
+  } else {
+    DeviceGuard g(m->device);
+    for (void *b : bufs) cudaFree(b);
+    if (m->mempool) cudaMemPoolDestroy(m->mempool);   // deferred until pending frees complete
+  }
   delete m;
 }
 
+void free_model_any(Model *m) { free_model(m); }
+
+hb_status dev_upload(Model *m, const void *src, size_t bytes, void **dst) {
+  const size_t alloc = std::max<size_t>(bytes, 16);
+  if (m->host_only) {
+    *dst = std::malloc(alloc);
+    if (!*dst) return fail(HB_E_OOM, "malloc(host-only model)");
+    std::memset(*dst, 0, alloc);
+    if (bytes) std::memcpy(*dst, src, bytes);
+    m->device_bytes += alloc;
+    return HB_OK;
+  }
+  cudaError_t e = cudaMalloc(dst, alloc);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(model)");
+  m->device_bytes += alloc;
+  if (bytes) {
+    e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(model)");
+  }
+  return HB_OK;
+}
+
 hb_status ensure_pool(Model *m) {
-  if (m->mempool) return HB_OK;
+  if (m->mempool || m->host_only) return HB_OK;
   cudaMemPoolProps props = {};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;
@@ -455,20 +578,12 @@ hb_status scratch_alloc(const Model &m, size_t bytes, cudaStream_t s, void **p) 
 }
 
 template <typename T>
-static hb_status upload(const std::vector<T> &h, T **d, size_t *acct) {
-  const size_t bytes = std::max<size_t>(h.size() * sizeof(T), 16);
-  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(d), bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(model)");
-  *acct += bytes;
-  if (!h.empty()) {
-    e = cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(model)");
-  }
-  return HB_OK;
+static hb_status upload(Model *m, const std::vector<T> &h, T **d) {
+  return dev_upload(m, h.data(), h.size() * sizeof(T), reinterpret_cast<void **>(d));
 }
 
 static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy, int device,
-                              hb_model **out) {
+                              Model **out, bool host_only = false) {
   if (!out) return fail(HB_E_INVALID, "out is NULL");
   *out = nullptr;
   std::vector<TreeInfo> info;
@@ -480,12 +595,13 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   const int K = e->n_outputs;
   if (K > kMaxOutputs) return fail(HB_E_UNSUPPORTED, "n_outputs > 16 is not supported by this build");
   int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+  if (!host_only && (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev))
     return fail(HB_E_INVALID, "device " + std::to_string(device) + " is not a CUDA device");
-  DeviceGuard guard(device);
-  if (!guard.ok) return fail(HB_E_CUDA, "cudaSetDevice failed");
+  DeviceGuard guard(host_only ? -1 : device);
+  if (!host_only && !guard.ok) return fail(HB_E_CUDA, "cudaSetDevice failed");
 
   std::unique_ptr<Model, void (*)(Model *)> m(new Model(), free_model);
+  m->host_only = host_only;
   m->device = device;
   m->n_trees = t1 - t0;
   m->tree_begin = t0;
@@ -516,7 +632,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     const FeatureMap fmap = feature_map(e, t0, t1);
     m->n_xf = (int)fmap.used.size();
     if (!fmap.identity) {
-      st = upload(fmap.used, &m->d_fmap, &m->device_bytes);
+      st = upload(m.get(), fmap.used, &m->d_fmap);
       if (st != HB_OK) return st;
     }
     if (strat == HB_STRATEGY_PTT && D <= kPttMaxDepth) {
@@ -574,22 +690,25 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.t_smem = 0;
         c.ch = kTreeGroup;
         m->cfg = c;
+        WideLayout W;
+        st = build_ttw(e, t0, t1, m->n_trees_pad, &fmap, &W);
+        if (st != HB_OK) return st;
         // models larger than L2: walk them in tree chunks whose records stay
-        // L2-resident (HB_TT_CHUNK: -1 auto, N trees, 0 off). Auto size: the
-        // chunk's actual node + leaf bytes (not the padded stride) = 0.4 x L2
-        // — C5, 10k trees on one GPU (measured, 100K rows): 1000 / 1500 /
-        // 2500 / 3336 / 5000 trees per chunk = 15.5 / 14.7 / 13.7 / 15.1 /
-        // 17.2 ms; one launch over all trees 17.2 ms
-        int l2_bytes = 0;
-        cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
-        const bool big = (double)m->n_trees_pad * (double)L.stride > 0.75 * (double)l2_bytes;
+        // L2-resident (HB_TT_CHUNK: -1 auto, N trees, 0 off). The walk reads
+        // only the 16-B records (not the leaf-id tables), so the chunk is
+        // sized on record bytes: HB_TT_CHUNK_L2 (percent of L2, default 40)
+        // of records per chunk when they exceed HB_TT_BIG_L2 (default 50)
+        // percent of L2
+        int l2_bytes = 126 * 1024 * 1024;   // B200; the host-only compile assumes it
+        if (!host_only) cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
+        double rec_bytes = 0;
+        for (int lt = 0; lt < m->n_trees; ++lt) rec_bytes += 16.0 * W.words[(size_t)W.toff[lt] * 4];
+        const bool big = rec_bytes > 0.01 * env_int("HB_TT_BIG_L2", 50) * (double)l2_bytes;
         const int want_chunk = env_int("HB_TT_CHUNK", -1);
         if (want_chunk > 0 || (want_chunk == -1 && big)) {
-          double bytes = 0;
-          for (int t = t0; t < t1; ++t)
-            bytes += (double)(e->node_offset[t + 1] - e->node_offset[t]) * (8.0 + 4.0 * e->leaf_width);
-          const double per_tree = std::max(1.0, bytes / std::max(1, t1 - t0));
-          const int autoc = (int)(0.4 * (double)l2_bytes / per_tree) & ~(kTreeGroup - 1);
+          const double per_tree = std::max(1.0, rec_bytes / std::max(1, m->n_trees));
+          const int autoc = (int)(0.01 * env_int("HB_TT_CHUNK_L2", 40) * (double)l2_bytes / per_tree) &
+                            ~(kTreeGroup - 1);
           m->tt_chunk = std::max(kTreeGroup, want_chunk > 0 ? want_chunk : autoc);
           if (m->tt_chunk >= m->n_trees_pad) m->tt_chunk = 0;   // one chunk: one plain launch
         }
@@ -597,14 +716,19 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
           st = ensure_pool(m.get());
           if (st != HB_OK) return st;
         }
+        st = upload(m.get(), W.words, reinterpret_cast<uint32_t **>(&m->d_ttw));
+        if (st != HB_OK) return st;
+        st = upload(m.get(), W.toff, &m->d_ttw_off);
+        if (st != HB_OK) return st;
+        m->ttw_bytes = W.words.size() * 4;
       }
     }
     if (!done) {
       m->stride = L.stride;
       m->nslots = L.nslots;
-      st = upload(L.trees, reinterpret_cast<uint8_t **>(&m->d_trees), &m->device_bytes);
+      st = upload(m.get(), L.trees, reinterpret_cast<uint8_t **>(&m->d_trees));
       if (st != HB_OK) return st;
-      st = upload(L.leafmap, &m->d_leafmap, &m->device_bytes);
+      st = upload(m.get(), L.leafmap, &m->d_leafmap);
       if (st != HB_OK) return st;
     }
   }
@@ -638,10 +762,10 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
     build_ptt(e, t0, D, order, &S);
     m->sb_nrec = (int)order.local.size();
     uint8_t *dt = nullptr;
-    st = upload(S.trees, &dt, &m->device_bytes);
+    st = upload(m.get(), S.trees, &dt);
     if (st != HB_OK) return st;
     m->sb_own_trees = dt;
-    st = upload(S.leafmap, &m->sb_own_leafmap, &m->device_bytes);
+    st = upload(m.get(), S.leafmap, &m->sb_own_leafmap);
     if (st != HB_OK) return st;
     m->sb_trees = dt;
     m->sb_leafmap = m->sb_own_leafmap;
@@ -668,12 +792,16 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   if (e->base_score)
     for (int k = 0; k < K; ++k) base[k] = e->base_score[k];
   base[K] = e->post == HB_POST_ISOLATION ? e->post_param : 1.f;
-  st = upload(div, &m->d_scale, &m->device_bytes);
+  st = upload(m.get(), div, &m->d_scale);
   if (st != HB_OK) return st;
-  st = upload(base, &m->d_base, &m->device_bytes);
+  st = upload(m.get(), base, &m->d_base);
   if (st != HB_OK) return st;
-  *out = reinterpret_cast<hb_model *>(m.release());
+  *out = m.release();
   return HB_OK;
+}
+
+hb_status compile_model_host(const hb_ensemble *e, int t0, int t1, int strategy, Model **out) {
+  return compile_impl(e, t0, t1, strategy, 0, out, true);
 }
 
 static const Model *M(const hb_model *m) { return reinterpret_cast<const Model *>(m); }
@@ -846,12 +974,12 @@ hb_status hb_validate(const hb_ensemble *e) { return validate_impl(e, nullptr); 
 
 hb_status hb_compile(const hb_ensemble *e, int32_t strategy, int32_t device, hb_model **out) {
   if (!e) return fail(HB_E_INVALID, "ensemble is NULL");
-  return compile_impl(e, 0, e->n_trees, strategy, device, out);
+  return compile_impl(e, 0, e->n_trees, strategy, device, reinterpret_cast<Model **>(out));
 }
 
 hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tree_end,
                            int32_t strategy, int32_t device, hb_model **out) {
-  return compile_impl(e, tree_begin, tree_end, strategy, device, out);
+  return compile_impl(e, tree_begin, tree_end, strategy, device, reinterpret_cast<Model **>(out));
 }
 
 hb_status hb_predict_ex(const hb_model *m, const float *X, int64_t n, int64_t ldx, int32_t kind,

@@ -95,9 +95,17 @@ struct Model {
   int n_xf = 0;
 
   int tt_chunk = 0;          // tt_wide_kernel: trees per L2-resident chunk (0: one launch)
+  // tt_wide_kernel records (hb_host.cpp build_ttw): packed trees of 16-B
+  // internal-node records + per-tree offsets in 16-B units
+  void *d_ttw = nullptr;
+  uint32_t *d_ttw_off = nullptr;
+  size_t ttw_bytes = 0;
 
   size_t device_bytes = 0;
   LaunchCfg cfg;
+  // host-only compile (compile_model_host, the ASan/UBSan fuzz build): every
+  // "device" buffer is host memory (malloc) and no CUDA call is made
+  bool host_only = false;
 };
 
 // thread-local error text
@@ -131,7 +139,7 @@ hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m);
 bool gemm_tc_eligible(const hb_ensemble *e, int t0, int t1);
 hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m);
 hb_status launch_gemm_tc(const Model &m, const RunArgs &a);
-// record order of the PTT layouts (hb_host.cu ptt_order)
+// record order of the PTT layouts (hb_host.cpp ptt_order)
 struct TreeOrder {
   std::vector<int> local;   // per record: local tree id (t - t0), -1 = zero tree
   std::vector<int> cls;     // per record: output class
@@ -161,8 +169,14 @@ hb_status launch_tt(const Model &m, const RunArgs &a);
 hb_status launch_gemm(const Model &m, const RunArgs &a);
 hb_status launch_finalize(const Model &m, const RunArgs &a);
 hb_status launch_small_batch(const Model &m, const RunArgs &a);
-size_t tt_wide_smem(int F, int R, int nwarps, int nacc);
-// model-owned stream-ordered scratch (hb_host.cu): a pool created at compile
+// copy a compiled layout to the model's device (host memory for host-only
+// models); accounts the bytes in m->device_bytes
+hb_status dev_upload(Model *m, const void *src, size_t bytes, void **dst);
+// the whole compile (validation, strategy, layouts) without a GPU, for the
+// sanitizer fuzz build; the model's buffers are host memory
+hb_status compile_model_host(const hb_ensemble *e, int t0, int t1, int strategy, Model **out);
+void free_model_any(Model *m);
+// model-owned stream-ordered scratch (hb_host.cpp): a pool created at compile
 // time with release threshold UINT64_MAX, so per-call allocations reuse warm
 // memory; under stream capture the device default pool is used instead
 hb_status ensure_pool(Model *m);

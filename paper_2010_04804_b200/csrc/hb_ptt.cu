@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
             }
           }
           if (NACC > 1 && p.w == 1) {
-            // per-class records are ordered by class in groups of G (hb_host.cu
+            // per-class records are ordered by class in groups of G (hb_host.cpp
             // ptt_order): one output selection per group instead of per tree
             const uint32_t k0 = dev::lds_u32(tb[0]) & 0xFFu;
 #pragma unroll

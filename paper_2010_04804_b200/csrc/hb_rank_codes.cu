@@ -40,13 +40,13 @@
 #include <vector>
 
 #include "hb_internal.h"
+#include "hb_layouts.h"
 
 namespace hb {
 
 namespace {
 
 constexpr int kRcWarps = 8;                 // warps per CTA of the pre-pass
-constexpr uint32_t kRcSmemMax = 200 * 1024; // largest per-CTA table budget
 constexpr int kRcBatch = 16;                // X loads in flight together per lane
 constexpr int kRcRows = 4;                  // 32-row blocks per warp iteration (HB_RC_ROWS=8: eight)
 
@@ -392,138 +392,7 @@ RcFn staged_pick(bool le, int cw, int rb, bool one) {
   return le ? staged_pick_rb<true, 16, false>(rb) : staged_pick_rb<false, 16, false>(rb);
 }
 
-// Host twin of the bucket map in rank_code(): same fp32 operations, same
-// order, no contraction (volatile intermediates).
-uint32_t host_bucket(float x, float lo, float hi, float s, uint32_t B) {
-  volatile float xc = std::fmin(std::fmax(x, lo), hi);
-  volatile float d = xc - lo;
-  volatile float y = d * s;
-  const float yy = std::fmin((float)y, (float)(B - 1u));
-  return (uint32_t)yy;
-}
-
 }  // namespace
-
-// Bucket tables for the sorted distinct thresholds of each compact feature
-// (sorted[c], feature id orig[c]); words group 1 (CW 32) or 2 (CW 16) features.
-hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
-                             int cw, RankBuckets *out, size_t cap_bytes) {
-  // per-CTA table budget: 48 KB -> 4 CTAs (32 warps) per SM (HB_RC_SMEM_KB overrides)
-  const char *ev = std::getenv("HB_RC_SMEM_KB");
-  const size_t cap = cap_bytes ? cap_bytes
-                               : std::min<size_t>(kRcSmemMax, (ev && *ev ? (size_t)std::atoi(ev) : 48) * 1024);
-  out->smem_cap = cap;
-  const int n_fc = (int)sorted.size();
-  const int per_word = cw == 32 ? 1 : 2;
-  const int n_words = (n_fc + per_word - 1) / per_word;
-  RankBuckets R;
-  R.n_words = n_words;
-  R.feat.assign((size_t)n_fc * 8, 0u);
-  std::vector<std::vector<uint8_t>> tabs(n_fc);
-  for (int c = 0; c < n_fc; ++c) {
-    const std::vector<float> &u = sorted[c];
-    const uint32_t m = (uint32_t)u.size();
-    float lo = 0.f, hi = 0.f;
-    bool any = false;
-    for (float v : u)
-      if (std::isfinite(v)) {
-        if (!any) lo = v;
-        hi = v;
-        any = true;
-      }
-    // <= 2 thresholds per bucket on average (HB_RC_DENSITY=d: <= 2/d)
-    static const int dens = [] {
-      const char *e = std::getenv("HB_RC_DENSITY");
-      return e && *e ? std::max(1, std::atoi(e)) : 1;
-    }();
-    uint32_t B = 1;
-    while (2 * B < m * (uint32_t)dens && B < 16384u) B <<= 1;
-    float s = 0.f;
-    if (hi > lo) {
-      const float range = hi - lo;
-      s = std::isfinite(range) ? (float)B / range : (float)B / FLT_MAX;
-      if (!(s <= FLT_MAX)) s = FLT_MAX;     // tiny range: keep s finite (0 * s must stay 0)
-      if (!(s > 0.f)) s = FLT_MIN;
-    } else {
-      B = 1;
-    }
-    std::vector<uint32_t> start(B + 1, 0);
-    std::vector<uint32_t> bk(m);
-    for (uint32_t j = 0; j < m; ++j) bk[j] = host_bucket(u[j], lo, hi, s, B);
-    uint32_t maxocc = 0;
-    {
-      uint32_t j = 0;
-      for (uint32_t b = 0; b <= B; ++b) {
-        while (j < m && bk[j] < b) ++j;
-        start[b] = j;
-      }
-      for (uint32_t b = 0; b < B; ++b) maxocc = std::max(maxocc, start[b + 1] - start[b]);
-    }
-    uint32_t S = 0;
-    while ((1u << S) <= maxocc) ++S;        // bit_length(maxocc) search steps
-    const size_t sbytes = (size_t)B * 4;
-    const size_t ubytes = ((size_t)(m + 1) * 4);
-    std::vector<uint8_t> t(sbytes + ubytes, 0);
-    for (uint32_t b = 0; b < B; ++b) {
-      const uint32_t v = start[b] | ((start[b + 1] - start[b]) << 16);
-      std::memcpy(t.data() + 4 * b, &v, 4);
-    }
-    std::memcpy(t.data() + sbytes, u.data(), (size_t)m * 4);
-    const float pad = INFINITY;
-    std::memcpy(t.data() + sbytes + (size_t)m * 4, &pad, 4);
-    tabs[c] = std::move(t);
-    uint32_t *fm = R.feat.data() + (size_t)c * 8;
-    fm[0] = (uint32_t)orig[c];
-    fm[1] = B;
-    fm[2] = S;
-    fm[3] = 0;                                 // start offset: set when grouped
-    std::memcpy(&fm[4], &lo, 4);
-    std::memcpy(&fm[5], &hi, 4);
-    std::memcpy(&fm[6], &s, 4);
-    fm[7] = (uint32_t)sbytes;                  // u offset relative to start; rebased below
-  }
-  // groups of whole words, <= cap bytes each (an oversized word is a
-  // group of its own and is searched from global memory)
-  size_t goff = 0, gbytes = 0;
-  int wbeg = 0;
-  auto close = [&](int wend) {
-    // X columns the group's features span (the staged kernel copies them)
-    int clo = INT32_MAX, chi = -1;
-    for (int c = wbeg * per_word; c < std::min(wend * per_word, n_fc); ++c) {
-      clo = std::min(clo, orig[c]);
-      chi = std::max(chi, orig[c]);
-    }
-    const uint32_t ncols = chi >= clo ? (uint32_t)(chi - clo + 1) : 0u;
-    R.groups.insert(R.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)wbeg, (uint32_t)wend,
-                                     (uint32_t)(chi >= clo ? clo : 0), ncols, ncols | 1u, 0u});
-    R.max_span = std::max<uint32_t>(R.max_span, ncols);
-    if (gbytes > cap) R.any_global = true;
-    R.max_group_bytes = std::max(R.max_group_bytes, gbytes <= cap ? gbytes : (size_t)0);
-    goff += gbytes;
-    gbytes = 0;
-    wbeg = wend;
-    R.n_groups++;
-  };
-  for (int wd = 0; wd < n_words; ++wd) {
-    size_t wb = 0;
-    for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
-    if (gbytes > 0 && gbytes + wb > cap) close(wd);
-    for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) {
-      const int c = wd * per_word + q;
-      uint32_t *fm = R.feat.data() + (size_t)c * 8;
-      fm[3] = (uint32_t)gbytes;
-      fm[7] += (uint32_t)gbytes;
-      const size_t tb = (tabs[c].size() + 15) & ~size_t(15);
-      tabs[c].resize(tb, 0);
-      R.pool.insert(R.pool.end(), tabs[c].begin(), tabs[c].end());
-      gbytes += tb;
-    }
-  }
-  if (gbytes) close(n_words);
-  R.smem_cap = cap;
-  *out = std::move(R);
-  return HB_OK;
-}
 
 int sm_count(int device);
 

@@ -17,6 +17,7 @@
 
 #include "hb_device.cuh"
 #include "hb_internal.h"
+#include "hb_layouts.h"
 
 namespace hb {
 
@@ -35,6 +36,8 @@ struct TtParams {
   void *out;
   int nw, ns, ch, ntiles, x_smem, t_smem;
   int x_prefetch;         // tt_wide_kernel: L2 prefetch of the next row tile
+  const uint4 *ttw;       // tt_wide_kernel: packed 16-B records (hb_host.cpp build_ttw)
+  const uint32_t *toff;   // tt_wide_kernel: tree offsets in 16-B units
   // tt_wide_kernel over one tree chunk of a model larger than L2 (launch_tt):
   int accumulate;         // RAW64 / LEAF_HASH outputs are added to, not written
   int leaf_stride;        // LEAF output row stride (the model's tree count)
@@ -194,28 +197,38 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // whose records do not fit SMEM). A CTA owns R rows whose X tile lives in SMEM
 // feature-major (xs[f*R + r]); lane = (tree slot, row) with 32/R tree slots per
 // warp, and all warps of the CTA walk disjoint trees of the same R rows. Node
-// records come through L1/L2 (__ldg): the top levels of a tree are shared by
-// the R rows and hit L1. Each lane walks G trees at once (memory-level
-// parallelism) and the walk stops early once every lane of the warp sits on a
-// leaf (the self-loop makes further iterations no-ops). Per-row sums
-// are combined with warp shuffles and one SMEM pass in a fixed order.
+// records (16 B per internal node with both children's payloads, hb_host.cpp
+// build_ttw: a walk to a leaf at depth D_k is D_k dependent loads, the last
+// one carrying the leaf value) come through L1/L2 (__ldg): the top levels of a
+// tree are shared by the R rows and hit L1. Each lane walks G trees at once
+// (memory-level parallelism); finished walks issue no loads and the group ends
+// once every walk of the warp reached a leaf (the fixed TREE_DEPTH loop of
+// Alg. 2 with its leaf self-loops, cut short). Per-row sums are
+// combined with warp shuffles and one SMEM pass in a fixed order.
 // X tile layout: plain xs[f*R + r], so the R lanes of one tree slot (distinct
 // rows) always read distinct banks whatever features their walks test; only
 // lanes of different tree slots on the same row can meet (<= 32/R-way). The
 // fill gives the 32/R row groups of a warp different 4-feature chunks and
 // rotates their store order so a warp's 32 stores hit 32 distinct banks.
 
+// One level of Alg. 2 on the 16-B records: T_V <- X[r, N_F]; go left iff
+// pred(T_V, N_T); the chosen child is the next record or, when its leaf flag
+// is set, the leaf payload (value bits for w == 1, leaf slot for w > 1).
+// Finished walks issue no load (st != 0: 1 = ended left, 2 = ended right).
 template <bool LE, int R>
-__device__ __forceinline__ void wide_step(const uint2 *n, uint32_t &i, const float *xs, int r,
-                                          bool &done) {
-  const uint2 d = __ldg(n + i);
-  const int f = (int)(d.x & 0xFFFFu);
-  const float x = xs[f * R + r];
-  const float t = __uint_as_float(d.y);
-  const bool pr = LE ? (x <= t) : (x < t);
-  const uint32_t nx = (d.x >> 16) - (pr ? 1u : 0u);   // left child = N_R - 1 (BFS, siblings adjacent)
-  done = done && (nx == i);
-  i = nx;
+__device__ __forceinline__ void wide_step(const uint4 *tr, uint32_t &q, uint32_t &pay, uint32_t &st,
+                                          const float *xs, int r) {
+  if (st == 0) {
+    const uint4 d = __ldg(tr + 1 + q);          // record q follows the 16-B tree header
+    const float x = xs[(d.x & 0xFFFFu) * R + r];
+    const float t = __uint_as_float(d.y);
+    const bool pr = LE ? (x <= t) : (x < t);
+    const uint32_t nx = pr ? d.z : d.w;
+    const bool leaf = (d.x >> (pr ? 16 : 17)) & 1u;
+    pay = nx;
+    if (leaf) st = pr ? 1u : 2u;
+    else q = nx;
+  }
 }
 
 template <bool LE, int NACC, int R, int G>   // G: trees walked at once per lane
@@ -230,7 +243,6 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   uint64_t *hred = reinterpret_cast<uint64_t *>(red + (size_t)nwarps * R * NACC);       // [nwarps][R]
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   const int slots = nwarps * L;
-  constexpr int noff = 16;                        // node array offset in a record
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row0 = (int64_t)tile * R;
     // X tile load: lane = (row group sub, row rr); each lane loads one
@@ -279,26 +291,30 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
-    // leaf of tree t reached (record rc, slot leaf): add its value / emit its id
-    auto finish = [&](int t, const uint8_t *rc, uint32_t leaf) {
-      const float *lv = reinterpret_cast<const float *>(rc + noff + (size_t)8 * p.nslots);
+    // walk of tree t ended on record q, side st (1 left, 2 right), payload
+    // pay: add the leaf value / emit the leaf's original id
+    auto finish = [&](int t, const uint4 *tr, uint32_t q, uint32_t st, uint32_t pay) {
       if (p.w == 1) {
-        const double v = (double)__ldg(lv + leaf);
+        const double v = (double)__uint_as_float(pay);
         if (NACC == 1) {
           acc[0] += v;
         } else {
-          const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(rc));
+          const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(tr) + 2);   // tree_output
 #pragma unroll
           for (int k = 0; k < NACC; ++k)
             if (k0 == (uint32_t)k) acc[k] += v;
         }
       } else {
+        const float *lv = reinterpret_cast<const float *>(
+            reinterpret_cast<const uint8_t *>(tr) + __ldg(reinterpret_cast<const uint32_t *>(tr) + 3));
 #pragma unroll
         for (int k = 0; k < NACC; ++k)
-          if (k < p.K) acc[k] += (double)__ldg(lv + leaf * p.w + k);
+          if (k < p.K) acc[k] += (double)__ldg(lv + pay * p.w + k);
       }
       if (lm && t < p.n_trees) {
-        const int32_t id = __ldg(p.leafmap + (size_t)t * p.nslots + leaf);
+        const uint32_t *ids = reinterpret_cast<const uint32_t *>(
+            reinterpret_cast<const uint8_t *>(tr) + __ldg(reinterpret_cast<const uint32_t *>(tr) + 1));
+        const int32_t id = (int32_t)__ldg(ids + 2 * q + (st - 1));
         if (lm == 1) {
           if (row < p.n) static_cast<int32_t *>(p.out)[row * p.leaf_stride + p.tree_off + t] = id;
         } else {
@@ -306,29 +322,31 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
         }
       }
     };
+    const int levels = p.depth > 0 ? p.depth : 1;   // a single-leaf tree still has one record
     // warp-uniform loop over groups of G tree slots (t = base + sub + g*slots)
     for (int base = warp * L; base < p.n_trees_pad; base += G * slots) {
-      const uint8_t *rec[G];
-      const uint2 *nd[G];
-      uint32_t idx[G];
-      bool valid[G];
+      const uint4 *tr[G];
+      uint32_t q[G], pay[G], st[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int t = base + sub + g * slots;
-        valid[g] = t < p.n_trees_pad;               // uniform across the warp
-        rec[g] = p.trees + (size_t)(valid[g] ? t : base + sub) * p.stride;
-        nd[g] = reinterpret_cast<const uint2 *>(rec[g] + noff);
-        idx[g] = 0;
+        const bool valid = t < p.n_trees_pad;         // uniform across the warp
+        tr[g] = p.ttw + __ldg(p.toff + (valid ? t : base + sub));
+        q[g] = 0;
+        pay[g] = 0;
+        st[g] = valid ? 0u : 3u;                      // 3: no tree, nothing to walk
       }
-      for (int l = 0; l < p.depth; ++l) {
+      for (int l = 0; l < levels; ++l) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) wide_step<LE, R>(tr[g], q[g], pay[g], st[g], xs, r);
         bool done = true;
 #pragma unroll
-        for (int g = 0; g < G; ++g) wide_step<LE, R>(nd[g], idx[g], xs, r, done);
-        if (__all_sync(0xFFFFFFFFu, done)) break;   // every lane on a self-looping leaf
+        for (int g = 0; g < G; ++g) done = done && st[g] != 0;
+        if (__all_sync(0xFFFFFFFFu, done)) break;   // every walk of the warp reached a leaf
       }
 #pragma unroll
       for (int g = 0; g < G; ++g)
-        if (valid[g]) finish(base + sub + g * slots, rec[g], idx[g]);
+        if (st[g] == 1u || st[g] == 2u) finish(base + sub + g * slots, tr[g], q[g], st[g], pay[g]);
     }
     // combine the L tree slots of a row inside the warp, then across warps
 #pragma unroll
@@ -404,11 +422,6 @@ static TtFn pick_wide(int R, int nacc) {
   }
 }
 
-// SMEM of tt_wide_kernel for R rows: X tile + fp64 per-warp row sums + hashes
-size_t tt_wide_smem(int F, int R, int nwarps, int nacc) {
-  return ((((size_t)F * R + 1) & ~(size_t)1) * 4) + (size_t)nwarps * R * (8 * (size_t)nacc + 8);
-}
-
 hb_status launch_tt(const Model &m, const RunArgs &a) {
   const bool wide = m.cfg.wide_rows > 0;
   TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc)
@@ -443,6 +456,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   p.x_smem = m.cfg.x_smem;
   p.t_smem = m.cfg.t_smem;
   p.x_prefetch = m.cfg.prefetch;
+  p.ttw = static_cast<const uint4 *>(m.d_ttw);
+  p.toff = m.d_ttw_off;
   p.accumulate = 0;
   p.leaf_stride = m.n_trees;
   p.tree_off = 0;
@@ -475,7 +490,7 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
   }
   for (int t0 = 0; t0 < m.n_trees_pad; t0 += m.tt_chunk) {
     TtParams pc = p;
-    pc.trees = p.trees + (size_t)t0 * p.stride;
+    pc.toff = p.toff + t0;
     pc.n_trees_pad = std::min(m.tt_chunk, m.n_trees_pad - t0);
     pc.n_trees = std::max(0, std::min(m.tt_chunk, m.n_trees - t0));
     pc.tree_begin = m.tree_begin + t0;
