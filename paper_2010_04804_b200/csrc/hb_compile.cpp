@@ -16,6 +16,12 @@
 
 namespace hb {
 
+// memcpy of possibly empty vectors (their data() may be null: memcpy with a
+// null pointer is undefined even for 0 bytes; found by the UBSan fuzz build)
+static inline void copy_bytes(void *dst, const void *src, size_t n) {
+  if (n) std::memcpy(dst, src, n);
+}
+
 bool gemm_supported(int depth) { return depth <= 6; }
 
 hb_status compile_gemm(const hb_ensemble *e, int t0, int t1, Model *m) {
@@ -607,9 +613,9 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     const size_t fb = A.fmeta.size() * 4, gb = A.groups.size() * 4, pb = A.pool.size() * 4;
     const size_t pool_off = (fb + gb + 127) & ~size_t(127);
     std::vector<uint8_t> aux(pool_off + pb, 0);
-    std::memcpy(aux.data(), A.fmeta.data(), fb);
-    std::memcpy(aux.data() + fb, A.groups.data(), gb);
-    std::memcpy(aux.data() + pool_off, A.pool.data(), pb);
+    copy_bytes(aux.data(), A.fmeta.data(), fb);
+    copy_bytes(aux.data() + fb, A.groups.data(), gb);
+    copy_bytes(aux.data() + pool_off, A.pool.data(), pb);
     ust = dev_upload(m, aux.data(), aux.size(), &m->d_aux);
     if (ust != HB_OK) return ust;
     m->aux_groups_off = fb;
@@ -626,9 +632,9 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     const size_t fb = R.feat.size() * 4, gb = R.groups.size() * 4;
     const size_t pool_off = (fb + gb + 127) & ~size_t(127);
     std::vector<uint8_t> aux(pool_off + R.pool.size(), 0);
-    std::memcpy(aux.data(), R.feat.data(), fb);
-    std::memcpy(aux.data() + fb, R.groups.data(), gb);
-    std::memcpy(aux.data() + pool_off, R.pool.data(), R.pool.size());
+    copy_bytes(aux.data(), R.feat.data(), fb);
+    copy_bytes(aux.data() + fb, R.groups.data(), gb);
+    copy_bytes(aux.data() + pool_off, R.pool.data(), R.pool.size());
     ust = dev_upload(m, aux.data(), aux.size(), &m->d_rb);
     if (ust != HB_OK) return ust;
     m->rb_groups_off = fb;

@@ -36,8 +36,12 @@ KEYS = [
 
 
 def raw(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """Records of an ncu report (.ncu-rep) or of its `--page raw --csv` export (.csv)."""
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, u = rows[0], rows[1]
     return [dict(zip(h, r)) for r in rows[2:]], dict(zip(h, u))
