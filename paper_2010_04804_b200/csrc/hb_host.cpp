@@ -338,7 +338,8 @@ static hb_status build_tt(const hb_ensemble *e, int t0, int t1, int Tpad, HostLa
 
 // Wide-row TT records (tt_wide_kernel). Alg. 2's per-node
 // tensors (Table 5: N_F, N_T, N_L, N_R, N_C) folded per INTERNAL node into one
-// 16-B record {N_F | leafL << 16 | leafR << 17, N_T, payload_L, payload_R},
+// 16-B record {4 R N_F | leafL | leafR << 1, N_T, payload_L, payload_R} (4 R N_F
+// = the byte offset of feature N_F's column in the kernel's R-row X tile),
 // in BFS order of the internal nodes. A payload is the child's record index,
 // or, when the child is a leaf (flag set), its value bits (w == 1) or its leaf
 // slot (w > 1; values at vals_off). So a walk ends on the record whose chosen
@@ -356,7 +357,7 @@ struct WideLayout {
 };
 
 static hb_status build_ttw(const hb_ensemble *e, int t0, int t1, int Tpad, const FeatureMap *fm,
-                           WideLayout *W) {
+                           int R, WideLayout *W) {
   const int w = e->leaf_width;
   const uint32_t pinf = f2u(INFINITY);
   std::vector<int> q, recid, slot;
@@ -368,7 +369,7 @@ static hb_status build_ttw(const hb_ensemble *e, int t0, int t1, int Tpad, const
     W->toff[lt] = (uint32_t)(base / 4);
     if (lt >= t1 - t0) {   // padding tree: one record, both children a zero leaf
       W->words.insert(W->words.end(), {1u, 32u, 0u, 48u});   // header (byte offsets)
-      W->words.insert(W->words.end(), {0u | 3u << 16, pinf, 0u, 0u});
+      W->words.insert(W->words.end(), {0u | 3u, pinf, 0u, 0u});
       W->words.insert(W->words.end(), {0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u});   // ids (never read)
       for (int k = 0; k < 4; ++k) W->words.push_back(0u);                  // w <= 4 zero values
       if (w > 4) W->words.resize(W->words.size() + ((size_t)w - 4 + 3) / 4 * 4, 0u);
@@ -412,7 +413,7 @@ static hb_status build_ttw(const hb_ensemble *e, int t0, int t1, int Tpad, const
     };
     if (root_leaf) {
       uint32_t *r = T + 4;
-      r[0] = 0u | 3u << 16;
+      r[0] = 0u | 3u;
       r[1] = pinf;
       r[2] = r[3] = payload(0);
       T[ids_off] = T[ids_off + 1] = 0u;
@@ -422,7 +423,7 @@ static hb_status build_ttw(const hb_ensemble *e, int t0, int t1, int Tpad, const
         uint32_t *r = T + 4 + 4 * recid[o];
         const int L = e->left[a + o], Rc = e->right[a + o];
         const uint32_t f = (uint32_t)(fm ? fm->remap[e->feature[a + o]] : e->feature[a + o]);
-        r[0] = f | (e->left[a + L] == -1 ? 1u << 16 : 0u) | (e->left[a + Rc] == -1 ? 1u << 17 : 0u);
+        r[0] = 4u * (uint32_t)R * f | (e->left[a + L] == -1 ? 1u : 0u) | (e->left[a + Rc] == -1 ? 2u : 0u);
         r[1] = f2u(e->threshold[a + o]);
         r[2] = payload(L);
         r[3] = payload(Rc);
@@ -690,8 +691,9 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.t_smem = 0;
         c.ch = kTreeGroup;
         m->cfg = c;
+        m->tt_g = env_int("HB_TT_G", 4);   // walks per lane (DESIGN.md §4.3 sweep)
         WideLayout W;
-        st = build_ttw(e, t0, t1, m->n_trees_pad, &fmap, &W);
+        st = build_ttw(e, t0, t1, m->n_trees_pad, &fmap, m->cfg.wide_rows, &W);
         if (st != HB_OK) return st;
         // models larger than L2: walk them in tree chunks whose records stay
         // L2-resident (HB_TT_CHUNK: -1 auto, N trees, 0 off). The walk reads

@@ -211,23 +211,22 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // fill gives the 32/R row groups of a warp different 4-feature chunks and
 // rotates their store order so a warp's 32 stores hit 32 distinct banks.
 
-// One level of Alg. 2 on the 16-B records: T_V <- X[r, N_F]; go left iff
-// pred(T_V, N_T); the chosen child is the next record or, when its leaf flag
-// is set, the leaf payload (value bits for w == 1, leaf slot for w > 1).
-// Finished walks issue no load (st != 0: 1 = ended left, 2 = ended right).
-template <bool LE, int R>
-__device__ __forceinline__ void wide_step(const uint4 *tr, uint32_t &q, uint32_t &pay, uint32_t &st,
-                                          const float *xs, int r) {
-  if (st == 0) {
+// One level of Alg. 2 on the 16-B records: T_V <- X[r, N_F] (the record holds
+// the column's byte offset in the X tile); go left iff pred(T_V, N_T); the
+// chosen child is the next record or, when its leaf flag is set, the leaf
+// payload (value bits for w == 1, leaf slot for w > 1). A finished walk
+// (done != 0) issues no load; q then still names the last record.
+template <bool LE>
+__device__ __forceinline__ void wide_step(const uint4 *tr, uint32_t &q, uint32_t &pay, uint32_t &done,
+                                          uint32_t xlane) {
+  if (done == 0u) {
     const uint4 d = __ldg(tr + 1 + q);          // record q follows the 16-B tree header
-    const float x = xs[(d.x & 0xFFFFu) * R + r];
+    const float x = dev::lds_f32(xlane + (d.x & ~3u));
     const float t = __uint_as_float(d.y);
     const bool pr = LE ? (x <= t) : (x < t);
-    const uint32_t nx = pr ? d.z : d.w;
-    const bool leaf = (d.x >> (pr ? 16 : 17)) & 1u;
-    pay = nx;
-    if (leaf) st = pr ? 1u : 2u;
-    else q = nx;
+    pay = pr ? d.z : d.w;
+    done = d.x & (pr ? 1u : 2u);
+    if (done == 0u) q = pay;
   }
 }
 
@@ -287,13 +286,14 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       dev::prefetch_rows_l2(p.X, (int64_t)(tile + gridDim.x) * R, R, p.n, p.ldx);
     __syncthreads();
     const int64_t row = row0 + r;
+    const uint32_t xlane = dev::smem_u32(xs) + 4u * (uint32_t)r;   // this lane's row in the X tile
     double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
-    // walk of tree t ended on record q, side st (1 left, 2 right), payload
-    // pay: add the leaf value / emit the leaf's original id
-    auto finish = [&](int t, const uint4 *tr, uint32_t q, uint32_t st, uint32_t pay) {
+    // walk of tree t ended on record q, payload pay: add the leaf value /
+    // emit the leaf's original id
+    auto finish = [&](int t, const uint4 *tr, uint32_t q, uint32_t pay) {
       if (p.w == 1) {
         const double v = (double)__uint_as_float(pay);
         if (NACC == 1) {
@@ -314,7 +314,12 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       if (lm && t < p.n_trees) {
         const uint32_t *ids = reinterpret_cast<const uint32_t *>(
             reinterpret_cast<const uint8_t *>(tr) + __ldg(reinterpret_cast<const uint32_t *>(tr) + 1));
-        const int32_t id = (int32_t)__ldg(ids + 2 * q + (st - 1));
+        // the side the walk took at record q (re-evaluated: only the leaf-id
+        // outputs need it, the value path does not carry it)
+        const uint4 d = __ldg(tr + 1 + q);
+        const float x = dev::lds_f32(xlane + (d.x & ~3u));
+        const bool pr = LE ? (x <= __uint_as_float(d.y)) : (x < __uint_as_float(d.y));
+        const int32_t id = (int32_t)__ldg(ids + 2 * q + (pr ? 0u : 1u));
         if (lm == 1) {
           if (row < p.n) static_cast<int32_t *>(p.out)[row * p.leaf_stride + p.tree_off + t] = id;
         } else {
@@ -326,27 +331,28 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
     // warp-uniform loop over groups of G tree slots (t = base + sub + g*slots)
     for (int base = warp * L; base < p.n_trees_pad; base += G * slots) {
       const uint4 *tr[G];
-      uint32_t q[G], pay[G], st[G];
+      uint32_t q[G], pay[G], dn[G];
+      bool valid[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int t = base + sub + g * slots;
-        const bool valid = t < p.n_trees_pad;         // uniform across the warp
-        tr[g] = p.ttw + __ldg(p.toff + (valid ? t : base + sub));
+        valid[g] = t < p.n_trees_pad;                 // uniform across the warp
+        tr[g] = p.ttw + __ldg(p.toff + (valid[g] ? t : base + sub));
         q[g] = 0;
         pay[g] = 0;
-        st[g] = valid ? 0u : 3u;                      // 3: no tree, nothing to walk
+        dn[g] = valid[g] ? 0u : 4u;                   // no tree, nothing to walk
       }
       for (int l = 0; l < levels; ++l) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) wide_step<LE, R>(tr[g], q[g], pay[g], st[g], xs, r);
-        bool done = true;
+        for (int g = 0; g < G; ++g) wide_step<LE>(tr[g], q[g], pay[g], dn[g], xlane);
+        bool all = true;
 #pragma unroll
-        for (int g = 0; g < G; ++g) done = done && st[g] != 0;
-        if (__all_sync(0xFFFFFFFFu, done)) break;   // every walk of the warp reached a leaf
+        for (int g = 0; g < G; ++g) all = all && dn[g] != 0u;
+        if (__all_sync(0xFFFFFFFFu, all)) break;    // every walk of the warp reached a leaf
       }
 #pragma unroll
       for (int g = 0; g < G; ++g)
-        if (st[g] == 1u || st[g] == 2u) finish(base + sub + g * slots, tr[g], q[g], st[g], pay[g]);
+        if (valid[g]) finish(base + sub + g * slots, tr[g], q[g], pay[g]);
     }
     // combine the L tree slots of a row inside the warp, then across warps
 #pragma unroll
@@ -404,7 +410,10 @@ static TtFn pick_nacc(int nacc) {
 int sm_count(int device);
 
 template <bool LE, int R>
-static TtFn pick_wide_nacc(int nacc) {
+static TtFn pick_wide_nacc(int nacc, int g) {
+  // 6 or 8 concurrent walks per lane: scalar outputs only (registers)
+  if (nacc == 1 && g == 8) return tt_wide_kernel<LE, 1, R, 8>;
+  if (nacc == 1 && g == 6) return tt_wide_kernel<LE, 1, R, 6>;
   switch (nacc) {
     case 1: return tt_wide_kernel<LE, 1, R, 4>;
     case 4: return tt_wide_kernel<LE, 4, R, 4>;
@@ -414,18 +423,18 @@ static TtFn pick_wide_nacc(int nacc) {
 }
 
 template <bool LE>
-static TtFn pick_wide(int R, int nacc) {
+static TtFn pick_wide(int R, int nacc, int g) {
   switch (R) {
-    case 32: return pick_wide_nacc<LE, 32>(nacc);
-    case 16: return pick_wide_nacc<LE, 16>(nacc);
-    default: return pick_wide_nacc<LE, 8>(nacc);
+    case 32: return pick_wide_nacc<LE, 32>(nacc, g);
+    case 16: return pick_wide_nacc<LE, 16>(nacc, g);
+    default: return pick_wide_nacc<LE, 8>(nacc, g);
   }
 }
 
 hb_status launch_tt(const Model &m, const RunArgs &a) {
   const bool wide = m.cfg.wide_rows > 0;
-  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc)
-                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc))
+  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g)
+                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g))
                  : (m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc));
   TtParams p;
   p.X = a.X;

@@ -343,9 +343,12 @@ static void check_tt_wide(const Ens &E, const Model &m, const std::vector<float>
         REQUIRE(q < nrec, "TT wide record index %u >= %u", q, nrec);
         if (q >= nrec) return;
         const uint32_t *d = T + 4 + 4 * q;
-        const bool pr = pred(E.cmp, x[orig_feature(m, (int)(d[0] & 0xFFFF))], u2f(d[1]));
+        // word 0 = byte offset 4 R f of the feature's column in the R-row X tile | flags
+        const int R = m.cfg.wide_rows;
+        REQUIRE(R > 0 && (d[0] & ~3u) % (4u * R) == 0, "TT wide feature offset");
+        const bool pr = pred(E.cmp, x[orig_feature(m, (int)((d[0] & ~3u) / (4u * R)))], u2f(d[1]));
         const uint32_t nx = pr ? d[2] : d[3];
-        if ((d[0] >> (pr ? 16 : 17)) & 1u) { side = pr ? 1 : 2; pay = nx; break; }
+        if (d[0] & (pr ? 1u : 2u)) { side = pr ? 1 : 2; pay = nx; break; }
         q = nx;
       }
       REQUIRE(side != 0, "TT wide walk did not end within depth");

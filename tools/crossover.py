@@ -51,7 +51,7 @@ def time_calls(fn, reps=20, iters=5):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_crossover.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_crossover.json"))
     ap.add_argument("--trees", type=int, default=100)
     ap.add_argument("--features", type=int, default=200)
     args = ap.parse_args()
@@ -66,9 +66,15 @@ def main():
             kernels.append(("gemm", {"strategy": "gemm"}, {"HB_SMALL_BATCH": "0"}))
         if D <= 10:
             kernels.append(("ptt", {"strategy": "ptt"}, {"HB_SMALL_BATCH": "0", "HB_PTT_RANK": "0"}))
-            kernels.append(("ptt-rank", {"strategy": "ptt"}, {"HB_SMALL_BATCH": "0", "HB_PTT_RANK": "1"}))
+            kernels.append(("ptt-rank", {"strategy": "ptt"},
+                            {"HB_SMALL_BATCH": "0", "HB_PTT_RANK": "1", "HB_RANK_PRE": "0"}))
+            kernels.append(("ptt-rank-pre", {"strategy": "ptt"},
+                            {"HB_SMALL_BATCH": "0", "HB_PTT_RANK": "1", "HB_RANK_PRE": "1"}))
         kernels.append(("tt", {"strategy": "tt"}, {"HB_SMALL_BATCH": "0"}))
         kernels.append(("small", {"strategy": "auto"}, {"HB_SMALL_BATCH": str(10 ** 9)}))
+        # what the library picks by itself (strategy, layout and small-batch
+        # threshold all default)
+        kernels.append(("auto", {"strategy": "auto"}, {}))
         for name, kw, env in kernels:
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
@@ -80,8 +86,11 @@ def main():
                     X = Xall[:n]
                     out = torch.empty((n, 2), dtype=torch.float32, device="cuda")
                     us = time_calls(lambda: m.predict_proba(X, out=out))
+                    info = m.info
                     res.append({"depth": D, "batch": n, "kernel": name, "us_per_call": us,
-                                "rows_per_s": n / (us * 1e-6), "layout": m.info["node_record_bytes"]})
+                                "rows_per_s": n / (us * 1e-6), "layout": info["node_record_bytes"],
+                                "ran": m.kernel_for(n), "strategy": info["strategy_name"],
+                                "rank_prepass": info["rank_prepass"]})
                     print(f"D={D:2d} batch={n:8d} {name:9s} {us:10.1f} us  {n / us:10.2f} Mrows/s",
                           flush=True)
                 m.free()
@@ -93,9 +102,23 @@ def main():
                         os.environ.pop(k, None)
                     else:
                         os.environ[k] = v
+    # AUTO against the best forced kernel at every (depth, batch)
+    summary = []
+    for D in sorted({r["depth"] for r in res}):
+        for n in batches:
+            rows = [r for r in res if r["depth"] == D and r["batch"] == n]
+            forced = [r for r in rows if r["kernel"] != "auto"]
+            auto = [r for r in rows if r["kernel"] == "auto"]
+            if not forced or not auto:
+                continue
+            best = min(forced, key=lambda r: r["us_per_call"])
+            summary.append({"depth": D, "batch": n, "best": best["kernel"], "best_us": best["us_per_call"],
+                            "auto_us": auto[0]["us_per_call"], "auto_ran": auto[0]["ran"],
+                            "auto_over_best": auto[0]["us_per_call"] / best["us_per_call"]})
+            print(f"D={D:2d} batch={n:8d} best={best['kernel']:12s} auto/best={summary[-1]['auto_over_best']:.3f}")
     json.dump({"setup": f"{args.trees} trees, F={args.features}, balanced, sigmoid proba; "
                         "device time per call from a replayed CUDA graph of 20 calls",
-               "results": res}, open(args.out, "w"), indent=1)
+               "results": res, "auto_vs_best": summary}, open(args.out, "w"), indent=1)
 
 
 if __name__ == "__main__":
