@@ -232,8 +232,10 @@ def workload_config(cfg, e, rows, args, mode="rows", scaling="strong", world=1):
                    "a 1/8 tree shard (~60 MB) is L2-resident, all 10k trees (~480 MB) are not")}
 
 
-def launch_names(info, n):
-    """Kernel names of one call's launches, in order (hb_predict_ex_events)."""
+def launch_names(info, n, kind):
+    """Kernel names of one call's launches, in order (hb_predict_ex_events):
+    rank-code pre-pass + scorer; one launch per L2-resident tree chunk plus a
+    finalize unless the output is accumulated in place (raw64, leaf hash)."""
     if n <= info["small_batch_max_rows"]:
         return ["small_batch_kernel"]
     if info.get("rank_prepass"):
@@ -241,7 +243,8 @@ def launch_names(info, n):
     chunk = info.get("tt_chunk_trees", 0)
     if chunk:
         pad = (info["n_trees"] + 3) // 4 * 4
-        return [info["kernel_name"]] * (-(-pad // chunk)) + ["finalize_kernel"]
+        fin = [] if kind in ("raw64", "leaf_hash", "leaf") else ["finalize_kernel"]
+        return [info["kernel_name"]] * (-(-pad // chunk)) + fin
     return [info["kernel_name"]]
 
 
@@ -310,7 +313,7 @@ def run_ours(args):
         rows_all = n
         scaling = "strong"
     info = m.info
-    names = launch_names(info, n)
+    names = launch_names(info, n, call_kind)
     small = n <= info["small_batch_max_rows"]
 
     def tail():
@@ -356,6 +359,7 @@ def run_ours(args):
             nl = len(names)
         else:
             nl = m.run_events(X, call_kind, call_out, evs[i], stream)
+            assert nl == len(names), f"call made {nl} launches, expected {names}"
         tail()
         return nl
 

@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
+    double cur = 0.0;     // running sum of the current class (per-class scalar trees)
+    uint32_t curk = 0;
 
     for (int c = 0; c < nchunks; ++c, ring.next()) {
       const int s = ring.s;
@@ -162,12 +164,19 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
             }
           }
           if (NACC > 1 && p.w == 1) {
-            // per-class records are ordered by class in groups of G (hb_host.cpp
-            // ptt_order): one output selection per group instead of per tree
+            // per-class records are ordered by class (hb_host.cpp ptt_order,
+            // whole groups of G): sum into one running accumulator and move
+            // it to acc[class] only when the class changes (K times per
+            // tile; the branch is warp-uniform, every lane reads the record)
             const uint32_t k0 = dev::lds_u32(tb[0]) & 0xFFu;
+            if (k0 != curk) {
 #pragma unroll
-            for (int k = 0; k < NACC; ++k)
-              if (k0 == (uint32_t)k) acc[k] += vsum;
+              for (int k = 0; k < NACC; ++k)
+                if (curk == (uint32_t)k) acc[k] += cur;
+              cur = 0.0;
+              curk = k0;
+            }
+            cur += vsum;
           }
           if (lm) {
             // record header: tree_output | (local tree id + 1) << 8 (0: padding)
@@ -187,6 +196,11 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
         }
       }
       dev::release_stage(&empty[s], lane);
+    }
+    if (NACC > 1 && p.w == 1) {
+#pragma unroll
+      for (int k = 0; k < NACC; ++k)
+        if (curk == (uint32_t)k) acc[k] += cur;
     }
     if (row < p.n) {
       if (lm == 2) {
