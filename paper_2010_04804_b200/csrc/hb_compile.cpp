@@ -145,9 +145,11 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
       used.push_back(f);
     }
   if (used.empty()) used.push_back(0), remap[0] = 0;
-  // X slices of 4 warps in SMEM when the used columns fit (else X is read
-  // from global with original feature ids)
-  const bool fits = 4L * (long)used.size() * 128 <= 160L * 1024;
+  // X slice of the 128-row tile in SMEM when the used columns fit next to
+  // the two A tiles, the record ring and the barriers (gemm_tc_kernel)
+  const TcGeom g0 = tc_geom(e->leaf_width);
+  const long fixed = (long)gemm_tc_a_region(m->nacc) + 3L * (long)g0.stride + 128;
+  const bool fits = 4L * (long)used.size() * 128 + fixed <= (long)kSmemBudget;
   const bool compact = fits && (int)used.size() < e->n_features;
   if (!compact)
     for (int f = 0; f < e->n_features; ++f) remap[f] = f;
@@ -235,12 +237,13 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
   m->n_xf = compact ? (int)used.size() : e->n_features;
   const long xb = 4L * m->n_xf * 128;
   m->cfg = LaunchCfg();
-  m->cfg.nw = 4;
+  m->cfg.nw = 16;
   m->cfg.x_smem = fits ? 1 : 0;
   m->cfg.t_smem = 1;
-  m->cfg.smem_bytes = (int)((m->cfg.x_smem ? xb : 0) + 2 * g.stride + kTcRows * 16 * 2 * kTcPairs + 64);
-  // 4 warps per CTA: fill the SM with up to 4 CTAs (TMEM: 4 x 128 columns = 512)
-  m->cfg.ctas_per_sm = std::max(1, std::min(4, (int)(kSmemBudget / std::max(1, m->cfg.smem_bytes))));
+  m->cfg.smem_bytes = (int)((m->cfg.x_smem ? xb : 0) + fixed);
+  // 16 warps per CTA, 256 TMEM columns each: up to 2 CTAs per SM (threads,
+  // TMEM: 2 x 256 of 512 columns) when SMEM allows
+  m->cfg.ctas_per_sm = std::max(1, std::min(2, (int)(kSmemBudget / std::max(1, m->cfg.smem_bytes))));
   m->gemm_tc = 1;
   return HB_OK;
 }
@@ -535,6 +538,16 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     }
   }
   if (!ok && force_pre != 0) {
+    // The pre-pass codes every used feature of every row (n_fc searches and
+    // a code write + read per row) to make the T * D node visits per row
+    // cheaper: it pays only when the walk is long next to the feature count.
+    // Measured (profiles/r02_crossover.json): C2 / C3 / C4
+    // (T*D / n_fc = 44 / 143 / 519) gain from it; the paper's Fig. 8 shape
+    // (100 trees over 200 features, T*D / n_fc = 1.5-5) loses to fp32 nodes
+    // at every batch size. Below HB_PRE_MIN_RATIO (16) AUTO keeps fp32 nodes.
+    const double ratio = (double)Tpad * (double)std::max(D, 1) / std::max(1, A.n_fc);
+    if (force_pre == -1 && force != 1 && ratio < (double)env_int2("HB_PRE_MIN_RATIO", 16))
+      return HB_E_UNSUPPORTED;
     pre = true;
     ok = pick_cw(true, cfg, cw);
   }

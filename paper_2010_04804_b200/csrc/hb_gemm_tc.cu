@@ -94,30 +94,47 @@ struct TcParams {
   int K, w, task, post, kind;
   void *out;
   int ntiles;
+  int prefetch;          // L2 prefetch of the CTA's next X row tile
+  uint32_t a_region;     // bytes of the A-tile region (also the tile-end reduction scratch)
 };
 
-template <bool LE, int NACC>
-__global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t xbytes = p.x_smem ? (size_t)4 * p.F * 128 : 0;
-  uint8_t *recbuf = smem + xbytes;                               // 2 x stride
-  uint8_t *atile = recbuf + 2 * (size_t)p.stride;                // kTcPairs x 4 KB
-  uint64_t *bars = reinterpret_cast<uint64_t *>(atile + (size_t)kTcPairs * 4096);
-  uint64_t *rec_full = bars;       // [2] group record landed
-  uint64_t *mma_done = bars + 2;   // MMA group finished
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3);
+constexpr int kTcThreads = 512;   // 4 row quarters x 4 tree quarters
+constexpr int kTcStages = 3;      // group-record ring: epilogue(i-1), MMA(i), landing(i+1)
 
-  if (threadIdx.x == 0) {
-    dev::mbar_init(&rec_full[0], 1);
-    dev::mbar_init(&rec_full[1], 1);
-    dev::mbar_init(mma_done, 1);
+// Software pipeline per CTA: iteration i builds the A tile
+// of group i (node predicates, CUDA cores), issues its 8 UMMAs into TMEM
+// buffer i & 1 (tensor cores, asynchronous), then runs the epilogue of group
+// i - 1 from the other TMEM buffer while the tensor cores work. Records come
+// through a 3-stage cp.async.bulk ring (record i - 1: D / E of the epilogue,
+// i: B operand of the MMA, i + 1: landing). Thread (row, part): row = tid %
+// 128 (TMEM lane), part = tid / 128 owns trees 4 part .. 4 part + 3 of every
+// group in the A build and pairs 2 part, 2 part + 1 in the epilogue; the 4
+// parts' per-row sums are combined in SMEM in a fixed order at the tile end.
+template <bool LE, int NACC>
+__global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const TcParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = tid & (kTcRows - 1), part = tid >> 7, quarter = r >> 5;
+  const size_t xbytes = p.x_smem ? (size_t)4 * p.F * 128 : 0;     // xs[quarter][F][32]
+  uint8_t *atiles = smem + xbytes;                                 // 2 x kTcPairs x 4 KB
+  uint8_t *recbuf = atiles + p.a_region;                           // kTcStages x stride
+  uint64_t *bars = reinterpret_cast<uint64_t *>(recbuf + (size_t)kTcStages * p.stride);
+  uint64_t *rec_full = bars;                // [kTcStages] group record landed
+  uint64_t *mma_done = bars + kTcStages;    // [2] MMA of TMEM buffer b finished
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + kTcStages + 2);
+  double *red = reinterpret_cast<double *>(atiles);                // tile-end reduction (aliases A)
+  uint64_t *hred = reinterpret_cast<uint64_t *>(atiles + (size_t)4 * kTcRows * NACC * 8);
+
+  if (tid == 0) {
+    for (int i = 0; i < kTcStages; ++i) dev::mbar_init(&rec_full[i], 1);
+    dev::mbar_init(&mma_done[0], 1);
+    dev::mbar_init(&mma_done[1], 1);
     dev::fence_mbar_init();
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      dev::smem_u32(tmem_slot)),
-                 "n"(kTcCols));
+                 "n"(2 * kTcCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -125,26 +142,53 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
+  float *xs = reinterpret_cast<float *>(smem) + (size_t)quarter * p.F * 32;
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
-  const uint32_t a_base = dev::smem_u32(atile);
-  uint32_t it = 0;            // global group counter of this CTA (record ring)
-  uint32_t mma_phase = 0;
-
+  const uint32_t a_base = dev::smem_u32(atiles);
   const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const uint32_t total = (uint32_t)my_tiles * p.ngroups;
-  if (threadIdx.x == 0 && total > 0) {
-    dev::mbar_arrive_expect_tx(&rec_full[0], p.stride);
-    dev::bulk_g2s(recbuf, p.groups, p.stride, &rec_full[0]);
-  }
+  // record ring: item `it` (global over this CTA's tiles x groups) in stage it % 3
+  auto issue_rec = [&](uint32_t it) {
+    if (it < total) {
+      const int st = (int)(it % kTcStages);
+      const int gi = (int)(it % (uint32_t)p.ngroups);
+      dev::mbar_arrive_expect_tx(&rec_full[st], p.stride);
+      dev::bulk_g2s(recbuf + (size_t)st * p.stride, p.groups + (size_t)gi * p.stride, p.stride,
+                    &rec_full[st]);
+    }
+  };
+  if (tid == 0) issue_rec(0);
+  uint32_t it = 0;          // record / MMA item counter
+  uint32_t mma_ph[2] = {0u, 0u};
 
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t row = (int64_t)tile * kTcRows + warp * 32 + lane;
+    const int64_t row0 = (int64_t)tile * kTcRows;
+    const int64_t row = row0 + r;
+    // ---- X slice of this tile: quarter q of the rows, features split over the 4 parts
     const float *xrow;
     int xstride;
     if (p.x_smem) {
-      if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
-      else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+      const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
+      if (p.vec4 && !p.fmap) {
+        for (int j = part; 4 * j < p.F; j += 4) {
+          const int f = 4 * j;
+          if (f + 4 <= p.F) {
+            const float4 v = row < p.n ? __ldg(reinterpret_cast<const float4 *>(xr + f))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            xs[(f + 0) * 32 + lane] = v.x;
+            xs[(f + 1) * 32 + lane] = v.y;
+            xs[(f + 2) * 32 + lane] = v.z;
+            xs[(f + 3) * 32 + lane] = v.w;
+          } else {
+            for (int c = f; c < p.F; ++c) xs[c * 32 + lane] = row < p.n ? __ldg(xr + c) : 0.f;
+          }
+        }
+      } else {
+        for (int c = part; c < p.F; c += 4)
+          xs[c * 32 + lane] = row < p.n ? __ldg(xr + (p.fmap ? __ldg(p.fmap + c) : c)) : 0.f;
+      }
+      if (tid == 0 && p.prefetch)
+        dev::prefetch_rows_l2(p.X, (int64_t)(tile + gridDim.x) * kTcRows, kTcRows, p.n, p.ldx);
       xrow = xs + lane;
       xstride = 32;
     } else {
@@ -155,28 +199,77 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
+    // previous group's item (its epilogue runs in the next iteration)
+    uint32_t prev_it = 0;
+    int prev_gi = -1;
+
+    // epilogue of group gi (item pit): T <- S == D ; R <- T.E for this
+    // thread's pairs 2 part, 2 part + 1 (16 TMEM columns each)
+    auto epilogue = [&](uint32_t pit, int gi) {
+      const int b = (int)(pit & 1u);
+      dev::mbar_wait(&mma_done[b], mma_ph[b]);
+      mma_ph[b] ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint8_t *rec = recbuf + (size_t)(pit % kTcStages) * p.stride;
+      const float *dval = reinterpret_cast<const float *>(rec + p.off_d);
+      const uint32_t *tout = reinterpret_cast<const uint32_t *>(rec + p.off_tout);
+      const float *E = reinterpret_cast<const float *>(rec + p.off_e);
+#pragma unroll
+      for (int sp = 0; sp < 2; ++sp) {
+        const int s = 2 * part + sp;
+        float S[16];
+        tc::ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTcCols + s * 16), S);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int q = 2 * s + hh;
+          int sel = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (S[hh * 8 + j] == dval[q * 8 + j]) sel = j;
+          if (p.w == 1) {
+            const double v = (double)E[q * 8 + sel];
+            if (NACC == 1) {
+              acc[0] += v;
+            } else {
+              const uint32_t k0 = tout[q];
+#pragma unroll
+              for (int k = 0; k < NACC; ++k)
+                if (k0 == (uint32_t)k) acc[k] += v;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < NACC; ++k)
+              if (k < p.K) acc[k] += (double)E[(q * 8 + sel) * p.w + k];
+          }
+          if (lm) {
+            const int t = gi * kTcTrees + q;
+            if (t < p.n_trees) {
+              const int32_t id = __ldg(p.leafmap + (size_t)t * 8 + sel);
+              if (lm == 1) {
+                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
+              } else {
+                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
+              }
+            }
+          }
+        }
+      }
+    };
 
     for (int gi = 0; gi < p.ngroups; ++gi, ++it) {
-      const int buf = it & 1;
-      uint8_t *rec = recbuf + (size_t)buf * p.stride;
-      // prefetch the next group record into the other buffer (its last reader
-      // finished before the previous group's closing barrier)
-      if (threadIdx.x == 0 && it + 1 < total) {
-        const int ng = (gi + 1 == p.ngroups) ? 0 : gi + 1;
-        dev::mbar_arrive_expect_tx(&rec_full[buf ^ 1], p.stride);
-        dev::bulk_g2s(recbuf + (size_t)(buf ^ 1) * p.stride, p.groups + (size_t)ng * p.stride,
-                      p.stride, &rec_full[buf ^ 1]);
-      }
-      dev::mbar_wait(&rec_full[buf], (it >> 1) & 1);
+      const int st = (int)(it % kTcStages);
+      const int b = (int)(it & 1u);
+      dev::mbar_wait(&rec_full[st], (it / kTcStages) & 1u);
+      const uint8_t *rec = recbuf + (size_t)st * p.stride;
       const uint32_t *feat = reinterpret_cast<const uint32_t *>(rec + p.off_feat);
       const float *thr = reinterpret_cast<const float *>(rec + p.off_thr);
-
-      // 1. T <- (X.A < B): 16 trees x 8 nodes -> bf16 {0,1} into the A tile.
-      //    Pair s is K-slab s: row r, k-chunk c (= tree 2s+c) at
-      //    s*4096 + (r>>3)*256 + c*128 + (r&7)*16.
-      const int r = threadIdx.x;
-#pragma unroll 2
-      for (int q = 0; q < kTcTrees; ++q) {
+      // 1. T <- (X.A < B) for this thread's 4 trees -> bf16 {0,1} into A
+      //    tile b. Pair s is K-slab s: row r, k-chunk c (= tree 2s + c) at
+      //    s * 4096 + (r >> 3) * 256 + c * 128 + (r & 7) * 16.
+      uint8_t *atile = atiles + (size_t)b * kTcPairs * 4096;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const int q = 4 * part + qq;
         uint32_t bits[4];
 #pragma unroll
         for (int i2 = 0; i2 < 4; ++i2) {
@@ -196,75 +289,58 @@ __global__ void __launch_bounds__(128) gemm_tc_kernel(const TcParams p) {
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
+      __syncthreads();   // A tile b built; epilogue(i - 2) done with TMEM buffer b and record i - 2
       asm volatile("tcgen05.fence::after_thread_sync;");
-
-      // 2. S <- T.C on the tensor cores: one M128 x N16 x K16 UMMA per pair.
-      if (threadIdx.x == 0) {
+      // 2. S <- T.C on the tensor cores (asynchronous): one M128 x N16 x K16
+      //    UMMA per pair into TMEM buffer b; then refill the ring stage that
+      //    held record i - 2 with record i + 1
+      if (tid == 0) {
         const uint32_t b_base = dev::smem_u32(rec);
+        const uint32_t ab = a_base + (uint32_t)b * kTcPairs * 4096u;
 #pragma unroll
         for (int s = 0; s < kTcPairs; ++s) {
-          const uint64_t ad = tc::smem_desc(a_base + s * 4096, 128, 256);
+          const uint64_t ad = tc::smem_desc(ab + s * 4096, 128, 256);
           const uint64_t bd = tc::smem_desc(b_base + s * 512, 128, 256);
-          tc::mma_bf16(tmem + s * 16, ad, bd);
+          tc::mma_bf16(tmem + (uint32_t)(b * kTcCols + s * 16), ad, bd);
         }
-        tc::commit(mma_done);
+        tc::commit(&mma_done[b]);
+        issue_rec(it + 1);
       }
-      dev::mbar_wait(mma_done, mma_phase);
-      mma_phase ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-
-      // 3. T <- S == D ; R <- T.E  (epilogue per pair: 16 TMEM columns)
-      const float *dval = reinterpret_cast<const float *>(rec + p.off_d);
-      const uint32_t *tout = reinterpret_cast<const uint32_t *>(rec + p.off_tout);
-      const float *E = reinterpret_cast<const float *>(rec + p.off_e);
-#pragma unroll 1
-      for (int s = 0; s < kTcPairs; ++s) {
-        float S[16];
-        tc::ld16(tmem + ((uint32_t)(warp * 32) << 16) + s * 16, S);
+      // 3. epilogue of the previous group while the tensor cores work
+      if (prev_gi >= 0) epilogue(prev_it, prev_gi);
+      prev_it = it;
+      prev_gi = gi;
+    }
+    // drain: the last group's epilogue
+    if (prev_gi >= 0) epilogue(prev_it, prev_gi);
+    // ---- combine the 4 parts of every row in a fixed order
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();   // every A tile consumed (all MMAs waited): reuse it for the reduction
+    asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int q = 2 * s + hh;
-          int sel = 0;
+    for (int k = 0; k < NACC; ++k) red[((size_t)part * kTcRows + r) * NACC + k] = acc[k];
+    hred[part * kTcRows + r] = h;
+    __syncthreads();
+    if (part == 0) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (S[hh * 8 + j] == dval[q * 8 + j]) sel = j;
-          if (p.w == 1) {
-            const double v = (double)E[q * 8 + sel];
-            const uint32_t k0 = tout[q];
-#pragma unroll
-            for (int k = 0; k < NACC; ++k)
-              if (k0 == (uint32_t)k) acc[k] += v;
-          } else {
-#pragma unroll
-            for (int k = 0; k < NACC; ++k)
-              if (k < p.K) acc[k] += (double)E[(q * 8 + sel) * p.w + k];
-          }
-          if (lm) {
-            const int t = gi * kTcTrees + q;
-            if (t < p.n_trees) {
-              const int32_t id = __ldg(p.leafmap + (size_t)t * 8 + sel);
-              if (lm == 1) {
-                if (row < p.n) static_cast<int32_t *>(p.out)[row * p.n_trees + t] = id;
-              } else {
-                h += dev::mix64(((uint64_t)(uint32_t)(p.tree_begin + t) << 32) | (uint32_t)id);
-              }
-            }
-          }
-        }
+      for (int k = 0; k < NACC; ++k) {
+        double t = 0.0;
+        for (int q = 0; q < 4; ++q) t += red[((size_t)q * kTcRows + r) * NACC + k];
+        acc[k] = t;
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();   // A tile, TMEM and this record buffer are free again
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint64_t ht = 0;
+      for (int q = 0; q < 4; ++q) ht += hred[q * kTcRows + r];
+      if (row < p.n) {
+        if (lm == 2) static_cast<uint64_t *>(p.out)[row] = ht;
+        else if (lm == 0) dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
+      }
     }
-    if (row < p.n) {
-      if (lm == 2) static_cast<uint64_t *>(p.out)[row] = h;
-      else if (lm == 0) dev::write_row<NACC>(p.kind, acc, p.K, p.task, p.post, p.scale, p.base, row, p.out);
-    }
+    __syncthreads();   // reduction scratch and X slice free for the next tile
   }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kTcCols));
 }
 
 using TcFn = void (*)(const TcParams);
@@ -313,12 +389,14 @@ hb_status launch_gemm_tc(const Model &m, const RunArgs &a) {
   const int64_t ntiles = (a.n + kTcRows - 1) / kTcRows;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows");
   p.ntiles = (int)ntiles;
+  p.prefetch = m.cfg.prefetch;
+  p.a_region = (uint32_t)gemm_tc_a_region(m.nacc);
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
   TcFn fn = m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        m.cfg.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(gemm_tc)");
-  fn<<<grid, 128, m.cfg.smem_bytes, a.stream>>>(p);
+  fn<<<grid, kTcThreads, m.cfg.smem_bytes, a.stream>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "gemm_tc_kernel launch");
   return HB_OK;

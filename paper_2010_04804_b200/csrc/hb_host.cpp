@@ -460,7 +460,9 @@ static bool choose_cfg(int F, size_t stride, int Tpad, bool allow_x_global, bool
     const long rem = budget - xb;
     int ns = (rem >= 3 * 8 * (long)stride) ? 3 : 2;
     if (env_int("HB_NS", 0)) ns = env_int("HB_NS", 0);
-    int ch = (int)std::min<long>(env_int("HB_CH", 32), rem / (ns * (long)stride)) & ~(kTreeGroup - 1);
+    // up to 128 trees per ring item: every item costs each warp an mbarrier
+    // wait + release, which small (shallow) trees do not amortise at 32
+    int ch = (int)std::min<long>(env_int("HB_CH", 128), rem / (ns * (long)stride)) & ~(kTreeGroup - 1);
     ch = std::min(ch, Tpad);
     if (ch < kTreeGroup) continue;
     c->nw = nw;

@@ -74,6 +74,14 @@ inline TcGeom tc_geom(int w) {
 }
 
 
+// gemm_tc_kernel SMEM: two A tiles (kTcPairs K-slabs of 4 KB each), reused
+// at the tile end as the scratch of the 4-part per-row reduction (fp64 sums
+// + leaf hash per part and row)
+inline size_t gemm_tc_a_region(int nacc) {
+  const size_t a = 2 * (size_t)kTcPairs * 4096, red = 4 * (size_t)kTcRows * (8 * (size_t)nacc + 8);
+  return a > red ? a : red;
+}
+
 // ---- rank-code pre-pass (hb_rank_codes.cu)
 constexpr uint32_t kRcSmemMax = 200 * 1024;  // largest per-CTA table budget
 
