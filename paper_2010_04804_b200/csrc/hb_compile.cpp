@@ -150,7 +150,10 @@ hb_status compile_gemm_tc(const hb_ensemble *e, int t0, int t1, Model *m) {
   const TcGeom g0 = tc_geom(e->leaf_width);
   const long fixed = (long)gemm_tc_a_region(m->nacc) + 3L * (long)g0.stride + 128;
   const bool fits = 4L * (long)used.size() * 128 + fixed <= (long)kSmemBudget;
-  const bool compact = fits && (int)used.size() < e->n_features;
+  // compact only when it removes a real share of the columns (see feature_map)
+  const char *fs = std::getenv("HB_FSEL_MAX_PCT");
+  const long pct = fs && *fs ? std::atol(fs) : 75;
+  const bool compact = fits && (long)used.size() * 100 <= pct * e->n_features;
   if (!compact)
     for (int f = 0; f < e->n_features; ++f) remap[f] = f;
   std::vector<uint8_t> buf((size_t)ngroups * g.stride, 0);

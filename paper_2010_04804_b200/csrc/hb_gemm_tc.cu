@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const TcParams p
         dev::prefetch_rows_l2(p.X, (int64_t)(tile + gridDim.x) * kTcRows, kTcRows, p.n, p.ldx);
       xrow = xs + lane;
       xstride = 32;
+      __syncthreads();   // the 4 parts filled different columns of each row's slice
     } else {
       xrow = p.X + (row < p.n ? row : 0) * p.ldx;
       xstride = 1;

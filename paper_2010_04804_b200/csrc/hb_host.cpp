@@ -203,6 +203,12 @@ struct FeatureMap {
   bool identity = true;
 };
 
+static int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
 static FeatureMap feature_map(const hb_ensemble *e, int t0, int t1) {
   FeatureMap fm;
   std::vector<char> u(e->n_features, 0);
@@ -216,9 +222,17 @@ static FeatureMap feature_map(const hb_ensemble *e, int t0, int t1) {
       fm.used.push_back(f);
     }
   if (fm.used.empty()) fm.used.push_back(0), fm.remap[0] = 0;
-  fm.identity = (int)fm.used.size() == e->n_features;
-  if (fm.identity)
-    for (int f = 0; f < e->n_features; ++f) fm.remap[f] = f;
+  // compact only when it removes a real share of the columns: a compacted
+  // tile is filled by per-column gathers through the map, the full one by
+  // 16-B row loads — with 6 of 200 features unused (the paper's Fig. 8
+  // shape at D3) the gather fill re-read X from DRAM twice (1.50 vs 0.82 GB
+  // per launch) and doubled the step (ncu). Threshold:
+  // HB_FSEL_MAX_PCT (75) percent of the columns used.
+  fm.identity = (long)fm.used.size() * 100 > (long)env_int("HB_FSEL_MAX_PCT", 75) * e->n_features;
+  if (fm.identity) {
+    fm.used.resize(e->n_features);
+    for (int f = 0; f < e->n_features; ++f) fm.remap[f] = f, fm.used[f] = f;
+  }
   return fm;
 }
 
@@ -439,11 +453,6 @@ static hb_status build_ttw(const hb_ensemble *e, int t0, int t1, int Tpad, const
   return HB_OK;
 }
 
-static int env_int(const char *name, int dflt) {
-  const char *v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  return std::atoi(v);
-}
 
 // Launch configuration: as many 32-row warps as SMEM allows
 // for the feature-major X slices (NW * F * 128 B), the rest for a 2-4 stage
