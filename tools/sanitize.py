@@ -35,6 +35,11 @@ cases = [
     ("tt-wide-chunks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
      {"HB_TT_WIDE": "1", "HB_TT_CHUNK": "8"}, "tt"),
     ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
+    ("gemm-tc-multiclass", synth.gen_forest(50, 3, 12, seed=5, n_outputs=3, post=synth.POST_SOFTMAX,
+                                            task=synth.TASK_CLASSIFICATION), {}, "gemm"),
+    ("tt-wide-multiclass", synth.gen_forest(30, 11, 12, seed=6, family="mixed", n_outputs=3,
+                                            post=synth.POST_SOFTMAX, task=synth.TASK_CLASSIFICATION),
+     {"HB_TT_WIDE": "1"}, "tt"),
     ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
 ]
 only = set(sys.argv[1:])   # optional case names; default: every case
@@ -46,7 +51,7 @@ for name, e, env, strat in cases:
         os.environ["HB_SMALL_BATCH"] = small
         m = hb.Model(e, strategy=strat, device=0)
         X = synth.dev.gen_X_device(7, n, 12)
-        for kind in ("predict", "raw", "leaf", "leaf_hash"):
+        for kind in ("predict", "raw", "raw64", "leaf", "leaf_hash"):
             m.run(X, kind)
         torch.cuda.synchronize()
         m.free()
