@@ -57,6 +57,12 @@ CONFIGS = {
     "C5": Config("C5", 1_000_000, 2000, 10_000, 12, "mixed", 1, 1, "normal", 0.05,
                  AGG_SUM, POST_SIGMOID, TASK_CLASSIFICATION, 0.0, 0xC5, 0x1C5,
                  note="10k-tree depth-12 ensemble, Epsilon-shaped 2000 features"),
+    # not a BASELINE config: the paper's Fig. 8 strategy-comparison shape
+    # (synthetic, 200 features, 100 trees; depth 3, the GEMM
+    # regime) at a 1M-row batch, for the GEMM (tcgen05) bench line
+    "F8D3": Config("F8D3", 1_000_000, 200, 100, 3, "balanced", 1, 1, "normal", 0.1,
+                   AGG_SUM, POST_SIGMOID, TASK_CLASSIFICATION, 0.0, 0xF8, 0x1F8,
+                   note="Fig. 8 shape (P:537): 100 trees depth 3, 200 features, binary, 1M rows"),
 }
 
 
