@@ -438,6 +438,28 @@ def run_ours(args):
                   "note": "the contraction is integer-exact bf16 (operands in {-1, 0, 1}); "
                           "the tensor pipe is not what binds (SURVEY §8(d))"}
     achieved = per_row * n / (dom_ms * 1e-3) / 1e9
+    chase = None
+    if dom == "tt_wide_kernel" and rank == 0:
+        # the walk's records come from L2 and every load depends on the one
+        # before: besides the streaming L2 roof, measure dependent random
+        # 16-B gathers in the same launch shape (tools/peaks.cu l2_chase) over
+        # a buffer the size of the records one launch walks
+        try:
+            import tools
+            tools.build()
+            chunk = info.get("tt_chunk_trees") or info["n_trees"]
+            rb = int(info["tt_record_bytes"] * min(1.0, chunk / max(1, info["n_trees"])))
+            g = info.get("tt_walks_per_lane") or 4
+            rate = tools.l2_chase(local, max(rb, 1 << 20), g)
+            loads = n * (t1 - t0) * max(levels, 1.0)
+            krate = loads / (dom_ms * 1e-3)
+            chase = {"kernel_node_loads_per_s": krate, "chase_loads_per_s": rate, "frac": krate / rate,
+                     "buffer_bytes": max(rb, 1 << 20), "chains_per_thread": g,
+                     "note": "node loads = rows x trees x mean levels (one 16-B record per internal "
+                             "node on the path); chase = dependent random 16-B __ldg gathers, "
+                             "1024 threads per SM, the same chains per thread (tools/peaks.cu)"}
+        except Exception as ex:  # pragma: no cover
+            chase = {"error": str(ex)}
     peaks = {}
     if rank == 0:
         try:
@@ -489,6 +511,7 @@ def run_ours(args):
         "smem_peak_spec_gbs": 148 * 128 * 1.965,
         "l2_peak_gbs": peaks.get("l2_gbs"),
         "tensor": tensor,
+        "dependent_gather": chase,
         "hbm": {"achieved": hbm_bytes / (ms_per_step * 1e-3) / 1e9, "peak": hbm_peak,
                 "frac": hbm_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
                 "bytes_per_call": hbm_bytes,

@@ -173,6 +173,9 @@ typedef struct {
                                    walked in several launches (0: one launch) */
   int32_t small_batch_max_rows; /* calls with n_rows <= this run the small-batch kernel
                                    (trees across threads) instead of `kernel` (ABI 4) */
+  int32_t tt_walks_per_lane;    /* wide-row TT: concurrent walks per lane (ABI 4)        */
+  int64_t tt_record_bytes;      /* wide-row TT: bytes of the 16-B node records the walk
+                                   reads (tables of leaf ids excluded) (ABI 4)          */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls): the tree structure

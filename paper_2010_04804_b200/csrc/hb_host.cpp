@@ -716,6 +716,7 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         if (!host_only) cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device);
         double rec_bytes = 0;
         for (int lt = 0; lt < m->n_trees; ++lt) rec_bytes += 16.0 * W.words[(size_t)W.toff[lt] * 4];
+        m->ttw_rec_bytes = (size_t)rec_bytes;
         const bool big = rec_bytes > 0.01 * env_int("HB_TT_BIG_L2", 50) * (double)l2_bytes;
         const int want_chunk = env_int("HB_TT_CHUNK", -1);
         if (want_chunk > 0 || (want_chunk == -1 && big)) {
@@ -1089,6 +1090,8 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->tt_sector = 0;   // sector-paired TT records were removed
   info->tt_chunk_trees = m.tt_chunk;
   info->small_batch_max_rows = m.small_max;
+  info->tt_walks_per_lane = m.cfg.wide_rows ? m.tt_g : 0;
+  info->tt_record_bytes = (int64_t)m.ttw_rec_bytes;
   return HB_OK;
 }
 

@@ -101,6 +101,7 @@ struct Model {
   void *d_ttw = nullptr;
   uint32_t *d_ttw_off = nullptr;
   size_t ttw_bytes = 0;
+  size_t ttw_rec_bytes = 0;  // node-record bytes the walk reads (sum over trees)
 
   size_t device_bytes = 0;
   LaunchCfg cfg;

@@ -252,31 +252,58 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       const int F4 = (p.F + 3) >> 2;
       const int nblk = (F4 + SUBS - 1) / SUBS;
       const bool v4 = !p.fmap && p.vec4 && (p.F & 3) == 0;
-      for (int idx = threadIdx.x; idx < nblk * 32; idx += blockDim.x) {
-        const int q = idx & 31, rr = q % R, sub = q / R;
-        const int c = (idx >> 5) * SUBS + sub;
-        if (c >= F4) continue;
-        const int f = 4 * c;
-        const int64_t gr = row0 + rr;
-        float v0, v1, v2, v3;
-        if (v4) {
-          const float4 v = gr < p.n ? __ldg(reinterpret_cast<const float4 *>(p.X + gr * p.ldx + f))
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-          v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
-        } else {
+      if (v4) {
+        // U independent 16-B loads per thread in flight before the stores:
+        // the fill waits one L2/HBM latency per U chunks, not per chunk
+        constexpr int U = 4;
+        const int total = nblk * 32;
+        for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+          float4 v[U];
+          int f_[U], rr_[U], sub_[U];
+          bool ok[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int idx = i0 + u * (int)blockDim.x;
+            const int q = idx & 31, rr = q % R, sub = q / R;
+            const int c = (idx >> 5) * SUBS + sub;
+            ok[u] = idx < total && c < F4;
+            f_[u] = 4 * c;
+            rr_[u] = rr;
+            sub_[u] = sub;
+            const int64_t gr = row0 + rr;
+            v[u] = ok[u] && gr < p.n ? __ldg(reinterpret_cast<const float4 *>(p.X + gr * p.ldx + 4 * c))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int jj = (j + sub_[u]) & 3;
+              const float val = jj == 0 ? v[u].x : (jj == 1 ? v[u].y : (jj == 2 ? v[u].z : v[u].w));
+              xs[(f_[u] + jj) * R + rr_[u]] = val;
+            }
+          }
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < nblk * 32; idx += blockDim.x) {
+          const int q = idx & 31, rr = q % R, sub = q / R;
+          const int c = (idx >> 5) * SUBS + sub;
+          if (c >= F4) continue;
+          const int f = 4 * c;
+          const int64_t gr = row0 + rr;
           float t[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int fj = f + j;
             t[j] = (gr < p.n && fj < p.F) ? __ldg(p.X + gr * p.ldx + (p.fmap ? __ldg(p.fmap + fj) : fj)) : 0.f;
           }
-          v0 = t[0]; v1 = t[1]; v2 = t[2]; v3 = t[3];
-        }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int jj = (j + sub) & 3;
-          const float val = jj == 0 ? v0 : (jj == 1 ? v1 : (jj == 2 ? v2 : v3));
-          if (f + jj < p.F) xs[(f + jj) * R + rr] = val;
+          for (int j = 0; j < 4; ++j) {
+            const int jj = (j + sub) & 3;
+            const float val = jj == 0 ? t[0] : (jj == 1 ? t[1] : (jj == 2 ? t[2] : t[3]));
+            if (f + jj < p.F) xs[(f + jj) * R + rr] = val;
+          }
         }
       }
     }

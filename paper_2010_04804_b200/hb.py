@@ -52,7 +52,8 @@ class _Info(C.Structure):
                 ("kernel", C.c_int32), ("rows_per_cta", C.c_int32),
                 ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32),
                 ("tt_sector", C.c_int32), ("tt_chunk_trees", C.c_int32),
-                ("small_batch_max_rows", C.c_int32)]
+                ("small_batch_max_rows", C.c_int32), ("tt_walks_per_lane", C.c_int32),
+                ("tt_record_bytes", C.c_int64)]
 
 
 def _load():

@@ -21,3 +21,13 @@ def peaks(device=0):
     L.hbpeaks_smem_gbs.restype = C.c_double
     L.hbpeaks_l2_gbs.restype = C.c_double
     return {"smem_gbs": L.hbpeaks_smem_gbs(device), "l2_gbs": L.hbpeaks_l2_gbs(device)}
+
+
+def l2_chase(device=0, nbytes=16 << 20, chains=4):
+    """Dependent random 16-B gathers per second from an `nbytes` buffer, in
+    tt_wide_kernel's launch shape (1024 threads per SM, `chains` walks per
+    thread): the latency-bound roof of a tree walk whose records live in L2."""
+    L = C.CDLL(SO)
+    L.hbpeaks_l2_chase.restype = C.c_double
+    L.hbpeaks_l2_chase.argtypes = [C.c_int, C.c_longlong, C.c_int]
+    return L.hbpeaks_l2_chase(device, nbytes, chains)

@@ -95,3 +95,79 @@ extern "C" double hbpeaks_l2_gbs(int device) {
   cudaEventDestroy(b);
   return cudaGetLastError() == cudaSuccess ? best : -1.0;
 }
+
+// Dependent random 16-B gathers through the read-only path (the access
+// pattern of a tree walk whose records come from L2: every load's address
+// depends on the previous load). Each thread runs G independent chains over
+// a random single-cycle permutation of a `bytes` buffer (L2-resident when
+// bytes << L2) for `steps` steps, the chains of a thread issued back to back
+// like tt_wide_kernel's G walks. Launch shape = tt_wide_kernel's (one
+// 1024-thread CTA per SM). Returns dependent loads per second.
+template <int G>
+__global__ void __launch_bounds__(1024, 1) l2_chase_kernel(const uint4 *__restrict__ buf, uint32_t n,
+                                                           int steps, uint32_t *sink) {
+  uint32_t idx[G];
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int g = 0; g < G; ++g) idx[g] = (t * 2654435761u + (uint32_t)g * 40503u) % n;
+  for (int s = 0; s < steps; ++s) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) idx[g] = __ldg(buf + idx[g]).x;
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc ^= idx[g];
+  if (acc == 0xFFFFFFFFu) sink[threadIdx.x] = acc;
+}
+
+extern "C" double hbpeaks_l2_chase(int device, long long bytes, int chains) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const uint32_t n = (uint32_t)(bytes / 16);
+  // single random cycle (Sattolo's shuffle), LCG-driven: every chain visits
+  // the whole buffer in random order
+  uint32_t *next = (uint32_t *)malloc((size_t)n * 4);
+  for (uint32_t i = 0; i < n; ++i) next[i] = i;
+  uint64_t z = 0x9E3779B97F4A7C15ull;
+  for (uint32_t i = n - 1; i > 0; --i) {
+    z = z * 6364136223846793005ull + 1442695040888963407ull;
+    const uint32_t j = (uint32_t)((z >> 33) % i);
+    const uint32_t tmp = next[i]; next[i] = next[j]; next[j] = tmp;
+  }
+  uint4 *h = (uint4 *)malloc((size_t)n * 16);
+  for (uint32_t i = 0; i < n; ++i) h[i] = make_uint4(next[i], i, 0, 0);
+  uint4 *buf;
+  uint32_t *sink;
+  cudaMalloc(&buf, (size_t)n * 16);
+  cudaMemcpy(buf, h, (size_t)n * 16, cudaMemcpyHostToDevice);
+  cudaMalloc(&sink, 4096);
+  free(next);
+  free(h);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int steps = 2048;
+  auto launch = [&](int s) {
+    if (chains >= 8) l2_chase_kernel<8><<<sms, 1024>>>(buf, n, s, sink);
+    else if (chains >= 4) l2_chase_kernel<4><<<sms, 1024>>>(buf, n, s, sink);
+    else if (chains >= 2) l2_chase_kernel<2><<<sms, 1024>>>(buf, n, s, sink);
+    else l2_chase_kernel<1><<<sms, 1024>>>(buf, n, s, sink);
+  };
+  launch(64);
+  double best = 0;
+  const int g = chains >= 8 ? 8 : chains >= 4 ? 4 : chains >= 2 ? 2 : 1;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(a);
+    launch(steps);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    const double loads = (double)sms * 1024 * g * steps;
+    best = fmax(best, loads / (time_ms(a, b) * 1e-3));
+  }
+  cudaFree(buf);
+  cudaFree(sink);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return cudaGetLastError() == cudaSuccess ? best : -1.0;
+}
