@@ -44,14 +44,17 @@ struct TtParams {
   int tree_off;           // first model-local tree of this chunk (LEAF column)
 };
 
+// One Alg. 2 walk over a tree record staged in shared memory: nodes at the
+// 32-bit shared address `nodes` (8-B records), this lane's X slice at `xlane`
+// (xs[f * 32 + lane] -> byte offset 128 f). Explicit ld.shared (the ring is
+// rewritten by the TMA engine between mbarrier phases).
 template <bool LE>
-__device__ __forceinline__ uint32_t tt_walk(const uint2 *nodes, const float *xrow, int xstride,
-                                            int depth) {
+__device__ __forceinline__ uint32_t tt_walk(uint32_t nodes, uint32_t xlane, int depth) {
   uint32_t i = 0;
 #pragma unroll 4
   for (int l = 0; l < depth; ++l) {
-    const uint2 d = nodes[i];
-    const float x = xrow[(d.x & 0xFFFFu) * xstride];
+    const uint2 d = dev::lds_v2(nodes + 8u * i);
+    const float x = dev::lds_f32(xlane + ((d.x & 0xFFFFu) << 7));
     const float t = __uint_as_float(d.y);
     const bool pr = LE ? (x <= t) : (x < t);
     i = (d.x >> 16) - (pr ? 1u : 0u);
@@ -59,30 +62,32 @@ __device__ __forceinline__ uint32_t tt_walk(const uint2 *nodes, const float *xro
   return i;
 }
 
+// Narrow-row TreeTraversal: the PTT kernel's structure (X slice per warp in
+// SMEM, tree records streamed through a cp.async.bulk ring by a producer
+// warp); AUTO uses it for TT models whose rows and records fit (the launch
+// configuration always stages both in SMEM).
 template <bool LE, int NACC>
 __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = p.nw, ns = p.ns, ch = p.ch;
-  const size_t xbytes = p.x_smem ? (size_t)nw * p.F * 128 : 0;
+  const size_t xbytes = (size_t)nw * p.F * 128;
   uint8_t *stages = smem + xbytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(stages + (p.t_smem ? (size_t)ns * ch * p.stride : 0));
+  uint64_t *full = reinterpret_cast<uint64_t *>(stages + (size_t)ns * ch * p.stride);
   uint64_t *empty = full + ns;
-  if (p.t_smem) {
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < ns; ++s) {
-        dev::mbar_init(&full[s], 1);
-        dev::mbar_init(&empty[s], nw);
-      }
-      dev::fence_mbar_init();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], nw);
     }
-    __syncthreads();
+    dev::fence_mbar_init();
   }
+  __syncthreads();
   const int nchunks = (p.n_trees_pad + ch - 1) / ch;
   const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
   if (warp == nw) {
-    if (p.t_smem && lane == 0) {
+    if (lane == 0) {
       const long total = (long)my_tiles * nchunks;
       dev::Ring r(ns);
       int c = 0;
@@ -101,53 +106,39 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
   }
 
   float *xs = reinterpret_cast<float *>(smem) + (size_t)warp * p.F * 32;
+  const uint32_t xlane = dev::smem_u32(xs) + 4u * (uint32_t)lane;
+  const uint32_t stage0 = dev::smem_u32(stages);
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   dev::Ring ring(ns);
   for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const int64_t row = (int64_t)tile * (nw * 32) + warp * 32 + lane;
-    const float *xrow;
-    int xstride;
-    if (p.x_smem) {
-      if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
-      else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
-      xrow = xs + lane;
-      xstride = 32;
-    } else {
-      xrow = p.X + (row < p.n ? row : 0) * p.ldx;
-      xstride = 1;
-    }
+    if (p.fmap) dev::load_x_slice_map(xs, p.X, row, p.n, p.ldx, p.fmap, p.F, lane);
+    else dev::load_x_slice(xs, p.X, row, p.n, p.ldx, p.F, lane, p.vec4 != 0);
+    __syncwarp();
     double acc[NACC];   // fp64 accumulation (R23)
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     uint64_t h = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const uint8_t *cb;
-      int s = 0;
-      if (p.t_smem) {
-        s = ring.s;
-        dev::mbar_wait(&full[s], ring.ph);
-        cb = stages + (size_t)s * ch * p.stride;
-      } else {
-        cb = p.trees + (size_t)c * ch * p.stride;
-      }
+    for (int c = 0; c < nchunks; ++c, ring.next()) {
+      const int s = ring.s;
+      dev::mbar_wait(&full[s], ring.ph);
+      const uint32_t cb = stage0 + (uint32_t)(s * ch) * p.stride;
       const int nt = min(ch, p.n_trees_pad - c * ch);
       for (int j = 0; j < nt; j += 2) {
-        const uint8_t *ra = cb + (size_t)j * p.stride;
-        const uint8_t *rb = ra + p.stride;
-        const uint2 *na = reinterpret_cast<const uint2 *>(ra + 16);
-        const uint2 *nb = reinterpret_cast<const uint2 *>(rb + 16);
-        const uint32_t ia = tt_walk<LE>(na, xrow, xstride, p.depth);
-        const uint32_t ib = tt_walk<LE>(nb, xrow, xstride, p.depth);
-        const float *la = reinterpret_cast<const float *>(na + p.nslots);
-        const float *lb = reinterpret_cast<const float *>(nb + p.nslots);
+        const uint32_t ra = cb + (uint32_t)j * p.stride;
+        const uint32_t rb = ra + p.stride;
+        const uint32_t ia = tt_walk<LE>(ra + 16u, xlane, p.depth);
+        const uint32_t ib = tt_walk<LE>(rb + 16u, xlane, p.depth);
+        const uint32_t la = ra + 16u + 8u * (uint32_t)p.nslots;   // leaf[nslots][w]
+        const uint32_t lb = rb + 16u + 8u * (uint32_t)p.nslots;
         if (p.w == 1) {
-          const double va = (double)la[ia], vb = (double)lb[ib];
+          const double va = (double)dev::lds_f32(la + 4u * ia), vb = (double)dev::lds_f32(lb + 4u * ib);
           if (NACC == 1) {
             acc[0] += va;
             acc[0] += vb;
           } else {
-            const uint32_t ka = *reinterpret_cast<const uint32_t *>(ra);
-            const uint32_t kb = *reinterpret_cast<const uint32_t *>(rb);
+            const uint32_t ka = dev::lds_u32(ra);
+            const uint32_t kb = dev::lds_u32(rb);
 #pragma unroll
             for (int k = 0; k < NACC; ++k) {
               if (ka == (uint32_t)k) acc[k] += va;
@@ -157,10 +148,10 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
         } else {
 #pragma unroll
           for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += (double)la[ia * p.w + k];
+            if (k < p.K) acc[k] += (double)dev::lds_f32(la + 4u * (ia * (uint32_t)p.w + k));
 #pragma unroll
           for (int k = 0; k < NACC; ++k)
-            if (k < p.K) acc[k] += (double)lb[ib * p.w + k];
+            if (k < p.K) acc[k] += (double)dev::lds_f32(lb + 4u * (ib * (uint32_t)p.w + k));
         }
         if (lm) {
           const int tg = c * ch + j;
@@ -178,10 +169,7 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
           }
         }
       }
-      if (p.t_smem) {
-        dev::release_stage(&empty[s], lane);
-        ring.next();
-      }
+      dev::release_stage(&empty[s], lane);
     }
     if (row < p.n) {
       if (lm == 2) {
@@ -506,6 +494,8 @@ hb_status launch_tt(const Model &m, const RunArgs &a) {
                                        m.cfg.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tt)");
   const int threads = wide ? 32 * m.cfg.nw : 32 * (m.cfg.nw + 1);
+  if (!wide && (!m.cfg.x_smem || !m.cfg.t_smem))
+    return fail(HB_E_UNSUPPORTED, "tt_kernel needs its X slices and tree ring in SMEM");
   if (!(wide && m.tt_chunk > 0 && m.n_trees_pad > m.tt_chunk)) {
     fn<<<grid, threads, m.cfg.smem_bytes, a.stream>>>(p);
     e = cudaGetLastError();
