@@ -19,7 +19,14 @@ TSCALE = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
 
 
 def num(x):
-    return float(str(x).replace(",", ""))
+    try:
+        return float(str(x).replace(",", ""))
+    except ValueError:
+        return float("nan")
+
+
+def as_int(x):
+    return None if x != x else int(x)   # ncu reports -nan for some counters of long replays
 
 
 def main(key, rep, summary):
@@ -30,8 +37,8 @@ def main(key, rep, summary):
                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         smem = num(d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "0")) * 128
         ms = num(d.get("gpu__time_duration.sum", "0")) * TSCALE.get(units.get("gpu__time_duration.sum", "nsecond"), 1e-6)
-        launches.append({"kernel": d.get("Kernel Name", "")[:80], "dram_bytes": int(dram),
-                         "smem_ld_bytes": int(smem), "ncu_ms": round(ms, 4)})
+        launches.append({"kernel": d.get("Kernel Name", "")[:80], "dram_bytes": as_int(dram),
+                         "smem_ld_bytes": as_int(smem), "ncu_ms": round(ms, 4)})
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         js = json.load(open(p))
@@ -43,7 +50,9 @@ def main(key, rep, summary):
                     "(key config:layout:rows:trees). dram = dram__bytes_read.sum + dram__bytes_write.sum; "
                     "smem = l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum x 128 B; ncu_ms = "
                     "gpu__time_duration under the profiler (cold cache, serialised: shares, not absolutes).")
-    js[key] = {"round": 2, "launches": launches, "dram_bytes_per_call": int(sum(l["dram_bytes"] for l in launches)),
+    known = [l["dram_bytes"] for l in launches]
+    js[key] = {"round": 2, "launches": launches,
+               "dram_bytes_per_call": None if None in known else int(sum(known)),
                "source": summary}
     json.dump(js, open(p, "w"), indent=1)
     print(key, js[key]["dram_bytes_per_call"], [(l["kernel"][:30], l["dram_bytes"]) for l in launches])
