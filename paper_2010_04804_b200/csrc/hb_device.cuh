@@ -22,18 +22,24 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Consumer release of a ring stage that the TMA engine will overwrite:
-// order this warp's generic-proxy reads before the async-proxy writes
-// (fence.proxy.async), then arrive on the stage's `empty` barrier.
+// Consumer release of a ring stage that the TMA engine will overwrite: every
+// consumer thread orders its own generic-proxy reads of the stage before the
+// async-proxy writes of the next fill (fence.proxy.async) and arrives on the
+// stage's `empty` barrier (release semantics), which the producer acquires
+// before issuing the next cp.async.bulk into the stage. The barrier counts
+// kRingArrivals(nw) = 32 arrivals per consumer warp (each reading thread
+// signals for itself, as CUTLASS's PipelineTmaAsync consumers do; an elected
+// lane after __syncwarp is equivalent under the memory model but invisible to
+// compute-sanitizer racecheck, which then reported the ring reuse).
 __device__ __forceinline__ void release_stage(uint64_t *bar, int lane) {
-  __syncwarp();
-  if (lane == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-                 : "memory");
-  }
+  (void)lane;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
 }
+
+__device__ __forceinline__ constexpr uint32_t ring_arrivals(int nw) { return 32u * (uint32_t)nw; }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < ns; ++s) {
       dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], nw);
+      dev::mbar_init(&empty[s], dev::ring_arrivals(nw));
     }
     dev::fence_mbar_init();
   }
