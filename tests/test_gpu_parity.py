@@ -579,6 +579,33 @@ def test_predict_host_end_to_end(kind, pre, monkeypatch):
     assert torch.equal(got, dev)
 
 
+@pytest.mark.parametrize("cfg,n,F", [("C3", 2_000_000, 28), ("C4p", 1_000_000, 54)])
+def test_predict_host_multichunk_against_oracle(cfg, n, F):
+    """hb_predict_host streams X in ~64 MB chunks through two staging buffers
+    and two streams (H2D of chunk i+1 overlapping the scoring of chunk i):
+    C3's model on 2M rows (4 chunks of 599,186 rows) and C4p's on 1M rows
+    (4 chunks of 310,689), every output kind the host API offers, every row
+    against the oracle (the path bench.py's e2e number comes from)."""
+    c, e = synth.make_config(cfg)
+    m = hb.Model(e, device=0)
+    Xh = synth.gen_X(c.seed_x, n, F)
+    Xp = torch.from_numpy(Xh).pin_memory()
+    raw, hsh = oracle.raw_and_hash(e, Xh, threads=0)
+    mg = oracle.margin(e, raw)
+    post = oracle.post(e, mg)
+    cls = e.task == synth.TASK_CLASSIFICATION
+    got = m.predict_host(Xp, "leaf_hash").numpy().view(np.uint64)
+    assert np.array_equal(got, hsh), "leaf hash"
+    assert_scores(m.predict_host(Xp, "raw").numpy(), raw, "raw")
+    assert_scores(m.predict_host(Xp, "raw64").numpy(), raw, "raw64")
+    assert_scores(m.predict_host(Xp, "margin").numpy(), mg, "margin")
+    if cls:
+        assert_scores(m.predict_host(Xp, "proba").numpy(), oracle.proba(e, post), "proba")
+        assert_labels(e, m.predict_host(Xp, "predict").numpy(), oracle.label(e, mg), mg, f"{cfg} host labels")
+    else:
+        assert_scores(m.predict_host(Xp, "predict").numpy(), post, "predict")
+
+
 def test_host_and_device_generators_agree():
     for grid, sp in ((0, 0), (1, 0), (0, SPECIAL_Q24)):
         Xd, Xh = X_pair(77, 5000, 37, grid=grid, special_q24=sp, row_offset=12345)
