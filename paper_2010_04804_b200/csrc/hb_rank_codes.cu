@@ -39,6 +39,7 @@
 #include <cstring>
 #include <vector>
 
+#include "hb_device.cuh"
 #include "hb_internal.h"
 #include "hb_layouts.h"
 
@@ -394,6 +395,95 @@ RcFn staged_pick(bool le, int cw, int rb, bool one) {
 
 }  // namespace
 
+// Single-feature table groups with 32-bit cells (C3, C4: one ~34-40 KB table
+// per feature, one feature per CTA): a lean column kernel. The CTA owns one
+// feature for a contiguous slice of 32-row blocks (group-major grid: the CTAs
+// of all features for the same rows run together and share X's L2 sectors);
+// each warp takes U = 4 blocks at a time, lane = row. The U column values are
+// loaded straight into registers with 32-bit per-unit offsets (the next
+// unit's loads are issued before this unit's searches, so one X latency hides
+// behind a unit of work), the U searches run in lockstep over the SMEM table
+// with 32-bit shared addresses, and each code word is one coalesced 128-B
+// store. Same arithmetic as rank_codes_lockstep (exact, R28); what it removes
+// is the generic staging loop's 64-bit index math (242 instructions per lane
+// and 2 codes in the staged kernel, ncu round 2).
+constexpr int kOneU = 4;
+
+template <bool LE>
+__global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_one_kernel(const RankCodeParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int gi = blockIdx.x;                        // table group = one feature = one code word
+  const uint4 g = __ldg(p.groups + 2 * gi);
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.pool + g.x);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem);
+    for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const int wd = (int)g.z;                          // the word (= compact feature) of this group
+  const uint4 m0 = __ldg(p.feat + 2 * wd), m1 = __ldg(p.feat + 2 * wd + 1);
+  const float lo = __uint_as_float(m1.x), hi = __uint_as_float(m1.y), sc = __uint_as_float(m1.z);
+  const float bmax = (float)(m0.y - 1u);
+  const uint32_t smax = m0.z;
+  const uint32_t tab = dev::smem_u32(smem);
+  const uint32_t sbase = tab + m0.w, ubase = tab + m1.w;
+  const uint32_t cellhi = (uint32_t)wd << 23;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // this CTA's contiguous slice of units (U blocks each)
+  const int64_t nunits = (p.nblocks + kOneU - 1) / kOneU;
+  const int64_t ubeg = blockIdx.y * nunits / gridDim.y, uend = (blockIdx.y + 1) * nunits / gridDim.y;
+  const float *xcol = p.X + m0.x;                   // column f of X
+  const int64_t rstride = 32 * p.ldx;               // one row block, in floats
+  auto load = [&](int64_t u, float (&x)[kOneU]) {
+    const int64_t row0 = u * (kOneU * 32) + lane;
+    const float *ptr = xcol + row0 * p.ldx;
+    if (row0 + (kOneU - 1) * 32 < p.n) {
+#pragma unroll
+      for (int i = 0; i < kOneU; ++i) x[i] = __ldg(ptr + i * rstride);
+    } else {                                        // last unit: rows past n read row n - 1
+#pragma unroll
+      for (int i = 0; i < kOneU; ++i) {
+        const int64_t r = min(row0 + i * 32, p.n - 1);
+        x[i] = __ldg(xcol + r * p.ldx);
+      }
+    }
+  };
+  float xn[kOneU];
+  int64_t u = ubeg + warp;
+  if (u < uend) load(u, xn);
+  for (; u < uend; u += kRcWarps) {
+    float x[kOneU];
+#pragma unroll
+    for (int i = 0; i < kOneU; ++i) x[i] = xn[i];
+    if (u + kRcWarps < uend) load(u + kRcWarps, xn);   // next unit's loads in flight
+    uint32_t base[kOneU], cnt[kOneU];
+#pragma unroll
+    for (int i = 0; i < kOneU; ++i) {
+      const float xc = fminf(fmaxf(x[i], lo), hi);      // NaN -> lo; replaced below
+      const float y = fminf(__fmul_rn(__fsub_rn(xc, lo), sc), bmax);
+      const uint32_t be = dev::lds_u32(sbase + 4u * __float2uint_rz(y));
+      base[i] = be & 0xFFFFu;
+      cnt[i] = be >> 16;
+    }
+    for (uint32_t k = 0; k < smax; ++k) {
+#pragma unroll
+      for (int i = 0; i < kOneU; ++i) {
+        const uint32_t half = cnt[i] >> 1;
+        const float v = dev::lds_f32(ubase + 4u * (base[i] + half));
+        const bool go = (LE ? v < x[i] : v <= x[i]) && cnt[i] != 0u;
+        base[i] += go ? half + 1u : 0u;
+        cnt[i] = go ? cnt[i] - half - 1u : half;
+      }
+    }
+    uint32_t *dst = p.codes + ((size_t)u * kOneU * p.n_words + (size_t)wd) * 32 + lane;
+#pragma unroll
+    for (int i = 0; i < kOneU; ++i) {
+      if (u * kOneU + i < p.nblocks)
+        dst[(size_t)i * p.n_words * 32] = cellhi | (x[i] != x[i] ? 0xFFFFu : base[i]);
+    }
+  }
+}
+
 int sm_count(int device);
 
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks) {
@@ -426,6 +516,23 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   // per lockstep set over 4 row blocks (HB_RC_ONE=0/1 forces)
   const char *eone = std::getenv("HB_RC_ONE");
   bool one = m.rank_cw == 32 && m.rb_ngroups == m.rank_nwords;
+  // single-feature groups whose tables are all SMEM-resident: the lean
+  // column kernel (HB_RC_ONEK=0 keeps the staged kernel)
+  const char *eonek = std::getenv("HB_RC_ONEK");
+  if (one && !m.rb_global && !(eonek && *eonek && std::atoi(eonek) == 0) && !(ev && *ev && std::atoi(ev) >= 0)) {
+    auto fn1 = m.cmp == HB_CMP_LE ? rank_code_one_kernel<true> : rank_code_one_kernel<false>;
+    const int smem1 = (int)tbytes;
+    cudaError_t e1 = cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+    if (e1 != cudaSuccess) return cuda_fail(e1, "cudaFuncSetAttribute(rank codes one)");
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / std::max<size_t>(tbytes, 1)));
+    const int64_t units = (nblocks + kOneU - 1) / kOneU;
+    const int64_t want = std::max<int64_t>(1, ((int64_t)per_sm * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
+    const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(want, (units + kRcWarps - 1) / kRcWarps));
+    fn1<<<dim3(m.rb_ngroups, gy), 32 * kRcWarps, smem1, a.stream>>>(p);
+    e1 = cudaGetLastError();
+    if (e1 != cudaSuccess) return cuda_fail(e1, "rank_code_one_kernel launch");
+    return HB_OK;
+  }
   if (eone && *eone) one = m.rank_cw == 32 && std::atoi(eone) != 0;
   // 2 row blocks per stage: C3 13.13 ms per step (single-feature sets; 4
   // blocks: 13.39); feature pairs: 13.46 (4 blocks: 13.64)

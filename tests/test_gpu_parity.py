@@ -941,6 +941,30 @@ def test_rank_prepass_staged_spans(cw, rb, order, monkeypatch):
             check_all(e, m, Xd, Xh)
 
 
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_rank_code_one_kernel_edges(cmp, monkeypatch):
+    """The lean single-feature pre-pass kernel (rank_code_one_kernel: one
+    feature per CTA, 4 row blocks per warp step, next unit's X loads in
+    flight): scattered feature columns, an odd row stride, row counts that end
+    inside a 32-row block and inside a 4-block unit, fewer rows than one unit,
+    NaN / +-Inf / +-0 cells, thresholds at ties; leaf ids bit-exact and scores
+    within tolerance against the oracle, and identical to the staged kernel."""
+    _set_layout(monkeypatch, "pre32")
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")
+    used = np.sort(np.random.default_rng(31).choice(47, 19, replace=False))
+    e = synth.gen_forest(120, 8, 47, seed=40 + cmp, family="balanced", features=used, cmp=cmp,
+                         post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["rank_prepass"] == 1 and m.info["code_cell_bits"] == 32
+    for n, ldx in ((1, 47), (33, 49), (127, 47), (129, 47), (4 * 32 * 8 + 5, 51), (50_000, 47)):
+        Xd, Xh = X_pair(60 + n, n, 47, ldx=ldx, special_q24=SPECIAL_Q24)
+        check_all(e, m, Xd, Xh, kinds=("predict", "proba", "raw", "leaf_hash"))
+    monkeypatch.setenv("HB_RC_ONEK", "0")       # the staged kernel on the same model
+    m2 = hb.Model(e, strategy="ptt", device=0)
+    Xd, Xh = X_pair(7, 50_000, 47, special_q24=SPECIAL_Q24)
+    assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), m2.predict_leaf(Xd).cpu().numpy())
+
+
 def test_auto_layout_per_config():
     """AUTO picks, for each BASELINE config, the layout DESIGN.md §4 measured
     fastest: C1 any strategy (small-batch path per call), C2 rank-coded PTT
