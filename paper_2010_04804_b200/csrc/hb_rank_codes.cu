@@ -465,14 +465,19 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_one_kernel(const R
       base[i] = be & 0xFFFFu;
       cnt[i] = be >> 16;
     }
+    // binary search inside the bucket; a search whose bucket range is empty
+    // issues no further loads (predicated), so the shared-memory wavefronts
+    // follow the actual occupancy (~1 threshold per bucket), not S_max
     for (uint32_t k = 0; k < smax; ++k) {
 #pragma unroll
       for (int i = 0; i < kOneU; ++i) {
-        const uint32_t half = cnt[i] >> 1;
-        const float v = dev::lds_f32(ubase + 4u * (base[i] + half));
-        const bool go = (LE ? v < x[i] : v <= x[i]) && cnt[i] != 0u;
-        base[i] += go ? half + 1u : 0u;
-        cnt[i] = go ? cnt[i] - half - 1u : half;
+        if (cnt[i] != 0u) {
+          const uint32_t half = cnt[i] >> 1;
+          const float v = dev::lds_f32(ubase + 4u * (base[i] + half));
+          const bool go = LE ? v < x[i] : v <= x[i];
+          base[i] += go ? half + 1u : 0u;
+          cnt[i] = go ? cnt[i] - half - 1u : half;
+        }
       }
     }
     uint32_t *dst = p.codes + ((size_t)u * kOneU * p.n_words + (size_t)wd) * 32 + lane;
