@@ -465,19 +465,17 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_one_kernel(const R
       base[i] = be & 0xFFFFu;
       cnt[i] = be >> 16;
     }
-    // binary search inside the bucket; a search whose bucket range is empty
-    // issues no further loads (predicated), so the shared-memory wavefronts
-    // follow the actual occupancy (~1 threshold per bucket), not S_max
+    // binary search inside the bucket, S_max lockstep steps with
+    // unconditional loads (a predicated variant that skips finished searches
+    // diverged and measured slower: C3 pre-pass 1.39 -> 1.97 ms)
     for (uint32_t k = 0; k < smax; ++k) {
 #pragma unroll
       for (int i = 0; i < kOneU; ++i) {
-        if (cnt[i] != 0u) {
-          const uint32_t half = cnt[i] >> 1;
-          const float v = dev::lds_f32(ubase + 4u * (base[i] + half));
-          const bool go = LE ? v < x[i] : v <= x[i];
-          base[i] += go ? half + 1u : 0u;
-          cnt[i] = go ? cnt[i] - half - 1u : half;
-        }
+        const uint32_t half = cnt[i] >> 1;
+        const float v = dev::lds_f32(ubase + 4u * (base[i] + half));
+        const bool go = (LE ? v < x[i] : v <= x[i]) && cnt[i] != 0u;
+        base[i] += go ? half + 1u : 0u;
+        cnt[i] = go ? cnt[i] - half - 1u : half;
       }
     }
     uint32_t *dst = p.codes + ((size_t)u * kOneU * p.n_words + (size_t)wd) * 32 + lane;
@@ -524,7 +522,12 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   // single-feature groups whose tables are all SMEM-resident: the lean
   // column kernel (HB_RC_ONEK=0 keeps the staged kernel)
   const char *eonek = std::getenv("HB_RC_ONEK");
-  if (one && !m.rb_global && !(eonek && *eonek && std::atoi(eonek) == 0) && !(ev && *ev && std::atoi(ev) >= 0)) {
+  // Measured: C3 (28 single-feature groups, ~34 KB tables) 1.65 -> 1.39 ms;
+  // C4 (54 groups, ~48 KB tables) 2.34 -> 2.67 ms, so the staged kernel keeps
+  // models with more than 32 groups (HB_RC_ONEK=1 forces the column kernel)
+  const bool onek_auto = m.rb_ngroups <= 32;
+  const bool onek = eonek && *eonek ? std::atoi(eonek) != 0 : onek_auto;
+  if (one && !m.rb_global && onek && !(ev && *ev && std::atoi(ev) >= 0)) {
     auto fn1 = m.cmp == HB_CMP_LE ? rank_code_one_kernel<true> : rank_code_one_kernel<false>;
     const int smem1 = (int)tbytes;
     cudaError_t e1 = cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);

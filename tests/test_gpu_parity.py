@@ -951,6 +951,7 @@ def test_rank_code_one_kernel_edges(cmp, monkeypatch):
     within tolerance against the oracle, and identical to the staged kernel."""
     _set_layout(monkeypatch, "pre32")
     monkeypatch.setenv("HB_SMALL_BATCH", "0")
+    monkeypatch.setenv("HB_RC_ONEK", "1")
     used = np.sort(np.random.default_rng(31).choice(47, 19, replace=False))
     e = synth.gen_forest(120, 8, 47, seed=40 + cmp, family="balanced", features=used, cmp=cmp,
                          post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
