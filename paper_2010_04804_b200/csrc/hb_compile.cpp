@@ -268,7 +268,7 @@ uint32_t host_bucket(float x, float lo, float hi, float s, uint32_t B) {
 // Bucket tables for the sorted distinct thresholds of each compact feature
 // (sorted[c], feature id orig[c]); words group 1 (CW 32) or 2 (CW 16) features.
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
-                             int cw, RankBuckets *out, size_t cap_bytes) {
+                             int cw, RankBuckets *out, size_t cap_bytes, int density, bool one_per_group) {
   // per-CTA table budget: 48 KB -> 4 CTAs (32 warps) per SM (HB_RC_SMEM_KB overrides)
   const char *ev = std::getenv("HB_RC_SMEM_KB");
   const size_t cap = cap_bytes ? cap_bytes
@@ -293,10 +293,11 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
         any = true;
       }
     // <= 2 thresholds per bucket on average (HB_RC_DENSITY=d: <= 2/d)
-    static const int dens = [] {
+    static const int dens_env = [] {
       const char *e = std::getenv("HB_RC_DENSITY");
       return e && *e ? std::max(1, std::atoi(e)) : 1;
     }();
+    const int dens = density > 0 ? density : dens_env;
     uint32_t B = 1;
     while (2 * B < m * (uint32_t)dens && B < 16384u) B <<= 1;
     float s = 0.f;
@@ -368,7 +369,7 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
   for (int wd = 0; wd < n_words; ++wd) {
     size_t wb = 0;
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
-    if (gbytes > 0 && gbytes + wb > cap) close(wd);
+    if (gbytes > 0 && (one_per_group || gbytes + wb > cap)) close(wd);
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) {
       const int c = wd * per_word + q;
       uint32_t *fm = R.feat.data() + (size_t)c * 8;
@@ -643,7 +644,14 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     for (int f = 0; f < F; ++f)
       if (fc_of[f] >= 0) origf.push_back(f);
     RankBuckets R;
-    const hb_status st = build_rank_buckets(sorted, origf, cw, &R);
+    // at most 32 used features with 32-bit cells: the pre-pass runs the
+    // single-feature column kernel (hb_rank_codes.cu), one table per CTA;
+    // HB_RC_ONE_DENS / HB_RC_ONE_CAP_KB size those tables (measured, §4.6.1)
+    const bool colk = cw == 32 && A.n_fc <= 32;
+    const hb_status st = colk ? build_rank_buckets(sorted, origf, cw, &R,
+                                                   (size_t)env_int2("HB_RC_ONE_CAP_KB", 48) * 1024,
+                                                   env_int2("HB_RC_ONE_DENS", 1), true)
+                              : build_rank_buckets(sorted, origf, cw, &R);
     if (st != HB_OK) return st;
     const size_t fb = R.feat.size() * 4, gb = R.groups.size() * 4;
     const size_t pool_off = (fb + gb + 127) & ~size_t(127);

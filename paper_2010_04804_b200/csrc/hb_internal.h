@@ -163,7 +163,8 @@ struct RankBuckets {
   bool any_global = false;        // some group's table exceeds the cap (searched from global memory)
 };
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
-                             int cw, RankBuckets *out, size_t cap_bytes = 0);
+                             int cw, RankBuckets *out, size_t cap_bytes = 0, int density = 0,
+                             bool one_per_group = false);
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);

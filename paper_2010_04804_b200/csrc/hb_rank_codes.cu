@@ -409,8 +409,8 @@ RcFn staged_pick(bool le, int cw, int rb, bool one) {
 // and 2 codes in the staged kernel, ncu round 2).
 constexpr int kOneU = 4;
 
-template <bool LE>
-__global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_one_kernel(const RankCodeParams p) {
+template <bool LE, int NWARP>
+__global__ void __launch_bounds__(32 * NWARP, NWARP == 8 ? 4 : 2) rank_code_one_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int gi = blockIdx.x;                        // table group = one feature = one code word
   const uint4 g = __ldg(p.groups + 2 * gi);
@@ -451,11 +451,11 @@ __global__ void __launch_bounds__(32 * kRcWarps, 4) rank_code_one_kernel(const R
   float xn[kOneU];
   int64_t u = ubeg + warp;
   if (u < uend) load(u, xn);
-  for (; u < uend; u += kRcWarps) {
+  for (; u < uend; u += NWARP) {
     float x[kOneU];
 #pragma unroll
     for (int i = 0; i < kOneU; ++i) x[i] = xn[i];
-    if (u + kRcWarps < uend) load(u + kRcWarps, xn);   // next unit's loads in flight
+    if (u + NWARP < uend) load(u + NWARP, xn);   // next unit's loads in flight
     uint32_t base[kOneU], cnt[kOneU];
 #pragma unroll
     for (int i = 0; i < kOneU; ++i) {
@@ -528,15 +528,18 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   const bool onek_auto = m.rb_ngroups <= 32;
   const bool onek = eonek && *eonek ? std::atoi(eonek) != 0 : onek_auto;
   if (one && !m.rb_global && onek && !(ev && *ev && std::atoi(ev) >= 0)) {
-    auto fn1 = m.cmp == HB_CMP_LE ? rank_code_one_kernel<true> : rank_code_one_kernel<false>;
+    const char *ewp = std::getenv("HB_RC_ONE_WARPS");
+    const int ow = ewp && *ewp && std::atoi(ewp) == 16 ? 16 : 8;
+    auto fn1 = ow == 16 ? (m.cmp == HB_CMP_LE ? rank_code_one_kernel<true, 16> : rank_code_one_kernel<false, 16>)
+                        : (m.cmp == HB_CMP_LE ? rank_code_one_kernel<true, 8> : rank_code_one_kernel<false, 8>);
     const int smem1 = (int)tbytes;
     cudaError_t e1 = cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
     if (e1 != cudaSuccess) return cuda_fail(e1, "cudaFuncSetAttribute(rank codes one)");
-    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / std::max<size_t>(tbytes, 1)));
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(32 / ow, (220 * 1024) / std::max<size_t>(tbytes, 1)));
     const int64_t units = (nblocks + kOneU - 1) / kOneU;
     const int64_t want = std::max<int64_t>(1, ((int64_t)per_sm * sm_count(m.device) + m.rb_ngroups - 1) / m.rb_ngroups);
-    const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(want, (units + kRcWarps - 1) / kRcWarps));
-    fn1<<<dim3(m.rb_ngroups, gy), 32 * kRcWarps, smem1, a.stream>>>(p);
+    const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(want, (units + ow - 1) / ow));
+    fn1<<<dim3(m.rb_ngroups, gy), 32 * ow, smem1, a.stream>>>(p);
     e1 = cudaGetLastError();
     if (e1 != cudaSuccess) return cuda_fail(e1, "rank_code_one_kernel launch");
     return HB_OK;
