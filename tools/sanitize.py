@@ -30,6 +30,8 @@ cases = [
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "1"}, "ptt"),
     ("ptt-rank-prepass-staged-32-rb1", synth.gen_forest(40, 6, 12, seed=1),
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_STAGED": "1", "HB_RC_RB": "1"}, "ptt"),
+    ("ptt-rank-prepass-column", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_ONEK": "1"}, "ptt"),
     ("ptt-rank-prepass-rows8", synth.gen_forest(40, 6, 12, seed=1),
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "0", "HB_RC_ROWS": "8"}, "ptt"),
     ("tt-wide-chunks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
