@@ -85,10 +85,12 @@ typedef enum { HB_TASK_REGRESSION = 0, HB_TASK_CLASSIFICATION = 1 } hb_task;
 /* Compilation strategy (Sec. 4.1). AUTO applies the depth heuristic of
  * Sec. 5.1 with thresholds recalibrated on B200 (DESIGN.md §6.1,
  * reading R24): PTT if D_max <= 10, else TT; GEMM only when forced or when
- * env HB_GEMM_MAX_DEPTH is set (3 restores the paper's CPU rule). Independently
- * of the strategy, calls with n_rows <= hb_model_info.small_batch_max_rows
- * (4096; env HB_SMALL_BATCH read at compile time) use the trees-across-threads
- * small-batch kernel (small batches favour other kernels). */
+ * env HB_GEMM_MAX_DEPTH is set (3 restores the paper's CPU rule). For AUTO
+ * models, calls with n_rows <= hb_model_info.small_batch_max_rows (4096) use
+ * the trees-across-threads small-batch kernel (small batches
+ * favour other kernels); a forced strategy runs its own kernel at every batch
+ * size (small_batch_max_rows = 0) unless env HB_SMALL_BATCH is set at compile
+ * time (the test / sweep override).  */
 typedef enum {
   HB_STRATEGY_AUTO = 0,
   HB_STRATEGY_GEMM = 1,

@@ -791,7 +791,11 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
   // request/response sizes: trees-across-threads kernel (f2) for n_rows <=
   // small_max; threshold from the crossover sweep (tools/crossover.py,
   // DESIGN.md §6.2), env HB_SMALL_BATCH overrides (0: off) at compile time
-  m->small_max = m->sb_trees ? std::max(0, env_int("HB_SMALL_BATCH", 4096)) : 0;
+  // A forced strategy is honoured at every batch size: the small-batch
+  // kernel serves AUTO models only, unless HB_SMALL_BATCH is set explicitly
+  const char *sbe = std::getenv("HB_SMALL_BATCH");
+  const bool sb_on = strategy == HB_STRATEGY_AUTO || (sbe && *sbe);
+  m->small_max = (m->sb_trees && sb_on) ? std::max(0, env_int("HB_SMALL_BATCH", 4096)) : 0;
 
   // global per-output tree counts (MEAN divisor) and base score
   std::vector<float> div(K, 1.f), base(K + 1, 0.f);   // base[K] = post_param
