@@ -144,6 +144,21 @@ __device__ __forceinline__ void load_x_slice(float *xs, const float *__restrict_
     const float *xr = X + row * ldx;
     int f = 0;
     if (vec4) {
+      // 8 independent 16-B loads in flight per lane before their stores: the
+      // slice waits one memory latency per 32 columns, not per 4 (wide rows,
+      // e.g. the Fig. 8 shape's 200 columns, are load-latency bound otherwise)
+      for (; f + 32 <= F; f += 32) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const float4 *>(xr + f + 4 * u));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          xs[(f + 4 * u + 0) * 32 + lane] = v[u].x;
+          xs[(f + 4 * u + 1) * 32 + lane] = v[u].y;
+          xs[(f + 4 * u + 2) * 32 + lane] = v[u].z;
+          xs[(f + 4 * u + 3) * 32 + lane] = v[u].w;
+        }
+      }
       for (; f + 4 <= F; f += 4) {
         float4 v = __ldg(reinterpret_cast<const float4 *>(xr + f));
         xs[(f + 0) * 32 + lane] = v.x;

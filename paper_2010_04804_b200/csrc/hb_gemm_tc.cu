@@ -170,7 +170,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemm_tc_kernel(const TcParams p
     if (p.x_smem) {
       const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
       if (p.vec4 && !p.fmap) {
-        for (int j = part; 4 * j < p.F; j += 4) {
+        // this thread's 16-B chunks j = part, part + 4, ...: 4 loads in flight
+        // before their stores (one memory latency per 4 chunks)
+        const int F4 = p.F >> 2;
+        int j = part;
+        for (; j + 12 < F4; j += 16) {
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            v[u] = row < p.n ? __ldg(reinterpret_cast<const float4 *>(xr + 4 * (j + 4 * u)))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int f = 4 * (j + 4 * u);
+            xs[(f + 0) * 32 + lane] = v[u].x;
+            xs[(f + 1) * 32 + lane] = v[u].y;
+            xs[(f + 2) * 32 + lane] = v[u].z;
+            xs[(f + 3) * 32 + lane] = v[u].w;
+          }
+        }
+        for (; 4 * j < p.F; j += 4) {
           const int f = 4 * j;
           if (f + 4 <= p.F) {
             const float4 v = row < p.n ? __ldg(reinterpret_cast<const float4 *>(xr + f))
