@@ -607,6 +607,22 @@ def run_ours(args):
         parity = parity_report(m, e, cfg, X, tm["rows"], t0, t1, kind, cls)
         if mode == "trees" and whole is False:
             parity["scope"] = f"tree shard [{t0}, {t1}) raw fp64 partials and leaf hashes"
+            if dist and world == max(world, args.emulate_gpus):
+                # the NCCL-reduced, finalized output of the whole ensemble on
+                # rank 0 (last timed step) against the full-model oracle
+                import oracle
+                rf = min(10_000, n)
+                Xf = synth.gen_X(cfg.seed_x, rf, cfg.n_features)
+                rawf, _ = oracle.raw_and_hash(e, Xf, threads=0)
+                postf = oracle.post(e, oracle.margin(e, rawf))
+                ref = oracle.proba(e, postf) if cls else postf
+                got = out[:rf].double().cpu().numpy()
+                d = np.abs(got - ref)
+                parity["final_output"] = {
+                    "rows": rf, "kind": kind, "max_abs_err": float(d.max()),
+                    "outside_tol": int((d > 1e-5 + 1e-5 * np.abs(ref)).sum()),
+                    "scope": f"{kind} of all {e.n_trees} trees after the reduce over {world} ranks"}
+                parity["pass"] = parity["pass"] and parity["final_output"]["outside_tol"] == 0
 
     if rank == 0:
         cfgd = dict(workload_config(cfg, e, rows_all, args, mode, scaling, world), strategy=info["strategy_name"],

@@ -95,10 +95,14 @@ def test_multi_rank_bench_on_one_device(cfg, extra):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    d = _torchrun(["--config", cfg, "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e"] + extra)
+    d = _torchrun(["--config", cfg, "--steps", "2", "--warmup", "3", "--no-e2e"]
+                  + (["--no-cpu"] if cfg == "C3" else []) + extra)
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["scaling"] == "strong"
     assert d["config"]["trees_per_gpu"] == (500 if cfg == "C3" else 5000)
+    if cfg == "C5":   # the reduced, finalized output of all 10k trees against the oracle
+        fo = d["parity"]["final_output"]
+        assert fo["outside_tol"] == 0 and fo["rows"] == 2000 and d["parity"]["pass"]
     if cfg == "C3":   # BASELINE C3: 10M rows sharded over the GPUs (strong scaling)
         assert d["config"]["rows_total"] == 10_000_000 and d["config"]["rows_per_gpu"] == 5_000_000
         assert d["value"] == pytest.approx(10_000_000 / (d["ms_per_step"] * 1e-3), rel=1e-6)
