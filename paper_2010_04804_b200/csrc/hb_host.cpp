@@ -703,7 +703,6 @@ static hb_status compile_impl(const hb_ensemble *e, int t0, int t1, int strategy
         c.ch = kTreeGroup;
         m->cfg = c;
         m->tt_g = env_int("HB_TT_G", 4);   // walks per lane (DESIGN.md §4.3 sweep)
-        m->tt_refill = env_int("HB_TT_REFILL", 0);
         WideLayout W;
         st = build_ttw(e, t0, t1, m->n_trees_pad, &fmap, m->cfg.wide_rows, &W);
         if (st != HB_OK) return st;

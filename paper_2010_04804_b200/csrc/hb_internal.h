@@ -96,7 +96,6 @@ struct Model {
 
   int tt_chunk = 0;          // tt_wide_kernel: trees per L2-resident chunk (0: one launch)
   int tt_g = 4;              // tt_wide_kernel: concurrent walks per lane (4; 6, 8 for K = 1)
-  int tt_refill = 0;         // tt_wide_kernel: refill finished walks (value outputs, w = 1)
   // tt_wide_kernel records (hb_host.cpp build_ttw): packed trees of 16-B
   // internal-node records + per-tree offsets in 16-B units
   void *d_ttw = nullptr;

@@ -218,7 +218,7 @@ __device__ __forceinline__ void wide_step(const uint4 *tr, uint32_t &q, uint32_t
   }
 }
 
-template <bool LE, int NACC, int R, int G, bool REFILL = false>   // G: trees walked at once per lane
+template <bool LE, int NACC, int R, int G>   // G: trees walked at once per lane
 __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int L = 32 / R;                       // tree slots per warp
@@ -343,53 +343,6 @@ __global__ void __launch_bounds__(1024, 1) tt_wide_kernel(const TtParams p) {
       }
     };
     const int levels = p.depth > 0 ? p.depth : 1;   // a single-leaf tree still has one record
-    if (REFILL) {
-      // Value outputs of scalar-leaf models (opt-in HB_TT_REFILL): each of a
-      // lane's G walk slots runs its own sequence of trees (t += G * slots)
-      // and starts the next tree as soon as its walk reaches a leaf, so no
-      // slot idles while the warp's deepest path finishes; the warp loops
-      // until every slot of every lane ran out of trees.
-      const int tstep = G * slots;
-      int t[G];
-      uint32_t ofs[G], q[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        t[g] = warp * L + sub + g * slots;
-        ofs[g] = __ldg(p.toff + min(t[g], p.n_trees_pad - 1));
-        q[g] = 0;
-      }
-      while (true) {
-        bool any = false;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          if (t[g] < p.n_trees_pad) {
-            any = true;
-            const uint4 d = __ldg(p.ttw + ofs[g] + 1 + q[g]);
-            const float x = dev::lds_f32(xlane + (d.x & ~3u));
-            const float th = __uint_as_float(d.y);
-            const bool pr = LE ? (x <= th) : (x < th);
-            const uint32_t nx = pr ? d.z : d.w;
-            if (d.x & (pr ? 1u : 2u)) {            // reached a leaf: add it, next tree
-              const double v = (double)__uint_as_float(nx);
-              if (NACC == 1) {
-                acc[0] += v;
-              } else {
-                const uint32_t k0 = __ldg(reinterpret_cast<const uint32_t *>(p.ttw + ofs[g]) + 2);
-#pragma unroll
-                for (int k = 0; k < NACC; ++k)
-                  if (k0 == (uint32_t)k) acc[k] += v;
-              }
-              t[g] += tstep;
-              ofs[g] = __ldg(p.toff + min(t[g], p.n_trees_pad - 1));
-              q[g] = 0;
-            } else {
-              q[g] = nx;
-            }
-          }
-        }
-        if (!__any_sync(0xFFFFFFFFu, any)) break;
-      }
-    } else
     // warp-uniform loop over groups of G tree slots (t = base + sub + g*slots)
     for (int base = warp * L; base < p.n_trees_pad; base += G * slots) {
       const uint4 *tr[G];
@@ -472,8 +425,7 @@ static TtFn pick_nacc(int nacc) {
 int sm_count(int device);
 
 template <bool LE, int R>
-static TtFn pick_wide_nacc(int nacc, int g, bool refill) {
-  if (refill && nacc == 1) return tt_wide_kernel<LE, 1, R, 4, true>;
+static TtFn pick_wide_nacc(int nacc, int g) {
   // 6 or 8 concurrent walks per lane: scalar outputs only (registers)
   if (nacc == 1 && g == 8) return tt_wide_kernel<LE, 1, R, 8>;
   if (nacc == 1 && g == 6) return tt_wide_kernel<LE, 1, R, 6>;
@@ -486,22 +438,18 @@ static TtFn pick_wide_nacc(int nacc, int g, bool refill) {
 }
 
 template <bool LE>
-static TtFn pick_wide(int R, int nacc, int g, bool refill) {
+static TtFn pick_wide(int R, int nacc, int g) {
   switch (R) {
-    case 32: return pick_wide_nacc<LE, 32>(nacc, g, refill);
-    case 16: return pick_wide_nacc<LE, 16>(nacc, g, refill);
-    default: return pick_wide_nacc<LE, 8>(nacc, g, refill);
+    case 32: return pick_wide_nacc<LE, 32>(nacc, g);
+    case 16: return pick_wide_nacc<LE, 16>(nacc, g);
+    default: return pick_wide_nacc<LE, 8>(nacc, g);
   }
 }
 
 hb_status launch_tt(const Model &m, const RunArgs &a) {
   const bool wide = m.cfg.wide_rows > 0;
-  // refill schedule: value outputs of scalar-leaf models only (the leaf-id
-  // outputs and vector leaves keep the lockstep groups)
-  const bool refill = wide && m.tt_refill && m.leaf_width == 1 && a.kind != HB_OUT_LEAF &&
-                      a.kind != HB_OUT_LEAF_HASH;
-  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g, refill)
-                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g, refill))
+  TtFn fn = wide ? (m.cmp == HB_CMP_LE ? pick_wide<true>(m.cfg.wide_rows, m.nacc, m.tt_g)
+                                      : pick_wide<false>(m.cfg.wide_rows, m.nacc, m.tt_g))
                  : (m.cmp == HB_CMP_LE ? pick_nacc<true>(m.nacc) : pick_nacc<false>(m.nacc));
   TtParams p;
   p.X = a.X;
