@@ -647,7 +647,8 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     // at most 32 used features with 32-bit cells: the pre-pass runs the
     // single-feature column kernel (hb_rank_codes.cu), one table per CTA;
     // HB_RC_ONE_DENS / HB_RC_ONE_CAP_KB size those tables (measured, §4.6.1)
-    const bool colk = cw == 32 && A.n_fc <= 32;
+    const int nwords_colk = cw == 32 ? A.n_fc : (A.n_fc + 1) / 2;
+    const bool colk = nwords_colk <= env_int2("HB_RC_ONEK_MAX_GROUPS", 32);
     const hb_status st = colk ? build_rank_buckets(sorted, origf, cw, &R,
                                                    (size_t)env_int2("HB_RC_ONE_CAP_KB", 48) * 1024,
                                                    env_int2("HB_RC_ONE_DENS", 1), true)

@@ -409,10 +409,11 @@ RcFn staged_pick(bool le, int cw, int rb, bool one) {
 // and 2 codes in the staged kernel, ncu round 2).
 constexpr int kOneU = 4;
 
-template <bool LE, int NWARP>
+template <bool LE, int NWARP, int CW>
 __global__ void __launch_bounds__(32 * NWARP, NWARP == 8 ? 4 : 2) rank_code_one_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int gi = blockIdx.x;                        // table group = one feature = one code word
+  constexpr int PW = CW == 32 ? 1 : 2;              // features per code word
+  const int gi = blockIdx.x;                        // table group = one code word
   const uint4 g = __ldg(p.groups + 2 * gi);
   {
     const uint4 *src = reinterpret_cast<const uint4 *>(p.pool + g.x);
@@ -420,74 +421,110 @@ __global__ void __launch_bounds__(32 * NWARP, NWARP == 8 ? 4 : 2) rank_code_one_
     for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
   }
   __syncthreads();
-  const int wd = (int)g.z;                          // the word (= compact feature) of this group
-  const uint4 m0 = __ldg(p.feat + 2 * wd), m1 = __ldg(p.feat + 2 * wd + 1);
-  const float lo = __uint_as_float(m1.x), hi = __uint_as_float(m1.y), sc = __uint_as_float(m1.z);
-  const float bmax = (float)(m0.y - 1u);
-  const uint32_t smax = m0.z;
+  const int wd = (int)g.z;                          // the word of this group
   const uint32_t tab = dev::smem_u32(smem);
-  const uint32_t sbase = tab + m0.w, ubase = tab + m1.w;
-  const uint32_t cellhi = (uint32_t)wd << 23;
+  // per feature of the word: column, bucket map, search depth, table bases
+  const float *xcol[PW];
+  float lo[PW], hi[PW], sc[PW], bmax[PW];
+  uint32_t sbase[PW], ubase[PW];
+  bool okf[PW];
+  uint32_t smax = 0;
+#pragma unroll
+  for (int q = 0; q < PW; ++q) {
+    const int c = PW * wd + q;
+    okf[q] = c < p.n_fc;
+    const int cc = okf[q] ? c : PW * wd;
+    const uint4 m0 = __ldg(p.feat + 2 * cc), m1 = __ldg(p.feat + 2 * cc + 1);
+    xcol[q] = p.X + m0.x;
+    lo[q] = __uint_as_float(m1.x);
+    hi[q] = __uint_as_float(m1.y);
+    sc[q] = __uint_as_float(m1.z);
+    bmax[q] = (float)(m0.y - 1u);
+    sbase[q] = tab + m0.w;
+    ubase[q] = tab + m1.w;
+    if (okf[q]) smax = max(smax, m0.z);
+  }
+  const uint32_t cellhi = CW == 32 ? (uint32_t)wd << 23 : 0u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // this CTA's contiguous slice of units (U blocks each)
   const int64_t nunits = (p.nblocks + kOneU - 1) / kOneU;
   const int64_t ubeg = blockIdx.y * nunits / gridDim.y, uend = (blockIdx.y + 1) * nunits / gridDim.y;
-  const float *xcol = p.X + m0.x;                   // column f of X
   const int64_t rstride = 32 * p.ldx;               // one row block, in floats
-  auto load = [&](int64_t u, float (&x)[kOneU]) {
+  auto load = [&](int64_t u, float (&x)[PW][kOneU]) {
     const int64_t row0 = u * (kOneU * 32) + lane;
-    const float *ptr = xcol + row0 * p.ldx;
-    if (row0 + (kOneU - 1) * 32 < p.n) {
 #pragma unroll
-      for (int i = 0; i < kOneU; ++i) x[i] = __ldg(ptr + i * rstride);
-    } else {                                        // last unit: rows past n read row n - 1
+    for (int q = 0; q < PW; ++q) {
+      const float *ptr = xcol[q] + row0 * p.ldx;
+      if (row0 + (kOneU - 1) * 32 < p.n) {
 #pragma unroll
-      for (int i = 0; i < kOneU; ++i) {
-        const int64_t r = min(row0 + i * 32, p.n - 1);
-        x[i] = __ldg(xcol + r * p.ldx);
+        for (int i = 0; i < kOneU; ++i) x[q][i] = __ldg(ptr + i * rstride);
+      } else {                                      // last unit: rows past n read row n - 1
+#pragma unroll
+        for (int i = 0; i < kOneU; ++i) {
+          const int64_t r = min(row0 + i * 32, p.n - 1);
+          x[q][i] = __ldg(xcol[q] + r * p.ldx);
+        }
       }
     }
   };
-  float xn[kOneU];
+  float xn[PW][kOneU];
   int64_t u = ubeg + warp;
   if (u < uend) load(u, xn);
   for (; u < uend; u += NWARP) {
-    float x[kOneU];
+    float x[PW][kOneU];
 #pragma unroll
-    for (int i = 0; i < kOneU; ++i) x[i] = xn[i];
+    for (int q = 0; q < PW; ++q)
+#pragma unroll
+      for (int i = 0; i < kOneU; ++i) x[q][i] = xn[q][i];
     if (u + NWARP < uend) load(u + NWARP, xn);   // next unit's loads in flight
-    uint32_t base[kOneU], cnt[kOneU];
+    uint32_t base[PW][kOneU], cnt[PW][kOneU];
 #pragma unroll
-    for (int i = 0; i < kOneU; ++i) {
-      const float xc = fminf(fmaxf(x[i], lo), hi);      // NaN -> lo; replaced below
-      const float y = fminf(__fmul_rn(__fsub_rn(xc, lo), sc), bmax);
-      const uint32_t be = dev::lds_u32(sbase + 4u * __float2uint_rz(y));
-      base[i] = be & 0xFFFFu;
-      cnt[i] = be >> 16;
-    }
+    for (int q = 0; q < PW; ++q)
+#pragma unroll
+      for (int i = 0; i < kOneU; ++i) {
+        const float xc = fminf(fmaxf(x[q][i], lo[q]), hi[q]);      // NaN -> lo; replaced below
+        const float y = fminf(__fmul_rn(__fsub_rn(xc, lo[q]), sc[q]), bmax[q]);
+        const uint32_t be = dev::lds_u32(sbase[q] + 4u * __float2uint_rz(y));
+        base[q][i] = be & 0xFFFFu;
+        cnt[q][i] = be >> 16;
+      }
     // binary search inside the bucket, S_max lockstep steps with
     // unconditional loads (a predicated variant that skips finished searches
     // diverged and measured slower: C3 pre-pass 1.39 -> 1.97 ms)
     for (uint32_t k = 0; k < smax; ++k) {
 #pragma unroll
-      for (int i = 0; i < kOneU; ++i) {
-        const uint32_t half = cnt[i] >> 1;
-        const float v = dev::lds_f32(ubase + 4u * (base[i] + half));
-        const bool go = (LE ? v < x[i] : v <= x[i]) && cnt[i] != 0u;
-        base[i] += go ? half + 1u : 0u;
-        cnt[i] = go ? cnt[i] - half - 1u : half;
-      }
+      for (int q = 0; q < PW; ++q)
+#pragma unroll
+        for (int i = 0; i < kOneU; ++i) {
+          const uint32_t half = cnt[q][i] >> 1;
+          const float v = dev::lds_f32(ubase[q] + 4u * (base[q][i] + half));
+          const bool go = (LE ? v < x[q][i] : v <= x[q][i]) && cnt[q][i] != 0u;
+          base[q][i] += go ? half + 1u : 0u;
+          cnt[q][i] = go ? cnt[q][i] - half - 1u : half;
+        }
     }
     uint32_t *dst = p.codes + ((size_t)u * kOneU * p.n_words + (size_t)wd) * 32 + lane;
 #pragma unroll
     for (int i = 0; i < kOneU; ++i) {
-      if (u * kOneU + i < p.nblocks)
-        dst[(size_t)i * p.n_words * 32] = cellhi | (x[i] != x[i] ? 0xFFFFu : base[i]);
+      if (u * kOneU + i < p.nblocks) {
+        const uint32_t c0 = x[0][i] != x[0][i] ? 0xFFFFu : base[0][i];
+        uint32_t w = cellhi | c0;
+        if (PW == 2) {
+          const uint32_t c1 = x[PW - 1][i] != x[PW - 1][i] ? 0xFFFFu : base[PW - 1][i];
+          w |= (okf[PW - 1] ? c1 : 0u) << 16;
+        }
+        dst[(size_t)i * p.n_words * 32] = w;
+      }
     }
   }
 }
 
 int sm_count(int device);
+
+static int env_int_rc(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
 
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks) {
   if (m.rb_ngroups == 0 || nblocks == 0) return HB_OK;   // no split uses any feature: no codes
@@ -525,13 +562,18 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   // Measured: C3 (28 single-feature groups, ~34 KB tables) 1.65 -> 1.39 ms;
   // C4 (54 groups, ~48 KB tables) 2.34 -> 2.67 ms, so the staged kernel keeps
   // models with more than 32 groups (HB_RC_ONEK=1 forces the column kernel)
-  const bool onek_auto = m.rb_ngroups <= 32;
+  const bool one_word = m.rb_ngroups == m.rank_nwords;   // one code word per table group
+  const bool onek_auto = m.rb_ngroups <= env_int_rc("HB_RC_ONEK_MAX_GROUPS", 32);
   const bool onek = eonek && *eonek ? std::atoi(eonek) != 0 : onek_auto;
-  if (one && !m.rb_global && onek && !(ev && *ev && std::atoi(ev) >= 0)) {
+  if (one_word && !m.rb_global && onek && !(ev && *ev && std::atoi(ev) >= 0)) {
     const char *ewp = std::getenv("HB_RC_ONE_WARPS");
     const int ow = ewp && *ewp && std::atoi(ewp) == 16 ? 16 : 8;
-    auto fn1 = ow == 16 ? (m.cmp == HB_CMP_LE ? rank_code_one_kernel<true, 16> : rank_code_one_kernel<false, 16>)
-                        : (m.cmp == HB_CMP_LE ? rank_code_one_kernel<true, 8> : rank_code_one_kernel<false, 8>);
+    const bool le = m.cmp == HB_CMP_LE;
+    RcFn fn1 = m.rank_cw == 16
+                   ? (ow == 16 ? (le ? rank_code_one_kernel<true, 16, 16> : rank_code_one_kernel<false, 16, 16>)
+                               : (le ? rank_code_one_kernel<true, 8, 16> : rank_code_one_kernel<false, 8, 16>))
+                   : (ow == 16 ? (le ? rank_code_one_kernel<true, 16, 32> : rank_code_one_kernel<false, 16, 32>)
+                               : (le ? rank_code_one_kernel<true, 8, 32> : rank_code_one_kernel<false, 8, 32>));
     const int smem1 = (int)tbytes;
     cudaError_t e1 = cudaFuncSetAttribute(fn1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
     if (e1 != cudaSuccess) return cuda_fail(e1, "cudaFuncSetAttribute(rank codes one)");
