@@ -275,6 +275,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("HB_BENCH_BACKEND", "nccl")   # gloo: 1-GPU multi-rank test
+        # communicator set-up (transports, NVLink / NVLS channels) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
