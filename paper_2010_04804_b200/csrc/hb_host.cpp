@@ -890,10 +890,12 @@ static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int
   }
   RunArgs a{X, n, ldx, kind, out, static_cast<cudaStream_t>(stream), nullptr};
   int k = 0;
+  cudaError_t ev_err = cudaSuccess;
   if (events && nev > 0) {
     a.ev = reinterpret_cast<cudaEvent_t *>(events);
     a.nev = nev;
     a.ev_k = &k;
+    a.ev_err = &ev_err;
   }
   mark_launch(a);
   // request/response sizes: trees-across-threads kernel (f2); threshold from
@@ -901,6 +903,7 @@ static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int
   st = n <= m.small_max ? launch_small_batch(m, a) : run(m, a);
   mark_launch(a);
   if (n_launches) *n_launches = k > 0 ? k - 1 : 0;
+  if (st == HB_OK && ev_err != cudaSuccess) return cuda_fail(ev_err, "cudaEventRecord(hb_predict_ex_events)");
   return st;
 }
 

@@ -129,11 +129,15 @@ struct RunArgs {
   cudaEvent_t *ev = nullptr;
   int nev = 0;
   int *ev_k = nullptr;
+  cudaError_t *ev_err = nullptr;   // first cudaEventRecord failure of the call
 };
 
 // record the next profiling event of a call (no-op without events)
 inline void mark_launch(const RunArgs &a) {
-  if (a.ev && a.ev_k && *a.ev_k < a.nev) cudaEventRecord(a.ev[(*a.ev_k)++], a.stream);
+  if (a.ev && a.ev_k && *a.ev_k < a.nev) {
+    const cudaError_t e = cudaEventRecord(a.ev[(*a.ev_k)++], a.stream);
+    if (e != cudaSuccess && a.ev_err && *a.ev_err == cudaSuccess) *a.ev_err = e;
+  }
 }
 
 bool gemm_supported(int depth);
