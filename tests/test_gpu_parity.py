@@ -606,6 +606,39 @@ def test_predict_host_multichunk_against_oracle(cfg, n, F):
         assert_scores(m.predict_host(Xp, "predict").numpy(), post, "predict")
 
 
+def test_predict_ex_events_counts_launches(monkeypatch):
+    """hb_predict_ex_events (the per-kernel timing bench.py's roofline uses):
+    the same result as hb_predict_ex, one event at the start of every launch
+    and one after the last, so elapsed times are positive and add up; two
+    launches for a pre-pass model, one per tree chunk (+ finalize) for a
+    chunked TT model, one otherwise."""
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")
+    cases = []
+    monkeypatch.setenv("HB_RANK_PRE", "1")
+    monkeypatch.setenv("HB_PTT_RANK", "1")
+    cases.append((_forest("binary", 64, 8, 28, 3, "balanced", 0), "ptt", 2, 28))
+    monkeypatch.setenv("HB_RANK_PRE", "0")
+    monkeypatch.setenv("HB_PTT_RANK", "0")
+    cases.append((_forest("binary", 64, 6, 28, 4, "balanced", 0), "ptt", 1, 28))
+    monkeypatch.setenv("HB_TT_WIDE", "1")
+    monkeypatch.setenv("HB_TT_CHUNK", "16")
+    cases.append((_forest("binary", 45, 9, 37, 5, "mixed", 0), "tt", 3 + 1, 37))   # 3 chunks + finalize
+    for e, strat, want, F in cases:
+        m = hb.Model(e, strategy=strat, device=0)
+        Xd, _ = X_pair(9, 5000, F)
+        ref = m.run(Xd, "proba")
+        out = torch.empty_like(ref)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(want + 1)]
+        s = torch.cuda.current_stream()
+        for ev in evs:
+            ev.record(s)
+        nl = m.run_events(Xd, "proba", out, evs, s)
+        torch.cuda.synchronize()
+        assert nl == want and torch.equal(out, ref)
+        parts = [evs[i].elapsed_time(evs[i + 1]) for i in range(want)]
+        assert all(t >= 0 for t in parts) and sum(parts) > 0
+
+
 def test_host_and_device_generators_agree():
     for grid, sp in ((0, 0), (1, 0), (0, SPECIAL_Q24)):
         Xd, Xh = X_pair(77, 5000, 37, grid=grid, special_q24=sp, row_offset=12345)
