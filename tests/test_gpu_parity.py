@@ -616,15 +616,17 @@ def test_predict_ex_events_counts_launches(monkeypatch):
     cases = []
     monkeypatch.setenv("HB_RANK_PRE", "1")
     monkeypatch.setenv("HB_PTT_RANK", "1")
-    cases.append((_forest("binary", 64, 8, 28, 3, "balanced", 0), "ptt", 2, 28))
+    # compile each model while its layout variables are set
+    cases.append((hb.Model(_forest("binary", 64, 8, 28, 3, "balanced", 0), strategy="ptt", device=0), 2, 28))
     monkeypatch.setenv("HB_RANK_PRE", "0")
     monkeypatch.setenv("HB_PTT_RANK", "0")
-    cases.append((_forest("binary", 64, 6, 28, 4, "balanced", 0), "ptt", 1, 28))
+    cases.append((hb.Model(_forest("binary", 64, 6, 28, 4, "balanced", 0), strategy="ptt", device=0), 1, 28))
     monkeypatch.setenv("HB_TT_WIDE", "1")
     monkeypatch.setenv("HB_TT_CHUNK", "16")
-    cases.append((_forest("binary", 45, 9, 37, 5, "mixed", 0), "tt", 3 + 1, 37))   # 3 chunks + finalize
-    for e, strat, want, F in cases:
-        m = hb.Model(e, strategy=strat, device=0)
+    cases.append((hb.Model(_forest("binary", 45, 9, 37, 5, "mixed", 0), strategy="tt", device=0),
+                  3 + 1, 37))   # 3 chunks + finalize
+    assert cases[0][0].info["rank_prepass"] == 1 and cases[1][0].info["rank_prepass"] == 0
+    for m, want, F in cases:
         Xd, _ = X_pair(9, 5000, F)
         ref = m.run(Xd, "proba")
         out = torch.empty_like(ref)
