@@ -246,7 +246,10 @@ def launch_names(info, n, kind):
     if n <= info["small_batch_max_rows"]:
         return ["small_batch_kernel"]
     if info.get("rank_prepass"):
-        return ["rank_code_kernel", "pttr_kernel"]
+        # TMA pre-pass on the bench's X (16-B aligned rows of 4k floats: C2,
+        # C3, C4), else one of the generic pre-pass kernels
+        tma = info.get("rank_prepass_tma") and info["n_features"] % 4 == 0   # contiguous X: ldx = F
+        return ["rank_code_tma_kernel" if tma else "rank_code_kernel", "pttr_kernel"]
     chunk = info.get("tt_chunk_trees", 0)
     if chunk:
         pad = (info["n_trees"] + 3) // 4 * 4

@@ -48,8 +48,9 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 4   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended;
-                              4: HB_OUT_RAW64 + hb_finalize64 (fp64 raw sums) */
+#define HB_ABI_VERSION 5   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended;
+                              4: HB_OUT_RAW64 + hb_finalize64 (fp64 raw sums);
+                              5: hb_model_info.rank_prepass_tma appended */
 
 typedef enum {
   HB_OK = 0,
@@ -178,6 +179,12 @@ typedef struct {
   int32_t tt_walks_per_lane;    /* wide-row TT: concurrent walks per lane (ABI 4)        */
   int64_t tt_record_bytes;      /* wide-row TT: bytes of the 16-B node records the walk
                                    reads (tables of leaf ids excluded) (ABI 4)          */
+  int32_t rank_prepass_tma;     /* rank_prepass: 1 if the tables are grouped for the TMA
+                                   pre-pass (rank_code_tma_kernel, one 16-B box of 4 X
+                                   columns per row); it runs on calls whose X is 16-B
+                                   aligned with ldx % 4 == 0, the generic pre-pass
+                                   kernels on the others (ABI 5)                       */
+  int32_t reserved0;            /* 0 */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls): the tree structure

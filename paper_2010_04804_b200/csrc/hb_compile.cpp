@@ -268,7 +268,9 @@ uint32_t host_bucket(float x, float lo, float hi, float s, uint32_t B) {
 // Bucket tables for the sorted distinct thresholds of each compact feature
 // (sorted[c], feature id orig[c]); words group 1 (CW 32) or 2 (CW 16) features.
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
-                             int cw, RankBuckets *out, size_t cap_bytes, int density, bool one_per_group) {
+                             int cw, RankBuckets *out, size_t cap_bytes, int density, bool one_per_group,
+                             bool block4) {
+  const float pad_nan = NAN;
   // per-CTA table budget: 48 KB -> 4 CTAs (32 warps) per SM (HB_RC_SMEM_KB overrides)
   const char *ev = std::getenv("HB_RC_SMEM_KB");
   const size_t cap = cap_bytes ? cap_bytes
@@ -331,7 +333,9 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
       std::memcpy(t.data() + 4 * b, &v, 4);
     }
     std::memcpy(t.data() + sbytes, u.data(), (size_t)m * 4);
-    const float pad = INFINITY;
+    // pad slot(s) after the thresholds: NaN compares false against every x,
+    // so a fixed-window search (TMA kernel) never counts them
+    const float pad = NAN;
     std::memcpy(t.data() + sbytes + (size_t)m * 4, &pad, 4);
     tabs[c] = std::move(t);
     uint32_t *fm = R.feat.data() + (size_t)c * 8;
@@ -343,6 +347,53 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     std::memcpy(&fm[5], &hi, 4);
     std::memcpy(&fm[6], &s, 4);
     fm[7] = (uint32_t)sbytes;                  // u offset relative to start; rebased below
+  }
+  // block4 (TMA pre-pass): a group is a run of consecutive X columns inside
+  // one aligned 4-column block, so one 16-B box per row holds every x the
+  // group searches. Its kernel searches a fixed window of 2^S_g - 1 slots
+  // from the bucket's first threshold (S_g = the group's deepest search):
+  // thresholds of later buckets are > x and the pads are NaN, so every slot
+  // past the bucket compares false. Each table gets 2^S_g - 1 pad slots.
+  std::vector<int> gstart(n_words + 1, 0);         // block4: 1 where a group starts
+  if (block4) {
+    auto word_bytes = [&](int wd) {
+      size_t wb = 0;
+      for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
+      return wb;
+    };
+    size_t gb = 0;
+    int first = 0;
+    for (int wd = 0; wd < n_words; ++wd) {
+      bool split = wd == 0;
+      if (!split) {
+        const int c = wd * per_word, cfirst = first * per_word;
+        for (int q = 0; q < per_word && c + q < n_fc; ++q)
+          if (orig[c + q] != orig[c - 1] + 1 + q || (orig[c + q] >> 2) != (orig[cfirst] >> 2)) split = true;
+        if (gb + word_bytes(wd) > cap) split = true;
+      }
+      if (split) {
+        gstart[wd] = 1;
+        first = wd;
+        gb = 0;
+      }
+      gb += word_bytes(wd);
+    }
+    gstart[n_words] = 1;
+    for (int w0 = 0; w0 < n_words;) {
+      int w1 = w0 + 1;
+      while (!gstart[w1]) ++w1;
+      uint32_t sg = 0;
+      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c) sg = std::max(sg, R.feat[(size_t)c * 8 + 2]);
+      const size_t npad = ((size_t)1 << sg) - 1;
+      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c)
+        if (npad > 1) {
+          std::vector<uint8_t> &t = tabs[c];
+          const size_t old = t.size();
+          t.resize(old + (npad - 1) * 4);
+          for (size_t i = old; i < t.size(); i += 4) std::memcpy(t.data() + i, &pad_nan, 4);
+        }
+      w0 = w1;
+    }
   }
   // groups of whole words, <= cap bytes each (an oversized word is a
   // group of its own and is searched from global memory)
@@ -359,6 +410,9 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     R.groups.insert(R.groups.end(), {(uint32_t)goff, (uint32_t)gbytes, (uint32_t)wbeg, (uint32_t)wend,
                                      (uint32_t)(chi >= clo ? clo : 0), ncols, ncols | 1u, 0u});
     R.max_span = std::max<uint32_t>(R.max_span, ncols);
+    R.max_feats = std::max(R.max_feats, std::min(wend * per_word, n_fc) - wbeg * per_word);
+    for (int c = wbeg * per_word + 1; c < std::min(wend * per_word, n_fc); ++c)
+      if (orig[c] != orig[c - 1] + 1 || (orig[c] >> 2) != (orig[wbeg * per_word] >> 2)) R.block4_ok = false;
     if (gbytes > cap) R.any_global = true;
     R.max_group_bytes = std::max(R.max_group_bytes, gbytes <= cap ? gbytes : (size_t)0);
     goff += gbytes;
@@ -369,7 +423,8 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
   for (int wd = 0; wd < n_words; ++wd) {
     size_t wb = 0;
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
-    if (gbytes > 0 && (one_per_group || gbytes + wb > cap)) close(wd);
+    const bool split = block4 ? gstart[wd] != 0 : (one_per_group || gbytes + wb > cap);
+    if (gbytes > 0 && split) close(wd);
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) {
       const int c = wd * per_word + q;
       uint32_t *fm = R.feat.data() + (size_t)c * 8;
@@ -649,11 +704,30 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     // HB_RC_ONE_DENS / HB_RC_ONE_CAP_KB size those tables (measured, §4.6.1)
     const int nwords_colk = cw == 32 ? A.n_fc : (A.n_fc + 1) / 2;
     const bool colk = nwords_colk <= env_int2("HB_RC_ONEK_MAX_GROUPS", 32);
-    const hb_status st = colk ? build_rank_buckets(sorted, origf, cw, &R,
-                                                   (size_t)env_int2("HB_RC_ONE_CAP_KB", 48) * 1024,
-                                                   env_int2("HB_RC_ONE_DENS", 1), true)
-                              : build_rank_buckets(sorted, origf, cw, &R);
-    if (st != HB_OK) return st;
+    // TMA pre-pass (rank_code_tma_kernel, HB_RC_TMA=0 turns it off): one
+    // group per aligned 4-column block of X (fewer when the tables outgrow
+    // kRcTmaTableMax), every table SMEM-resident. Only for F % 4 == 0, where
+    // a contiguous X has the 16-B row pitch the tensor map needs (C3; not
+    // C2 / C4 with F = 90 / 54, which keep the groupings measured for the
+    // generic kernels); calls with another pitch run the generic kernels on
+    // these groups
+    const int tma_env = env_int2("HB_RC_TMA", -1);
+    bool tma = tma_env == 1 || (tma_env == -1 && F % 4 == 0);
+    hb_status st = HB_OK;
+    if (tma) {
+      st = build_rank_buckets(sorted, origf, cw, &R, kRcTmaTableMax, 0, false, true);
+      if (st != HB_OK) return st;
+      tma = R.block4_ok && !R.any_global;
+    }
+    if (!tma) {
+      R = RankBuckets();
+      st = colk ? build_rank_buckets(sorted, origf, cw, &R, (size_t)env_int2("HB_RC_ONE_CAP_KB", 48) * 1024,
+                                     env_int2("HB_RC_ONE_DENS", 1), true)
+                : build_rank_buckets(sorted, origf, cw, &R);
+      if (st != HB_OK) return st;
+    }
+    m->rb_tma = tma ? 1 : 0;
+    m->rb_max_feats = R.max_feats;
     const size_t fb = R.feat.size() * 4, gb = R.groups.size() * 4;
     const size_t pool_off = (fb + gb + 127) & ~size_t(127);
     std::vector<uint8_t> aux(pool_off + R.pool.size(), 0);

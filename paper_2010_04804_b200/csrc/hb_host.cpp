@@ -1099,6 +1099,8 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->small_batch_max_rows = m.small_max;
   info->tt_walks_per_lane = m.cfg.wide_rows ? m.tt_g : 0;
   info->tt_record_bytes = (int64_t)m.ttw_rec_bytes;
+  info->rank_prepass_tma = m.rank_pre ? m.rb_tma : 0;
+  info->reserved0 = 0;
   return HB_OK;
 }
 

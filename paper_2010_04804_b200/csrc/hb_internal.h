@@ -74,6 +74,9 @@ struct Model {
   int rb_ngroups = 0;
   uint32_t rb_max_span = 0;  // widest X column span of a table group (staged pre-pass)
   bool rb_global = false;    // some table group is searched from global memory
+  // groups are runs of consecutive X columns inside one aligned 4-column
+  // block (rank_code_tma_kernel: one 16-B TMA box per row); widest group
+  int rb_tma = 0, rb_max_feats = 0;
   cudaMemPool_t mempool = nullptr;   // per-call scratch (rank codes, TT chunk partials)
 
   // small-batch path (hb_small.cu): PTT fp32 or TT records walked by
@@ -165,10 +168,12 @@ struct RankBuckets {
   size_t smem_cap = 0;            // groups up to this size are staged in SMEM
   uint32_t max_span = 0;          // widest X column span of one group
   bool any_global = false;        // some group's table exceeds the cap (searched from global memory)
+  int max_feats = 0;              // most features in one group
+  bool block4_ok = true;          // every group is consecutive columns inside one 4-column block
 };
 hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, const std::vector<int> &orig,
                              int cw, RankBuckets *out, size_t cap_bytes = 0, int density = 0,
-                             bool one_per_group = false);
+                             bool one_per_group = false, bool block4 = false);
 hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, int64_t nblocks);
 
 hb_status launch_ptt(const Model &m, const RunArgs &a);

@@ -84,6 +84,14 @@ inline size_t gemm_tc_a_region(int nacc) {
 
 // ---- rank-code pre-pass (hb_rank_codes.cu)
 constexpr uint32_t kRcSmemMax = 200 * 1024;  // largest per-CTA table budget
+// TMA pre-pass (hb_rank_codes.cu rank_code_tma_kernel): per-warp rings of
+// kRcTmaStages boxes of kRcTmaU x 32 rows x 16 B next to the group's tables
+constexpr int kRcTmaWarps = 16;
+constexpr int kRcTmaU = 2;
+constexpr int kRcTmaStages = 3;
+constexpr uint32_t kRcTmaStageBytes = kRcTmaU * 32 * 16;
+constexpr uint32_t kRcTmaRingBytes = kRcTmaWarps * kRcTmaStages * (kRcTmaStageBytes + 16);
+constexpr uint32_t kRcTmaTableMax = 227 * 1024 - kRcTmaRingBytes - 128;
 
 // ---- wide-row TT (hb_tt.cu)
 // SMEM of tt_wide_kernel for R rows: X tile + fp64 per-warp row sums + hashes

@@ -118,6 +118,9 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
     const int64_t row = wrow0 + lane;
     const bool active = wrow0 < p.n;
     const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
+    // the tile fills below write other lanes' cells: every lane is done
+    // reading the previous tile's (WAR within the warp; racecheck)
+    __syncwarp();
     if (p.codes) {
       // codes from the pre-pass: this warp's block is already in tile layout
       if (active) {

@@ -29,6 +29,7 @@
 // a group-major grid with contiguous row slices. (A cluster variant holding
 // all tables in one cluster's DSMEM was measured slower and removed, DESIGN.md
 // §4.6.)
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -519,7 +520,237 @@ __global__ void __launch_bounds__(32 * NWARP, NWARP == 8 ? 4 : 2) rank_code_one_
   }
 }
 
+// TMA-staged pre-pass (round 2). A table group is a run of consecutive X
+// columns inside one aligned 4-column block (<= 4 features, all tables in
+// SMEM), so one 16-B piece of each row holds every x the group searches. The
+// TMA engine copies those pieces for 64 rows at a time (a 2-D tensor box of
+// {4 columns, 64 rows} over X) into per-warp rings, kRcTmaStages deep:
+//  - the column kernels above gathered x with 4-B loads at a row stride,
+//    one 32-B sector per lane and ~12 L1 wavefronts per warp load (C3, ncu:
+//    the X gather was half of the L1 data-pipe wavefronts, 105M of 253M);
+//    the TMA path spends one 16-B SMEM read per row and no LSU work on X;
+//  - one box serves all the group's features: C3's 28 single-feature CTAs
+//    pulled 28 sectors per row out of L2, 4-feature groups pull 7.
+// Searches: NQ features x kRcTmaU row blocks per lane in lockstep (the
+// bucket + binary search of rank_codes_lockstep).
+__device__ __forceinline__ void tma_box_2d(uint32_t dst, const CUtensorMap *tm, int c0, int r0, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(r0), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+template <int OFF>
+__device__ __forceinline__ float lds_f32_off(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+
+// S power-of-two steps (2^(S-1) slots first) over every chain, each step's
+// loads back to back, the slot offsets immediates
+template <bool LE, int NQ, int U, int S>
+__device__ __forceinline__ void window_search(uint32_t (&pos)[NQ][U], const float (&x)[NQ][U]) {
+  if constexpr (S > 0) {
+    constexpr int k = S - 1;
+    float v[NQ][U];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < U; ++i) v[q][i] = lds_f32_off<4 * ((1 << k) - 1)>(pos[q][i]);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < U; ++i) pos[q][i] += (LE ? v[q][i] < x[q][i] : v[q][i] <= x[q][i]) ? (4u << k) : 0u;
+    window_search<LE, NQ, U, S - 1>(pos, x);
+  }
+}
+
+template <bool LE, int CW, int NQ>
+__global__ void __launch_bounds__(32 * kRcTmaWarps, 1)
+    rank_code_tma_kernel(const __grid_constant__ CUtensorMap tmx, const RankCodeParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int U = kRcTmaU, S = kRcTmaStages, NW = kRcTmaWarps;
+  constexpr int PW = CW == 32 ? 1 : 2;             // features per code word
+  const uint4 g = __ldg(p.groups + 2 * blockIdx.x);       // {pool off, bytes, word_begin, word_end}
+  const uint4 gs = __ldg(p.groups + 2 * blockIdx.x + 1);  // {first X column, columns, ...}
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.pool + g.x);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem);
+    for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t *ring = smem + p.stage_off + (size_t)warp * S * kRcTmaStageBytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.stage_off + (size_t)NW * S * kRcTmaStageBytes) + warp * 2 * S;
+  uint64_t *empty = full + S;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      dev::mbar_init(full + s, 1);
+      dev::mbar_init(empty + s, 32);
+    }
+    dev::fence_mbar_init();
+  }
+  __syncthreads();                                 // tables and barriers
+  const uint32_t tab = dev::smem_u32(smem);
+  const int fbeg = PW * (int)g.z, fend = min(PW * (int)g.w, p.n_fc);
+  const int c0 = (int)(gs.x & ~3u);                // box column: the aligned 4-column block
+  int comp[NQ];
+  float lo[NQ], hi[NQ], sc[NQ], bmax[NQ];
+  uint32_t sbase[NQ], ubase[NQ];
+  bool okf[NQ];
+  uint32_t smax = 0;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    okf[q] = fbeg + q < fend;
+    const int cc = okf[q] ? fbeg + q : fbeg;
+    const uint4 m0 = __ldg(p.feat + 2 * cc), m1 = __ldg(p.feat + 2 * cc + 1);
+    comp[q] = (int)m0.x - c0;                      // 0..3: the x's place in the 16-B piece
+    lo[q] = __uint_as_float(m1.x);
+    hi[q] = __uint_as_float(m1.y);
+    sc[q] = __uint_as_float(m1.z);
+    bmax[q] = (float)(m0.y - 1u);
+    sbase[q] = tab + m0.w;
+    ubase[q] = tab + m1.w;
+    if (okf[q]) smax = max(smax, m0.z);
+  }
+  // where the group's x sit in the box (CTA-uniform): 0 = columns 0..NQ-1,
+  // 2 = columns 2, 3 (NQ = 2), 1 = anything else (per-feature selects)
+  bool first_cols = true, last_cols = NQ == 2;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    first_cols = first_cols && comp[q] == q;
+    last_cols = last_cols && comp[q] == 2 + q;
+  }
+  const int lay = first_cols ? 0 : (last_cols ? 2 : 1);
+  // this CTA's contiguous slice of units (U row blocks = one box each)
+  const int64_t nunits = (p.nblocks + U - 1) / U;
+  const int64_t ubeg = blockIdx.y * nunits / gridDim.y, uend = (blockIdx.y + 1) * nunits / gridDim.y;
+  const uint32_t ring_s = dev::smem_u32(ring);
+  auto issue = [&](int64_t u, int s) {
+    dev::mbar_arrive_expect_tx(full + s, kRcTmaStageBytes);
+    tma_box_2d(ring_s + (uint32_t)s * kRcTmaStageBytes, &tmx, c0, (int)(u * U * 32), dev::smem_u32(full + s));
+  };
+  int64_t u = ubeg + warp;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (u + (int64_t)s * NW < uend) issue(u + (int64_t)s * NW, s);
+  }
+  for (int k = 0; u < uend; ++k, u += NW) {
+    const int s = k % S;
+    const uint32_t ph = (uint32_t)(k / S) & 1u;
+    dev::mbar_wait(full + s, ph);
+    float x[NQ][U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const float4 v = lds_f4(ring_s + (uint32_t)s * kRcTmaStageBytes + (uint32_t)(i * 32 + lane) * 16u);
+      if (lay == 0) {            // the group's columns are the box's first NQ: no selects
+        x[0][i] = v.x;
+        x[1][i] = v.y;
+        if (NQ == 4) {
+          x[NQ - 2][i] = v.z;
+          x[NQ - 1][i] = v.w;
+        }
+      } else if (NQ == 2 && lay == 2) {    // columns 2, 3 of the box
+        x[0][i] = v.z;
+        x[NQ - 1][i] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) x[q][i] = comp[q] == 0 ? v.x : comp[q] == 1 ? v.y : comp[q] == 2 ? v.z : v.w;
+      }
+    }
+    // the stage is free once every lane holds its x (ordered before the
+    // next TMA write by each lane's proxy fence + arrive; lane 0 acquires)
+    dev::release_stage(empty + s, lane);
+    if (lane == 0 && u + (int64_t)S * NW < uend) {
+      dev::mbar_wait(empty + s, ph);
+      issue(u + (int64_t)S * NW, s);
+    }
+    // bucket, then a fixed window of 2^smax - 1 slots from the bucket's
+    // first threshold (build_rank_buckets block4 pads every table so the
+    // window stays inside it): thresholds of later buckets are > x and the
+    // pads are NaN, so the predicate "u <= x" is true on a prefix of the
+    // window and the code is the bucket start + the prefix length, found by
+    // smax power-of-two steps of one load, one compare and one select
+    uint32_t pos[NQ][U];                           // SMEM byte address of the window's next slot
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const float xc = fminf(fmaxf(x[q][i], lo[q]), hi[q]);      // NaN -> lo; replaced below
+        const float y = fminf(__fmul_rn(__fsub_rn(xc, lo[q]), sc[q]), bmax[q]);
+        const uint32_t be = dev::lds_u32(sbase[q] + 4u * __float2uint_rz(y));
+        pos[q][i] = ubase[q] + 4u * (be & 0xFFFFu);
+      }
+    switch (smax) {
+      case 0: break;
+      case 1: window_search<LE, NQ, U, 1>(pos, x); break;
+      case 2: window_search<LE, NQ, U, 2>(pos, x); break;
+      case 3: window_search<LE, NQ, U, 3>(pos, x); break;
+      case 4: window_search<LE, NQ, U, 4>(pos, x); break;
+      case 5: window_search<LE, NQ, U, 5>(pos, x); break;
+      case 6: window_search<LE, NQ, U, 6>(pos, x); break;
+      default:
+        for (uint32_t sb = 4u << (smax - 1u); sb >= 4u; sb >>= 1) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+              const float v = dev::lds_f32(pos[q][i] + sb - 4u);
+              pos[q][i] += (LE ? v < x[q][i] : v <= x[q][i]) ? sb : 0u;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const int64_t blk = u * U + i;
+      if (blk >= p.nblocks) continue;
+      // the group's words are consecutive: one base pointer, immediate offsets
+      uint32_t *dst = p.codes + ((size_t)blk * p.n_words + (size_t)(fbeg / PW)) * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < NQ; q += PW) {
+        if (!okf[q]) continue;
+        const uint32_t c0v = x[q][i] != x[q][i] ? 0xFFFFu : (pos[q][i] - ubase[q]) >> 2;
+        uint32_t w;
+        if (CW == 32) {
+          w = ((uint32_t)(fbeg + q) << 23) | c0v;
+        } else {
+          const uint32_t c1v = x[q + 1][i] != x[q + 1][i] ? 0xFFFFu : (pos[q + 1][i] - ubase[q + 1]) >> 2;
+          w = c0v | ((okf[q + 1] ? c1v : 0u) << 16);
+        }
+        dst[(q / PW) * 32] = w;
+      }
+    }
+  }
+}
+
 int sm_count(int device);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static const EncodeTiledFn fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<EncodeTiledFn>(nullptr);
+    }
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
 
 static int env_int_rc(const char *name, int dflt) {
   const char *v = std::getenv(name);
@@ -545,6 +776,50 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
                  a.ldx % 2 == 0 && (reinterpret_cast<uintptr_t>(a.X) & 7) == 0;
   const size_t tbytes = (m.rb_smem + 15) & ~size_t(15);
   p.stage_off = (uint32_t)tbytes;
+  // TMA pre-pass: X 16-B aligned with a 16-B multiple row pitch (the tensor
+  // map's requirements); otherwise the generic kernels below run the same
+  // groups
+  const char *etma = std::getenv("HB_RC_TMA");
+  if (m.rb_tma && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 && a.ldx % 4 == 0 && a.n <= INT32_MAX - 256 &&
+      !(etma && *etma && std::atoi(etma) == 0) && encode_tiled()) {
+    CUtensorMap tm;
+    const cuuint64_t dims[2] = {(cuuint64_t)m.n_features, (cuuint64_t)a.n};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.ldx * 4u};
+    const cuuint32_t box[2] = {4u, (cuuint32_t)(kRcTmaU * 32)};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult cr = encode_tiled()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(a.X), dims,
+                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(HB_E_CUDA, "cuTensorMapEncodeTiled failed for X");
+    const bool le = m.cmp == HB_CMP_LE;
+    using TmaFn = void (*)(const CUtensorMap, const RankCodeParams);
+    TmaFn fn;
+    if (m.rb_max_feats <= 2)
+      fn = m.rank_cw == 16 ? (le ? rank_code_tma_kernel<true, 16, 2> : rank_code_tma_kernel<false, 16, 2>)
+                           : (le ? rank_code_tma_kernel<true, 32, 2> : rank_code_tma_kernel<false, 32, 2>);
+    else
+      fn = m.rank_cw == 16 ? (le ? rank_code_tma_kernel<true, 16, 4> : rank_code_tma_kernel<false, 16, 4>)
+                           : (le ? rank_code_tma_kernel<true, 32, 4> : rank_code_tma_kernel<false, 32, 4>);
+    p.stage_off = (uint32_t)((tbytes + 127) & ~size_t(127));
+    const size_t smem = p.stage_off + (size_t)kRcTmaRingBytes;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(rank codes tma)");
+    // one wave: as many CTAs as fit per SM, spread over the groups
+    // (blockIdx.x = group, blockIdx.y = contiguous row slice)
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kRcTmaWarps, smem) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    const int64_t units = (nblocks + kRcTmaU - 1) / kRcTmaU;
+    const int64_t want = std::max<int64_t>(1, ((int64_t)per_sm * sm_count(m.device)) / m.rb_ngroups);   // no tail wave
+    const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(want, (units + kRcTmaWarps - 1) / kRcTmaWarps));
+    fn<<<dim3(m.rb_ngroups, gy), 32 * kRcTmaWarps, smem, a.stream>>>(tm, p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "rank_code_tma_kernel launch");
+    return HB_OK;
+  }
   // staged kernel (cp.async X staging) unless the groups span too many
   // columns for the SMEM staging budget (HB_RC_STAGED=0/1 forces; HB_RC_RB
   // picks the 32-row blocks per stage)

@@ -299,8 +299,22 @@ static void check_ptt_rank(const Ens &E, const Model &m, const std::vector<float
   const uint32_t *groups = reinterpret_cast<const uint32_t *>(rb + m.rb_groups_off);
   const uint8_t *pool = rb + m.rb_pool_off;
   const int per_word = m.rank_cw == 32 ? 1 : 2;
+  int words_seen = 0, max_feats = 0;
   for (int g = 0; g < m.rb_ngroups; ++g) {
     const uint32_t *G = groups + 8 * g;
+    REQUIRE((int)G[2] == words_seen && G[3] > G[2], "bucket groups must tile the code words");
+    words_seen = (int)G[3];
+    const int cb = (int)G[2] * per_word, ce = std::min((int)G[3] * per_word, (int)fc_feat.size());
+    max_feats = std::max(max_feats, ce - cb);
+    if (m.rb_tma) {
+      // TMA pre-pass: one 16-B box {aligned 4-column block} per row holds
+      // every x of the group, and the group's tables are SMEM-resident
+      REQUIRE((int)G[4] == fc_feat[cb], "TMA group first column");
+      for (int c = cb; c < ce; ++c)
+        REQUIRE(fc_feat[c] == fc_feat[cb] + (c - cb) && (fc_feat[c] >> 2) == (fc_feat[cb] >> 2),
+                "TMA group columns %d..%d not one aligned 4-column run", fc_feat[cb], fc_feat[ce - 1]);
+      REQUIRE(G[1] <= kRcTmaTableMax, "TMA group tables exceed the SMEM budget");
+    }
     for (int wd = (int)G[2]; wd < (int)G[3]; ++wd)
       for (int q = 0; q < per_word; ++q) {
         const int c = wd * per_word + q;
@@ -325,9 +339,26 @@ static void check_ptt_rank(const Ens &E, const Model &m, const std::vector<float
           for (uint32_t j = 0; j < cnt; ++j) got += E.cmp == 0 ? (uu[base + j] <= x) : (uu[base + j] < x);
           REQUIRE(got == code(fc_feat[c], x), "bucket code feature %d x %g: %u vs %u", fc_feat[c], x, got,
                   code(fc_feat[c], x));
+          if (m.rb_tma) {
+            // the TMA kernel's fixed window: S_g power-of-two steps from the
+            // bucket start over 2^S_g - 1 slots, which must stay inside the
+            // group's tables (NaN pads, later buckets compare false)
+            uint32_t sg = 0;
+            for (int c2 = cb; c2 < ce; ++c2) sg = std::max(sg, feat[8 * c2 + 2]);
+            REQUIRE(fm[7] + 4 * ((size_t)base + (1u << sg) - 1) <= G[1], "TMA window past the group tables");
+            uint32_t pos = base;
+            for (int k = (int)sg - 1; k >= 0; --k) {
+              const float v = uu[pos + (1u << k) - 1];
+              if (E.cmp == 0 ? v <= x : v < x) pos += 1u << k;
+            }
+            REQUIRE(pos == code(fc_feat[c], x), "TMA window code feature %d x %g: %u vs %u", fc_feat[c], x, pos,
+                    code(fc_feat[c], x));
+          }
         }
       }
   }
+  REQUIRE(words_seen == m.rank_nwords, "bucket groups cover %d of %d words", words_seen, m.rank_nwords);
+  REQUIRE(m.rb_max_feats == max_feats, "rb_max_feats %d vs %d", m.rb_max_feats, max_feats);
 }
 
 static void check_tt_wide(const Ens &E, const Model &m, const std::vector<float> &X, int n) {
@@ -436,19 +467,20 @@ int main(int argc, char **argv) {
   const long iters = argc > 1 ? std::atol(argv[1]) : 200;
   rng.seed(argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 1);
   long compiled = 0, rejected = 0, checked_rows = 0;
-  long n_fp32 = 0, n_rank = 0, n_pre = 0, n_ttw = 0, n_gemm = 0, n_cw16 = 0;
+  long n_fp32 = 0, n_rank = 0, n_pre = 0, n_ttw = 0, n_gemm = 0, n_cw16 = 0, n_tma = 0;
   const int strategies[4] = {HB_STRATEGY_AUTO, HB_STRATEGY_PTT, HB_STRATEGY_TT, HB_STRATEGY_GEMM};
   for (long it = 0; it < iters; ++it) {
     // layout choices the compile reads from the environment: cover every
     // PTT layout (fp32 nodes; rank codes in the scorer or from the pre-pass,
-    // 32- or 16-bit cells) and TT (narrow / wide rows, tree chunks)
+    // 32- or 16-bit cells; TMA or generic pre-pass groups) and TT (narrow / wide rows, tree chunks)
     static const char *rank[] = {"-1", "0", "1"}, *pre[] = {"-1", "0", "1"}, *cw[] = {"0", "32", "16"},
-                      *wide[] = {"-1", "1"}, *chunk[] = {"-1", "0", "4"};
+                      *wide[] = {"-1", "1"}, *chunk[] = {"-1", "0", "4"}, *rctma[] = {"0", "1"};
     setenv("HB_PTT_RANK", rank[rnd(3)], 1);
     setenv("HB_RANK_PRE", pre[rnd(3)], 1);
     setenv("HB_RANK_CW", cw[rnd(3)], 1);
     setenv("HB_TT_WIDE", wide[rnd(2)], 1);
     setenv("HB_TT_CHUNK", chunk[rnd(3)], 1);
+    setenv("HB_RC_TMA", rctma[rnd(2)], 1);
     Ens E = random_ensemble();
     hb_ensemble v = E.view();
     REQUIRE(hb_validate(&v) == HB_OK, "valid ensemble rejected (iteration %ld)", it);
@@ -463,7 +495,7 @@ int main(int argc, char **argv) {
       if (st != HB_OK) continue;
       ++compiled;
       if (m->strategy == HB_STRATEGY_PTT && !m->ptt_rank) check_ptt_fp32(E, *m, X, n), ++n_fp32;
-      if (m->strategy == HB_STRATEGY_PTT && m->ptt_rank) check_ptt_rank(E, *m, X, n, t0, t1), ++n_rank, n_pre += m->rank_pre, n_cw16 += m->rank_cw == 16;
+      if (m->strategy == HB_STRATEGY_PTT && m->ptt_rank) check_ptt_rank(E, *m, X, n, t0, t1), ++n_rank, n_pre += m->rank_pre, n_cw16 += m->rank_cw == 16, n_tma += m->rb_tma;
       if (m->strategy == HB_STRATEGY_TT && m->d_ttw) check_tt_wide(E, *m, X, n), ++n_ttw;
       if (m->strategy == HB_STRATEGY_GEMM && !m->gemm_tc) check_gemm(E, *m, X, n), ++n_gemm;
       checked_rows += n;
@@ -483,8 +515,9 @@ int main(int argc, char **argv) {
     ++rejected;
   }
   std::printf("fuzz_layout: %ld iterations, %ld models compiled and interpreted (%ld row checks: "
-              "PTT fp32 %ld, PTT rank %ld (pre-pass tables %ld, 16-bit cells %ld), wide TT %ld, GEMM %ld), "
-              "%ld corruptions rejected, %d failures\n", iters, compiled, checked_rows, n_fp32, n_rank, n_pre, n_cw16,
+              "PTT fp32 %ld, PTT rank %ld (pre-pass tables %ld of them TMA groups %ld, 16-bit cells %ld), wide TT %ld, "
+              "GEMM %ld), %ld corruptions rejected, %d failures\n", iters, compiled, checked_rows, n_fp32, n_rank, n_pre,
+              n_tma, n_cw16,
               n_ttw, n_gemm, rejected, failures);
   return failures ? 1 : 0;
 }

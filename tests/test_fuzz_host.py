@@ -5,6 +5,7 @@ mode, compiles random valid ensembles under every strategy and layout option,
 interprets every built layout against a plain tree walk, and checks that
 corrupted ensembles are rejected — any sanitizer report fails the run."""
 import os
+import re
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -29,3 +30,6 @@ def test_fuzz_layout_asan_ubsan(tmp_path):
         r = subprocess.run([exe, "800", str(seed)], capture_output=True, text=True, env=env, timeout=600)
         assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
         assert "0 failures" in r.stdout, r.stdout
+        # the TMA pre-pass grouping (rank_code_tma_kernel) was built and interpreted
+        m = re.search(r"TMA groups (\d+)", r.stdout)
+        assert m and int(m.group(1)) > 0, r.stdout

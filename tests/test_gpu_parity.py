@@ -976,6 +976,50 @@ def test_rank_prepass_staged_spans(cw, rb, order, monkeypatch):
             check_all(e, m, Xd, Xh)
 
 
+@pytest.mark.parametrize("cw", ["32", "16"])
+@pytest.mark.parametrize("cmp", [0, 1])
+def test_rank_prepass_tma(cmp, cw, monkeypatch):
+    """TMA pre-pass (rank_code_tma_kernel: tables of one aligned 4-column
+    block per CTA, X pieces {4 columns x 64 rows} copied by the tensor-map TMA
+    into per-warp rings): groups of 1-4 features from used columns with gaps
+    (32-bit cells) or a partial last block (16-bit cells), row counts below
+    one box, at a box edge, inside a 32-row block, several row slices per
+    group, padded row pitches (ldx % 4 == 0), NaN / +-Inf / +-0 cells; then
+    the pitches the tensor map cannot take (ldx % 4 != 0, X 4 B off 16-B
+    alignment), which run the generic kernels on the same groups; leaf ids
+    bit-exact, scores within tolerance, and identical leaf ids to a model
+    compiled for the generic kernels."""
+    _set_layout(monkeypatch, "pre" + cw)
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")
+    F = 64
+    if cw == "32":
+        used = np.sort(np.random.default_rng(51).choice(F, 41, replace=False))
+    else:
+        used = np.arange(F - 2)       # 31 code words, the last block half used
+    e = synth.gen_forest(150, 8, F, seed=52 + cmp, family="balanced", features=used, cmp=cmp,
+                         post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["rank_prepass"] == 1 and m.info["code_cell_bits"] == int(cw)
+    assert m.info["rank_prepass_tma"] == 1
+    for n, ldx in ((1, 64), (63, 64), (64, 64), (65, 68), (64 * 16 * 3 + 17, 64), (50_000, 72)):
+        Xd, Xh = X_pair(70 + n, n, F, ldx=ldx, special_q24=SPECIAL_Q24)
+        check_all(e, m, Xd, Xh, kinds=("predict", "proba", "raw", "leaf_hash"))
+    Xd, Xh = X_pair(9, 5000, F, ldx=F + 1, special_q24=SPECIAL_Q24)
+    check_all(e, m, Xd, Xh, kinds=("raw", "leaf_hash"))
+    Xd, Xh = X_pair(10, 5000, F, special_q24=SPECIAL_Q24)
+    flat = torch.zeros(5000 * F + 1, dtype=torch.float32, device="cuda")
+    Xm = flat[1:].view(5000, F)
+    Xm.copy_(Xd)
+    assert Xm.data_ptr() % 16 == 4
+    check_all(e, m, Xm, Xh, kinds=("raw", "leaf_hash"))
+    monkeypatch.setenv("HB_RC_TMA", "0")
+    m2 = hb.Model(e, strategy="ptt", device=0)
+    assert m2.info["rank_prepass"] == 1 and m2.info["rank_prepass_tma"] == 0
+    Xd, _ = X_pair(7, 200_000, F, special_q24=SPECIAL_Q24)
+    monkeypatch.delenv("HB_RC_TMA")
+    assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), m2.predict_leaf(Xd).cpu().numpy())
+
+
 @pytest.mark.parametrize("cmp", [0, 1])
 def test_rank_code_one_kernel_edges(cmp, monkeypatch):
     """The lean single-feature pre-pass kernel (rank_code_one_kernel: one
@@ -1015,6 +1059,8 @@ def test_auto_layout_per_config():
         got = (info["strategy_name"], info["code_cell_bits"], info["rank_prepass"])
         assert got == (strat, cw, pre), (name, got)
         assert info["node_record_bytes"] == 4
+        # TMA pre-pass groups where a contiguous X has a 16-B row pitch (C3: F = 28)
+        assert info["rank_prepass_tma"] == (1 if pre and e.n_features % 4 == 0 else 0), name
     _, e = synth.make_config("C5")
     shard = hb.Model(e, tree_range=(0, 1250), device=0).info
     assert shard["strategy_name"] == "tt" and shard["kernel_name"] == "tt_wide_kernel"

@@ -23,17 +23,17 @@ cases = [
     ("ptt-rank-wrap", synth.gen_forest(300, 8, 12, seed=4), {"HB_PTT_RANK": "1", "HB_CH": "8"}, "ptt"),
     ("ptt-fp32-wrap", synth.gen_forest(300, 8, 12, seed=4), {"HB_PTT_RANK": "0", "HB_CH": "8"}, "ptt"),
     ("ptt-rank-prepass-32", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32"}, "ptt"),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "32"}, "ptt"),
     ("ptt-rank-prepass-16", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16"}, "ptt"),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "16"}, "ptt"),
     ("ptt-rank-prepass-staged-16", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "1"}, "ptt"),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "16", "HB_RC_STAGED": "1"}, "ptt"),
     ("ptt-rank-prepass-staged-32-rb1", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_STAGED": "1", "HB_RC_RB": "1"}, "ptt"),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "32", "HB_RC_STAGED": "1", "HB_RC_RB": "1"}, "ptt"),
     ("ptt-rank-prepass-column", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_ONEK": "1"}, "ptt"),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "32", "HB_RC_ONEK": "1"}, "ptt"),
     ("ptt-rank-prepass-rows8", synth.gen_forest(40, 6, 12, seed=1),
-     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_STAGED": "0", "HB_RC_ROWS": "8"}, "ptt"),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "16", "HB_RC_STAGED": "0", "HB_RC_ROWS": "8"}, "ptt"),
     ("tt-wide-chunks", synth.gen_forest(24, 11, 12, seed=2, family="mixed"),
      {"HB_TT_WIDE": "1", "HB_TT_CHUNK": "8"}, "tt"),
     ("gemm-tc", synth.gen_forest(40, 3, 12, seed=3), {}, "gemm"),
@@ -43,15 +43,24 @@ cases = [
                                             post=synth.POST_SOFTMAX, task=synth.TASK_CLASSIFICATION),
      {"HB_TT_WIDE": "1"}, "tt"),
     ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
+    # TMA pre-pass (F = 12: three 4-column groups); 250K rows wrap every
+    # warp's 3-stage ring several times
+    ("ptt-rank-prepass-tma-32", synth.gen_forest(4, 4, 12, seed=7),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32", "HB_RC_TMA": "1"}, "ptt", (3000, 250_000)),
+    ("ptt-rank-prepass-tma-16", synth.gen_forest(4, 4, 12, seed=7),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_TMA": "1"}, "ptt", (3000, 250_000)),
 ]
 only = set(sys.argv[1:])   # optional case names; default: every case
-for name, e, env, strat in cases:
+for name, e, env, strat, *rows in cases:
     if only and name not in only:
         continue
     os.environ.update(env)
-    for n, small in ((3000, "0"), (40, "4096")):
+    runs = [(n, "0") for n in rows[0]] if rows else [(3000, "0"), (40, "4096")]
+    for n, small in runs:
         os.environ["HB_SMALL_BATCH"] = small
         m = hb.Model(e, strategy=strat, device=0)
+        if env.get("HB_RC_TMA") == "1":
+            assert m.info["rank_prepass_tma"] == 1, name
         X = synth.dev.gen_X_device(7, n, 12)
         for kind in ("predict", "raw", "raw64", "leaf", "leaf_hash"):
             m.run(X, kind)
