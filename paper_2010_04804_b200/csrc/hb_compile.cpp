@@ -348,50 +348,60 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     std::memcpy(&fm[6], &s, 4);
     fm[7] = (uint32_t)sbytes;                  // u offset relative to start; rebased below
   }
-  // block4 (TMA pre-pass): a group is a run of consecutive X columns inside
-  // one aligned 4-column block, so one 16-B box per row holds every x the
-  // group searches. Its kernel searches a fixed window of 2^S_g - 1 slots
-  // from the bucket's first threshold (S_g = the group's deepest search):
-  // thresholds of later buckets are > x and the pads are NaN, so every slot
-  // past the bucket compares false. Each table gets 2^S_g - 1 pad slots.
-  std::vector<int> gstart(n_words + 1, 0);         // block4: 1 where a group starts
-  if (block4) {
-    auto word_bytes = [&](int wd) {
-      size_t wb = 0;
-      for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
-      return wb;
+  // Groups of whole words (pass 1), each <= cap bytes with its pads (an
+  // oversized word is a group of its own and is searched from global
+  // memory); one word per group for the column kernel (one_per_group). With
+  // block4 (TMA pre-pass) a group is also a run of consecutive X columns
+  // inside one aligned 4-column block, so one 16-B box per row holds every x
+  // it searches.
+  // Every pre-pass kernel searches a fixed window of 2^S_g - 1 slots from the
+  // bucket's first threshold (S_g = the group's deepest search): thresholds
+  // of later buckets are > x and the pads are NaN (false against every x),
+  // so "u <= x" holds on a prefix of the window and its length completes the
+  // code. Each table therefore ends with max(1, 2^S_g - 1) NaN slots.
+  auto S_of = [&](int c) { return R.feat[(size_t)c * 8 + 2]; };
+  auto padded = [&](int c, uint32_t sg) {          // table bytes with the group's pads, 16-B rounded
+    const size_t pads = std::max<size_t>(1, ((size_t)1 << sg) - 1);
+    return (tabs[c].size() - 4 + 4 * pads + 15) & ~size_t(15);
+  };
+  std::vector<int> gstart(n_words + 1, 0);         // 1 where a group starts
+  {
+    auto group_bytes = [&](int w0, int w1, uint32_t sg) {
+      size_t b = 0;
+      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c) b += padded(c, sg);
+      return b;
     };
-    size_t gb = 0;
     int first = 0;
+    uint32_t sg = 0;
     for (int wd = 0; wd < n_words; ++wd) {
-      bool split = wd == 0;
-      if (!split) {
+      uint32_t sw = 0;
+      for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) sw = std::max(sw, S_of(wd * per_word + q));
+      bool split = wd == 0 || one_per_group;
+      if (!split && block4) {
         const int c = wd * per_word, cfirst = first * per_word;
         for (int q = 0; q < per_word && c + q < n_fc; ++q)
           if (orig[c + q] != orig[c - 1] + 1 + q || (orig[c + q] >> 2) != (orig[cfirst] >> 2)) split = true;
-        if (gb + word_bytes(wd) > cap) split = true;
       }
+      if (!split && group_bytes(first, wd + 1, std::max(sg, sw)) > cap) split = true;
       if (split) {
         gstart[wd] = 1;
         first = wd;
-        gb = 0;
+        sg = 0;
       }
-      gb += word_bytes(wd);
+      sg = std::max(sg, sw);
     }
     gstart[n_words] = 1;
     for (int w0 = 0; w0 < n_words;) {
       int w1 = w0 + 1;
       while (!gstart[w1]) ++w1;
-      uint32_t sg = 0;
-      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c) sg = std::max(sg, R.feat[(size_t)c * 8 + 2]);
-      const size_t npad = ((size_t)1 << sg) - 1;
-      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c)
-        if (npad > 1) {
-          std::vector<uint8_t> &t = tabs[c];
-          const size_t old = t.size();
-          t.resize(old + (npad - 1) * 4);
-          for (size_t i = old; i < t.size(); i += 4) std::memcpy(t.data() + i, &pad_nan, 4);
-        }
+      uint32_t sgg = 0;
+      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c) sgg = std::max(sgg, S_of(c));
+      for (int c = w0 * per_word; c < std::min(w1 * per_word, n_fc); ++c) {
+        std::vector<uint8_t> &t = tabs[c];
+        const size_t old = t.size(), want = old - 4 + 4 * std::max<size_t>(1, ((size_t)1 << sgg) - 1);
+        t.resize(want);
+        for (size_t i = old; i < want; i += 4) std::memcpy(t.data() + i, &pad_nan, 4);
+      }
       w0 = w1;
     }
   }
@@ -421,10 +431,7 @@ hb_status build_rank_buckets(const std::vector<std::vector<float>> &sorted, cons
     R.n_groups++;
   };
   for (int wd = 0; wd < n_words; ++wd) {
-    size_t wb = 0;
-    for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) wb += (tabs[wd * per_word + q].size() + 15) & ~size_t(15);
-    const bool split = block4 ? gstart[wd] != 0 : (one_per_group || gbytes + wb > cap);
-    if (gbytes > 0 && split) close(wd);
+    if (gbytes > 0 && gstart[wd]) close(wd);
     for (int q = 0; q < per_word && wd * per_word + q < n_fc; ++q) {
       const int c = wd * per_word + q;
       uint32_t *fm = R.feat.data() + (size_t)c * 8;

@@ -79,16 +79,34 @@ __device__ __forceinline__ uint32_t tab_u32(const uint8_t *tb, uint32_t off) {
   return __ldg(reinterpret_cast<const uint32_t *>(tb + off));
 }
 
-// NC rank codes in lockstep: the bucket step of every search first, then
-// S_max binary-search steps with all NC loads of a step issued back to back
-// (the searches are independent: their latencies overlap). A search whose own
-// S is smaller has cnt == 0 after S steps, and further steps are no-ops (they
-// read the pad slot u[base] and keep base), so running S_max steps is exact.
+// S power-of-two window steps (2^(S-1) slots first) over NC chains, each
+// step's NC loads back to back (see rank_codes_lockstep)
+template <bool LE, bool SM, int NC, int S>
+__device__ __forceinline__ void window_steps(const uint8_t *tb, uint32_t (&pos)[NC], const float (&x)[NC]) {
+  if constexpr (S > 0) {
+    constexpr uint32_t k = S - 1;
+    float v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = __uint_as_float(tab_u32<SM>(tb, pos[c] + 4u * ((1u << k) - 1u)));
+#pragma unroll
+    for (int c = 0; c < NC; ++c) pos[c] += (LE ? v[c] < x[c] : v[c] <= x[c]) ? (4u << k) : 0u;
+    window_steps<LE, SM, NC, S - 1>(tb, pos, x);
+  }
+}
+
+// NC rank codes in lockstep: the bucket step of every search first, then a
+// fixed window of 2^smax - 1 slots from each bucket's first threshold.
+// Thresholds of later buckets are > x and every table ends with 2^S_g - 1
+// NaN pads (build_rank_buckets; S_g >= smax for any set of one group's
+// features), so "u <= x" (LE: u < x) holds on a prefix of the window and the
+// code is the bucket start + the prefix length, found by smax power-of-two
+// steps of one load, one compare and one select — all NC loads of a step
+// back to back (the searches are independent: their latencies overlap).
 template <bool LE, bool SM, int NC>
 __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const uint4 *m0, const uint4 *m1,
                                                     const int (&mi)[NC], uint32_t smax, const uint8_t *tb,
                                                     uint32_t (&code)[NC]) {
-  uint32_t base[NC], cnt[NC], uo[NC];
+  uint32_t pos[NC], uo[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const uint4 a = m0[mi[c]], b = m1[mi[c]];
@@ -98,24 +116,27 @@ __device__ __forceinline__ void rank_codes_lockstep(const float (&x)[NC], const 
     y = fminf(y, (float)(a.y - 1u));
     const uint32_t bk = __float2uint_rz(y);
     const uint32_t be = tab_u32<SM>(tb, a.w + 4u * bk);   // first index | count << 16
-    base[c] = be & 0xFFFFu;
-    cnt[c] = be >> 16;
     uo[c] = b.w;
+    pos[c] = b.w + 4u * (be & 0xFFFFu);
   }
-  for (uint32_t k = 0; k < smax; ++k) {
+  switch (smax) {
+    case 0: break;
+    case 1: window_steps<LE, SM, NC, 1>(tb, pos, x); break;
+    case 2: window_steps<LE, SM, NC, 2>(tb, pos, x); break;
+    case 3: window_steps<LE, SM, NC, 3>(tb, pos, x); break;
+    case 4: window_steps<LE, SM, NC, 4>(tb, pos, x); break;
+    case 5: window_steps<LE, SM, NC, 5>(tb, pos, x); break;
+    default:
+      for (uint32_t sb = 4u << (smax - 1u); sb >= 4u; sb >>= 1) {
+        float v[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const uint32_t half = cnt[c] >> 1;
-      const float v = __uint_as_float(tab_u32<SM>(tb, uo[c] + 4u * (base[c] + half)));
-      // branch-free (the load is unconditional: u has a pad slot), so the
-      // NC chains of one step overlap instead of each waiting on its load
-      const uint32_t go = (uint32_t)(LE ? v < x[c] : v <= x[c]) & (uint32_t)(cnt[c] != 0);
-      base[c] += go * (half + 1u);
-      cnt[c] = go ? cnt[c] - half - 1u : half;
-    }
+        for (int c = 0; c < NC; ++c) v[c] = __uint_as_float(tab_u32<SM>(tb, pos[c] + sb - 4u));
+#pragma unroll
+        for (int c = 0; c < NC; ++c) pos[c] += (LE ? v[c] < x[c] : v[c] <= x[c]) ? sb : 0u;
+      }
   }
 #pragma unroll
-  for (int c = 0; c < NC; ++c) code[c] = x[c] != x[c] ? 0xFFFFu : base[c];
+  for (int c = 0; c < NC; ++c) code[c] = x[c] != x[c] ? 0xFFFFu : (pos[c] - uo[c]) >> 2;
 }
 
 template <bool LE, int CW, bool SM, int ROWS>
@@ -396,6 +417,34 @@ RcFn staged_pick(bool le, int cw, int rb, bool one) {
 
 }  // namespace
 
+// fixed-window search helpers over 32-bit shared addresses (column and TMA
+// kernels; rank_codes_lockstep explains the window)
+template <int OFF>
+__device__ __forceinline__ float lds_f32_off(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+
+// S power-of-two steps (2^(S-1) slots first) over every chain, each step's
+// loads back to back, the slot offsets immediates
+template <bool LE, int NQ, int U, int S>
+__device__ __forceinline__ void window_search(uint32_t (&pos)[NQ][U], const float (&x)[NQ][U]) {
+  if constexpr (S > 0) {
+    constexpr int k = S - 1;
+    float v[NQ][U];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < U; ++i) v[q][i] = lds_f32_off<4 * ((1 << k) - 1)>(pos[q][i]);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int i = 0; i < U; ++i) pos[q][i] += (LE ? v[q][i] < x[q][i] : v[q][i] <= x[q][i]) ? (4u << k) : 0u;
+    window_search<LE, NQ, U, S - 1>(pos, x);
+  }
+}
+
 // Single-feature table groups with 32-bit cells (C3, C4: one ~34-40 KB table
 // per feature, one feature per CTA): a lean column kernel. The CTA owns one
 // feature for a contiguous slice of 32-row blocks (group-major grid: the CTAs
@@ -478,7 +527,8 @@ __global__ void __launch_bounds__(32 * NWARP, NWARP == 8 ? 4 : 2) rank_code_one_
 #pragma unroll
       for (int i = 0; i < kOneU; ++i) x[q][i] = xn[q][i];
     if (u + NWARP < uend) load(u + NWARP, xn);   // next unit's loads in flight
-    uint32_t base[PW][kOneU], cnt[PW][kOneU];
+    // bucket, then the fixed window (rank_codes_lockstep)
+    uint32_t pos[PW][kOneU];
 #pragma unroll
     for (int q = 0; q < PW; ++q)
 #pragma unroll
@@ -486,24 +536,31 @@ __global__ void __launch_bounds__(32 * NWARP, NWARP == 8 ? 4 : 2) rank_code_one_
         const float xc = fminf(fmaxf(x[q][i], lo[q]), hi[q]);      // NaN -> lo; replaced below
         const float y = fminf(__fmul_rn(__fsub_rn(xc, lo[q]), sc[q]), bmax[q]);
         const uint32_t be = dev::lds_u32(sbase[q] + 4u * __float2uint_rz(y));
-        base[q][i] = be & 0xFFFFu;
-        cnt[q][i] = be >> 16;
+        pos[q][i] = ubase[q] + 4u * (be & 0xFFFFu);
       }
-    // binary search inside the bucket, S_max lockstep steps with
-    // unconditional loads (a predicated variant that skips finished searches
-    // diverged and measured slower: C3 pre-pass 1.39 -> 1.97 ms)
-    for (uint32_t k = 0; k < smax; ++k) {
+    switch (smax) {
+      case 0: break;
+      case 1: window_search<LE, PW, kOneU, 1>(pos, x); break;
+      case 2: window_search<LE, PW, kOneU, 2>(pos, x); break;
+      case 3: window_search<LE, PW, kOneU, 3>(pos, x); break;
+      case 4: window_search<LE, PW, kOneU, 4>(pos, x); break;
+      case 5: window_search<LE, PW, kOneU, 5>(pos, x); break;
+      default:
+        for (uint32_t sb = 4u << (smax - 1u); sb >= 4u; sb >>= 1) {
 #pragma unroll
-      for (int q = 0; q < PW; ++q)
+          for (int q = 0; q < PW; ++q)
 #pragma unroll
-        for (int i = 0; i < kOneU; ++i) {
-          const uint32_t half = cnt[q][i] >> 1;
-          const float v = dev::lds_f32(ubase[q] + 4u * (base[q][i] + half));
-          const bool go = (LE ? v < x[q][i] : v <= x[q][i]) && cnt[q][i] != 0u;
-          base[q][i] += go ? half + 1u : 0u;
-          cnt[q][i] = go ? cnt[q][i] - half - 1u : half;
+            for (int i = 0; i < kOneU; ++i) {
+              const float v = dev::lds_f32(pos[q][i] + sb - 4u);
+              pos[q][i] += (LE ? v < x[q][i] : v <= x[q][i]) ? sb : 0u;
+            }
         }
     }
+    uint32_t base[PW][kOneU];
+#pragma unroll
+    for (int q = 0; q < PW; ++q)
+#pragma unroll
+      for (int i = 0; i < kOneU; ++i) base[q][i] = (pos[q][i] - ubase[q]) >> 2;
     uint32_t *dst = p.codes + ((size_t)u * kOneU * p.n_words + (size_t)wd) * 32 + lane;
 #pragma unroll
     for (int i = 0; i < kOneU; ++i) {
@@ -545,32 +602,6 @@ __device__ __forceinline__ float4 lds_f4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
-}
-
-template <int OFF>
-__device__ __forceinline__ float lds_f32_off(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
-  return v;
-}
-
-// S power-of-two steps (2^(S-1) slots first) over every chain, each step's
-// loads back to back, the slot offsets immediates
-template <bool LE, int NQ, int U, int S>
-__device__ __forceinline__ void window_search(uint32_t (&pos)[NQ][U], const float (&x)[NQ][U]) {
-  if constexpr (S > 0) {
-    constexpr int k = S - 1;
-    float v[NQ][U];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-#pragma unroll
-      for (int i = 0; i < U; ++i) v[q][i] = lds_f32_off<4 * ((1 << k) - 1)>(pos[q][i]);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-#pragma unroll
-      for (int i = 0; i < U; ++i) pos[q][i] += (LE ? v[q][i] < x[q][i] : v[q][i] <= x[q][i]) ? (4u << k) : 0u;
-    window_search<LE, NQ, U, S - 1>(pos, x);
-  }
 }
 
 template <bool LE, int CW, int NQ>

@@ -339,10 +339,10 @@ static void check_ptt_rank(const Ens &E, const Model &m, const std::vector<float
           for (uint32_t j = 0; j < cnt; ++j) got += E.cmp == 0 ? (uu[base + j] <= x) : (uu[base + j] < x);
           REQUIRE(got == code(fc_feat[c], x), "bucket code feature %d x %g: %u vs %u", fc_feat[c], x, got,
                   code(fc_feat[c], x));
-          if (m.rb_tma) {
-            // the TMA kernel's fixed window: S_g power-of-two steps from the
-            // bucket start over 2^S_g - 1 slots, which must stay inside the
-            // group's tables (NaN pads, later buckets compare false)
+          {
+            // the pre-pass kernels' fixed window: S_g power-of-two steps from
+            // the bucket start over 2^S_g - 1 slots, which must stay inside
+            // the group's tables (NaN pads, later buckets compare false)
             uint32_t sg = 0;
             for (int c2 = cb; c2 < ce; ++c2) sg = std::max(sg, feat[8 * c2 + 2]);
             REQUIRE(fm[7] + 4 * ((size_t)base + (1u << sg) - 1) <= G[1], "TMA window past the group tables");

@@ -1020,6 +1020,42 @@ def test_rank_prepass_tma(cmp, cw, monkeypatch):
     assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), m2.predict_leaf(Xd).cpu().numpy())
 
 
+@pytest.mark.parametrize("kern", ["tma", "direct", "staged", "column"])
+@pytest.mark.parametrize("cw", ["32", "16"])
+def test_rank_prepass_deep_bucket(kern, cw, monkeypatch):
+    """Fixed-window search at depth: one feature's thresholds are 3000 values
+    packed into [1, 1.001] plus an outlier at 1e6, so the linear bucket map
+    puts ~all of them into one bucket (S = 12 window steps, the kernels'
+    runtime-step path, 4095 NaN pad slots); X hits the cluster, its fp32
+    neighbours, the outlier, NaN and +-Inf. Every pre-pass kernel must give
+    the oracle's leaf ids."""
+    if kern == "column" and cw == "16":
+        pytest.skip("the column kernel runs 32-bit cells only")
+    _set_layout(monkeypatch, "pre" + cw)
+    monkeypatch.setenv("HB_SMALL_BATCH", "0")
+    monkeypatch.setenv("HB_RC_TMA", "1" if kern == "tma" else "0")
+    monkeypatch.setenv("HB_RC_STAGED", "1" if kern == "staged" else "0")
+    monkeypatch.setenv("HB_RC_ONEK", "1" if kern == "column" else "0")
+    rng = np.random.default_rng(61)
+    F = 8
+    e = synth.gen_forest(300, 8, F, seed=62, family="balanced",
+                         post=synth.POST_SIGMOID, task=synth.TASK_CLASSIFICATION)
+    f32 = np.float32
+    internal = np.nonzero(e.left != -1)[0]
+    on0 = internal[e.feature[internal] == 0]
+    pool = np.concatenate([np.linspace(1.0, 1.001, 3000, dtype=f32), np.array([1e6], f32)])
+    e.threshold[on0] = pool[rng.integers(0, pool.size, on0.size)]
+    e.threshold[on0[:1]] = f32(1e6)
+    n = 20_000
+    Xh = synth.gen_X(63, n, F)
+    cand = np.concatenate([pool, np.nextafter(pool, f32(np.inf)), np.nextafter(pool, f32(-np.inf)),
+                           np.array([np.nan, np.inf, -np.inf, 0.0, 2e6], f32)])
+    Xh[:, 0] = cand[rng.integers(0, cand.size, n)]
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["rank_prepass"] == 1 and m.info["rank_prepass_tma"] == (1 if kern == "tma" else 0)
+    check_all(e, m, torch.from_numpy(Xh).cuda(), Xh, kinds=("raw", "leaf", "leaf_hash"))
+
+
 @pytest.mark.parametrize("cmp", [0, 1])
 def test_rank_code_one_kernel_edges(cmp, monkeypatch):
     """The lean single-feature pre-pass kernel (rank_code_one_kernel: one
