@@ -162,7 +162,8 @@ typedef struct {
   int64_t device_bytes;         /* device memory owned by the model            */
   int64_t tree_stride_bytes;    /* bytes per tree in the compiled layout       */
   int32_t tensor_cores;         /* 1 if the scorer runs tcgen05 MMAs (GEMM)    */
-  int32_t node_record_bytes;    /* PTT/TT node record size (4 = rank-coded PTT) */
+  int32_t node_record_bytes;    /* node record size: 4 rank-coded PTT, 8 fp32 PTT / narrow TT,
+                                   16 wide-row TT, 0 GEMM */
   int32_t kernel;               /* row-tile scorer: 0 ptt, 1 ptt rank-coded, 2 tt, 3 tt wide-row,
                                    4 gemm tcgen05, 5 gemm CUDA-core (6, 7: removed
                                    experimental TT kernels, never reported)

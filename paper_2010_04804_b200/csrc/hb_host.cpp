@@ -1085,7 +1085,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->device_bytes = (int64_t)m.device_bytes;
   info->tree_stride_bytes = (int64_t)m.stride;
   info->tensor_cores = m.gemm_tc;
-  info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : (m.ptt_rank ? 4 : 8);
+  info->node_record_bytes = m.strategy == HB_STRATEGY_GEMM ? 0 : m.ptt_rank ? 4 : m.cfg.wide_rows ? 16 : 8;
   if (m.strategy == HB_STRATEGY_PTT) info->kernel = m.ptt_rank ? 1 : 0;
   else if (m.strategy == HB_STRATEGY_TT)
     info->kernel = m.cfg.wide_rows ? 3 : 2;

@@ -187,8 +187,9 @@ __global__ void __launch_bounds__(32 * 17, 1) tt_kernel(const TtParams p) {
 // warp, and all warps of the CTA walk disjoint trees of the same R rows. Node
 // records (16 B per internal node with both children's payloads, hb_host.cpp
 // build_ttw: a walk to a leaf at depth D_k is D_k dependent loads, the last
-// one carrying the leaf value) come through L1/L2 (__ldg): the top levels of a
-// tree are shared by the R rows and hit L1. Each lane walks G trees at once
+// one carrying the leaf value) come through L1/L2 (__ldg): the R rows of a
+// tree slot share their top-level requests (one sector for the root, <= 2^l
+// at level l). Each lane walks G trees at once
 // (memory-level parallelism); finished walks issue no loads and the group ends
 // once every walk of the warp reached a leaf (the fixed TREE_DEPTH loop of
 // Alg. 2 with its leaf self-loops, cut short). Per-row sums are
