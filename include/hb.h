@@ -48,9 +48,10 @@
 extern "C" {
 #endif
 
-#define HB_ABI_VERSION 5   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended;
+#define HB_ABI_VERSION 6   /* 2: hb_model_info.tt_sector; 3: tt_chunk_trees appended;
                               4: HB_OUT_RAW64 + hb_finalize64 (fp64 raw sums);
-                              5: hb_model_info.rank_prepass_tma appended */
+                              5: hb_model_info.rank_prepass_tma appended;
+                              6: hb_model_info.rows_per_lane (was reserved0) */
 
 typedef enum {
   HB_OK = 0,
@@ -185,7 +186,9 @@ typedef struct {
                                    columns per row); it runs on calls whose X is 16-B
                                    aligned with ldx % 4 == 0, the generic pre-pass
                                    kernels on the others (ABI 5)                       */
-  int32_t reserved0;            /* 0 */
+  int32_t rows_per_lane;        /* rank-coded PTT scorer: rows each lane walks (2: the top
+                                   three tree levels are loaded once for a lane's two rows;
+                                   pre-pass codes, D >= 3); 1 otherwise (ABI 6)          */
 } hb_model_info;
 
 /* Host-only validation of an ensemble (no CUDA calls): the tree structure

@@ -534,9 +534,10 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   const int force_pre = env_int2("HB_RANK_PRE", -1);
   // pre: codes come from the pre-pass (hb_rank_codes.cu), the ring carries
   // tree chunks only; otherwise the ring also carries the Eytzinger arrays
-  auto try_cfg = [&](int cw, bool pre, LaunchCfg &cfg) {
+  // rpl: rows per lane (2: each warp holds two 32-row code blocks, pre-pass only)
+  auto try_cfg = [&](int cw, bool pre, LaunchCfg &cfg, int rpl = 1) {
     if (cw == 32 && A.n_fc > 511) return false;
-    const long tile = cw == 32 ? (long)A.n_fc * 128 : (long)((A.n_fc + 1) / 2) * 128;
+    const long tile = (cw == 32 ? (long)A.n_fc * 128 : (long)((A.n_fc + 1) / 2) * 128) * rpl;
     for (int nw : {24, 16, 12, 8, 4}) {
       if (force_nw && nw != force_nw) continue;
       const long xb = (long)nw * tile;
@@ -618,6 +619,21 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     ok = pick_cw(true, cfg, cw);
   }
   if (!ok) return HB_E_UNSUPPORTED;
+  // two rows per lane (pttr_kernel<RPL = 2>): the top three levels are
+  // shared by a lane's two rows; pre-pass codes and D >= 3 only. AUTO for
+  // scalar-output models (C3 835.7M -> 885.0M rows/s, C2 581.4M -> 596.6M);
+  // with 7 per-class accumulators per row (C4) the two rows' fp64 sums spill
+  // (107.3M -> 63.6M), so K > 1 keeps one row per lane. HB_PTTR_RPL: 1 / 2
+  // forces
+  int rpl = 1;
+  const int want_rpl = env_int2("HB_PTTR_RPL", 0);
+  if (pre && D >= 3 && (want_rpl == 2 || (want_rpl == 0 && m->nacc == 1))) {
+    LaunchCfg c2;
+    if (try_cfg(cw, true, c2, 2)) {
+      cfg = c2;
+      rpl = 2;
+    }
+  }
   // tree records: node = (cell offset) << 16 | k
   auto cell_off = [&](int fc) -> uint32_t {
     return cw == 32 ? (uint32_t)fc * 128u : (uint32_t)(fc >> 1) * 128u + (uint32_t)(fc & 1) * 2u;
@@ -765,6 +781,7 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
   m->ptt_rank = 1;
   m->n_trees_pad = Tpad;
   m->rank_cw = cw;
+  m->rank_rpl = rpl;
   return HB_OK;
 }
 

@@ -1091,7 +1091,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
     info->kernel = m.cfg.wide_rows ? 3 : 2;
   else info->kernel = m.gemm_tc ? 4 : 5;
   info->rows_per_cta = m.strategy == HB_STRATEGY_GEMM ? (m.gemm_tc ? 128 : 128)
-                       : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw);
+                       : (m.cfg.wide_rows ? m.cfg.wide_rows : 32 * m.cfg.nw * (m.ptt_rank ? m.rank_rpl : 1));
   info->code_cell_bits = m.ptt_rank ? m.rank_cw : 0;
   info->rank_prepass = m.rank_pre;
   info->tt_sector = 0;   // sector-paired TT records were removed
@@ -1100,7 +1100,7 @@ hb_status hb_model_get_info(const hb_model *hm, hb_model_info *info) {
   info->tt_walks_per_lane = m.cfg.wide_rows ? m.tt_g : 0;
   info->tt_record_bytes = (int64_t)m.ttw_rec_bytes;
   info->rank_prepass_tma = m.rank_pre ? m.rb_tma : 0;
-  info->reserved0 = 0;
+  info->rows_per_lane = m.strategy == HB_STRATEGY_PTT && m.ptt_rank ? m.rank_rpl : 1;
   return HB_OK;
 }
 

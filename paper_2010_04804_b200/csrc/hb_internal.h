@@ -61,6 +61,7 @@ struct Model {
   // PTT with rank-coded thresholds (hb_pttr.cu)
   int ptt_rank = 0;
   int rank_cw = 32;          // code cell width (32 or 16 bits)
+  int rank_rpl = 1;          // rows per lane of pttr_kernel (2: top levels shared by two rows)
   void *d_aux = nullptr;    // [fmeta | groups | eytzinger pool]
   size_t aux_groups_off = 0, aux_pool_off = 0;
   int rank_nfc = 0, rank_ngroups = 0;

@@ -47,8 +47,9 @@ namespace hb {
 int sm_count(int device);
 
 hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
-  PttrFn fn = m.rank_cw == 16 ? pttr_fn16(m.depth, m.cmp == HB_CMP_LE, m.nacc)
-                              : pttr_fn32(m.depth, m.cmp == HB_CMP_LE, m.nacc);
+  const bool le = m.cmp == HB_CMP_LE;
+  PttrFn fn = m.rank_rpl == 2 ? (m.rank_cw == 16 ? pttr_fn16_rpl2(m.depth, le, m.nacc) : pttr_fn32_rpl2(m.depth, le, m.nacc))
+                              : (m.rank_cw == 16 ? pttr_fn16(m.depth, le, m.nacc) : pttr_fn32(m.depth, le, m.nacc));
   if (!fn) return fail(HB_E_UNSUPPORTED, "PTT depth out of range");
   PttrParams p;
   // pre-pass: rank codes of every (row, used feature) into stream-ordered
@@ -100,7 +101,7 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   p.ns = m.cfg.ns;
   p.ch = m.cfg.ch;
   p.stage_bytes = (uint32_t)m.cfg.stage_bytes;
-  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
+  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32 * m.rank_rpl;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) {
     if (codes) cudaFreeAsync(codes, a.stream);

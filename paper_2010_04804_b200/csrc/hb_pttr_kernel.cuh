@@ -47,13 +47,22 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
 // share lane l's 32-bit word (bank l) of row m; node = off16 << 16 | k with
 // off16 = (fc>>1)*128 + (fc&1)*2, left <=> (node & 0xFFFF) >= c(x): half the
 // tile, one more instruction per level.
-template <int D, bool LE, int NACC, int G, int CW>
+//
+// RPL = rows per lane. RPL = 2 (codes from the pre-pass only, D >= 3): a warp
+// owns 64 rows, lane l rows l and l + 32 (two consecutive 32-row code blocks
+// in SMEM). The top three levels are shared by the two rows: the root with
+// one LDS, nodes 2-3 with one LDS.64 and nodes 4-7 with one LDS.128, all
+// broadcasts (one wavefront each), then selected per row; below level 2 each
+// row walks on its own. The kernel is bound by SMEM wavefronts (~20.3 per
+// warp-tree at one row per lane, three of them for levels 0-2), so sharing
+// the top levels saves ~3 of ~40.6 wavefronts per 64 rows and tree.
+template <int D, bool LE, int NACC, int G, int CW, int RPL = 1>
 __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = p.nw, ns = p.ns, ch = p.ch;
   const uint32_t tile_bytes = CW == 32 ? (uint32_t)p.n_fc * 128u : (uint32_t)((p.n_fc + 1) / 2) * 128u;
-  const size_t xbytes = (size_t)nw * tile_bytes;
+  const size_t xbytes = (size_t)nw * tile_bytes * RPL;
   uint8_t *stages = smem + xbytes;
   uint64_t *full = reinterpret_cast<uint64_t *>(stages + (size_t)ns * p.stage_bytes);
   uint64_t *empty = full + ns;
@@ -81,12 +90,12 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
           // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
           // (of code words, which are contiguous per tile, with the pre-pass)
           const long tile_i = it / items;
-          const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32);
+          const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32 * RPL);
           if (p.codes) {
             const int64_t nb = (p.n + 31) / 32, b0 = next / 32;
             if (b0 < nb)
               dev::prefetch_rows_l2(reinterpret_cast<const float *>(p.codes), b0,
-                                    min((int64_t)nw, nb - b0), nb, (int64_t)p.n_words * 32);
+                                    min((int64_t)nw * RPL, nb - b0), nb, (int64_t)p.n_words * 32);
           } else {
             dev::prefetch_rows_l2(p.X, next, (int64_t)nw * 32, p.n, p.ldx);
           }
@@ -104,6 +113,184 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
         }
         dev::mbar_arrive_expect_tx(&full[s], bytes);
         dev::bulk_g2s(stages + (size_t)s * p.stage_bytes, src, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  if constexpr (RPL == 2) {
+    static_assert(D >= 3, "RPL = 2 shares levels 0-2");
+    // pre-pass codes only (host: rank_pre, no feature groups in the ring)
+    const uint32_t codesA = dev::smem_u32(smem) + (uint32_t)warp * 2u * tile_bytes + 4u * lane;
+    const uint32_t codesB = codesA + tile_bytes;
+    const uint32_t stage0 = dev::smem_u32(stages);
+    const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
+    // go left <=> k >= c(x) (node and 32-bit cell share the high half; 16-bit
+    // cells compare the low half)
+    auto left_of = [&](uint32_t nd, uint32_t cbase) -> bool {
+      if (CW == 32) return nd >= dev::lds_u32(cbase + (nd >> 16));
+      return (nd & 0xFFFFu) >= lds_u16(cbase + (nd >> 16));
+    };
+    dev::Ring ring(ns);
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      const int64_t wrow0 = (int64_t)tile * (nw * 64) + warp * 64;
+      const int64_t rowA = wrow0 + lane, rowB = rowA + 32;
+      const bool active = wrow0 < p.n;
+      __syncwarp();   // previous tile's cell reads done before the fill (WAR)
+      if (active) {
+        const int nblk = wrow0 + 32 < p.n ? 2 : 1;
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.codes + (size_t)(wrow0 >> 5) * p.n_words * 32);
+        const uint32_t dst = codesA - 4u * lane;
+        for (int i = lane; i < nblk * p.n_words * 8; i += 32) {
+          const uint4 v = __ldg(src + i);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * i), "r"(v.x), "r"(v.y),
+                       "r"(v.z), "r"(v.w));
+        }
+        __syncwarp();
+      }
+      double accA[NACC], accB[NACC];
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) accA[k] = accB[k] = 0.0;
+      uint64_t hA = 0, hB = 0;
+      double curA = 0.0, curB = 0.0;
+      uint32_t curk = 0;
+      for (int c = 0; c < nchunks; ++c, ring.next()) {
+        const int s = ring.s;
+        dev::mbar_wait(&full[s], ring.ph);
+        if (active) {
+          const uint32_t cb = stage0 + (uint32_t)s * p.stage_bytes;
+          const int nt = min(ch, p.n_trees_pad - c * ch);
+          for (int j = 0; j < nt; j += G) {
+            uint32_t tb[G], aA[G], aB[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) tb[g] = cb + (uint32_t)(j + g) * p.stride;
+            // levels 0-2 shared by the two rows: one broadcast load per level
+            uint32_t r0[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) r0[g] = dev::lds_u32(tb[g] + 4u);
+            bool a0[G], b0[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              a0[g] = left_of(r0[g], codesA);
+              b0[g] = left_of(r0[g], codesB);
+            }
+            uint2 n23[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) n23[g] = dev::lds_v2(tb[g] + 8u);
+            bool a1[G], b1[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              a1[g] = left_of(a0[g] ? n23[g].x : n23[g].y, codesA);
+              b1[g] = left_of(b0[g] ? n23[g].x : n23[g].y, codesB);
+            }
+            uint4 n47[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(n47[g].x), "=r"(n47[g].y), "=r"(n47[g].z), "=r"(n47[g].w)
+                           : "r"(tb[g] + 16u));
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const uint32_t ndA = a0[g] ? (a1[g] ? n47[g].x : n47[g].y) : (a1[g] ? n47[g].z : n47[g].w);
+              const uint32_t ndB = b0[g] ? (b1[g] ? n47[g].x : n47[g].y) : (b1[g] ? n47[g].z : n47[g].w);
+              const bool a2 = left_of(ndA, codesA), b2 = left_of(ndB, codesB);
+              // heap node 8 + 4(!l0) + 2(!l1) + (!l2) at tree + 4 i
+              aA[g] = tb[g] + 32u + (a0[g] ? 0u : 16u) + (a1[g] ? 0u : 8u) + (a2 ? 0u : 4u);
+              aB[g] = tb[g] + 32u + (b0[g] ? 0u : 16u) + (b1[g] ? 0u : 8u) + (b2 ? 0u : 4u);
+            }
+            // levels 3 .. D-1: each row on its own (a' = 2 a - tree + (left ? 0 : 4))
+#pragma unroll
+            for (int l = 3; l < D; ++l) {
+              uint32_t ndA[G], ndB[G];
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                ndA[g] = dev::lds_u32(aA[g]);
+                ndB[g] = dev::lds_u32(aB[g]);
+              }
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                const bool la = left_of(ndA[g], codesA), lb = left_of(ndB[g], codesB);
+                aA[g] = 2u * aA[g] - tb[g] + (la ? 0u : 4u);
+                aB[g] = 2u * aB[g] - tb[g] + (lb ? 0u : 4u);
+              }
+            }
+            double vsA = 0.0, vsB = 0.0;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const uint32_t offA = aA[g] - tb[g], offB = aB[g] - tb[g];
+              if (p.w == 1) {
+                const double vA = (double)dev::lds_f32(tb[g] + offA);
+                const double vB = (double)dev::lds_f32(tb[g] + offB);
+                if (NACC == 1) {
+                  accA[0] += vA;
+                  accB[0] += vB;
+                } else {
+                  vsA += vA;
+                  vsB += vB;
+                }
+              } else {
+                const uint32_t lbA = tb[g] + (4u << D) + 4u * ((offA >> 2) - (1u << D)) * (uint32_t)p.w;
+                const uint32_t lbB = tb[g] + (4u << D) + 4u * ((offB >> 2) - (1u << D)) * (uint32_t)p.w;
+#pragma unroll
+                for (int k = 0; k < NACC; ++k)
+                  if (k < p.K) {
+                    accA[k] += (double)dev::lds_f32(lbA + 4u * k);
+                    accB[k] += (double)dev::lds_f32(lbB + 4u * k);
+                  }
+              }
+            }
+            if (NACC > 1 && p.w == 1) {
+              // class-ordered records (see the one-row path below)
+              const uint32_t k0 = dev::lds_u32(tb[0]) & 0xFFu;
+              if (k0 != curk) {
+#pragma unroll
+                for (int k = 0; k < NACC; ++k)
+                  if (curk == (uint32_t)k) {
+                    accA[k] += curA;
+                    accB[k] += curB;
+                  }
+                curA = curB = 0.0;
+                curk = k0;
+              }
+              curA += vsA;
+              curB += vsB;
+            }
+            if (lm) {
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                const int orig = (int)(dev::lds_u32(tb[g]) >> 8) - 1;
+                if (orig < 0) continue;
+                const size_t lmb = (size_t)(c * ch + j + g) * p.nslots;
+                const int32_t idA = __ldg(p.leafmap + lmb + (((aA[g] - tb[g]) >> 2) - (1u << D)));
+                const int32_t idB = __ldg(p.leafmap + lmb + (((aB[g] - tb[g]) >> 2) - (1u << D)));
+                if (lm == 1) {
+                  if (rowA < p.n) static_cast<int32_t *>(p.out)[rowA * p.n_trees + orig] = idA;
+                  if (rowB < p.n) static_cast<int32_t *>(p.out)[rowB * p.n_trees + orig] = idB;
+                } else {
+                  const uint64_t th = (uint64_t)(uint32_t)(p.tree_begin + orig) << 32;
+                  hA += dev::mix64(th | (uint32_t)idA);
+                  hB += dev::mix64(th | (uint32_t)idB);
+                }
+              }
+            }
+          }
+        }
+        dev::release_stage(&empty[s], lane);
+      }
+      if (NACC > 1 && p.w == 1) {
+#pragma unroll
+        for (int k = 0; k < NACC; ++k)
+          if (curk == (uint32_t)k) {
+            accA[k] += curA;
+            accB[k] += curB;
+          }
+      }
+      if (lm == 2) {
+        if (rowA < p.n) static_cast<uint64_t *>(p.out)[rowA] = hA;
+        if (rowB < p.n) static_cast<uint64_t *>(p.out)[rowB] = hB;
+      } else if (lm == 0) {
+        if (rowA < p.n) dev::write_row<NACC>(p.kind, accA, p.K, p.task, p.post, p.scale, p.base, rowA, p.out);
+        if (rowB < p.n) dev::write_row<NACC>(p.kind, accB, p.K, p.task, p.post, p.scale, p.base, rowB, p.out);
       }
     }
     return;
@@ -299,40 +486,58 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
 
 using PttrFn = void (*)(const PttrParams);
 
-template <int CW, int D, bool LE>
+template <int CW, int D, bool LE, int RPL>
 static PttrFn pttr_pick_nacc(int nacc) {
   switch (nacc) {
-    case 1: return pttr_kernel<D, LE, 1, kTreeGroup, CW>;
-    case 4: return pttr_kernel<D, LE, 4, kTreeGroup, CW>;
-    case 8: return pttr_kernel<D, LE, 8, kTreeGroup, CW>;
-    default: return pttr_kernel<D, LE, 16, kTreeGroup, CW>;
+    case 1: return pttr_kernel<D, LE, 1, kTreeGroup, CW, RPL>;
+    case 4: return pttr_kernel<D, LE, 4, kTreeGroup, CW, RPL>;
+    case 8: return pttr_kernel<D, LE, 8, kTreeGroup, CW, RPL>;
+    default: return pttr_kernel<D, LE, 16, kTreeGroup, CW, RPL>;
   }
 }
 
-template <int CW, int D>
+template <int CW, int D, int RPL>
 static PttrFn pttr_pick_le(bool le, int nacc) {
-  return le ? pttr_pick_nacc<CW, D, true>(nacc) : pttr_pick_nacc<CW, D, false>(nacc);
+  return le ? pttr_pick_nacc<CW, D, true, RPL>(nacc) : pttr_pick_nacc<CW, D, false, RPL>(nacc);
 }
 
 template <int CW>
 static PttrFn pttr_pick(int D, bool le, int nacc) {
   switch (D) {
-    case 0: return pttr_pick_le<CW, 0>(le, nacc);
-    case 1: return pttr_pick_le<CW, 1>(le, nacc);
-    case 2: return pttr_pick_le<CW, 2>(le, nacc);
-    case 3: return pttr_pick_le<CW, 3>(le, nacc);
-    case 4: return pttr_pick_le<CW, 4>(le, nacc);
-    case 5: return pttr_pick_le<CW, 5>(le, nacc);
-    case 6: return pttr_pick_le<CW, 6>(le, nacc);
-    case 7: return pttr_pick_le<CW, 7>(le, nacc);
-    case 8: return pttr_pick_le<CW, 8>(le, nacc);
-    case 9: return pttr_pick_le<CW, 9>(le, nacc);
-    case 10: return pttr_pick_le<CW, 10>(le, nacc);
+    case 0: return pttr_pick_le<CW, 0, 1>(le, nacc);
+    case 1: return pttr_pick_le<CW, 1, 1>(le, nacc);
+    case 2: return pttr_pick_le<CW, 2, 1>(le, nacc);
+    case 3: return pttr_pick_le<CW, 3, 1>(le, nacc);
+    case 4: return pttr_pick_le<CW, 4, 1>(le, nacc);
+    case 5: return pttr_pick_le<CW, 5, 1>(le, nacc);
+    case 6: return pttr_pick_le<CW, 6, 1>(le, nacc);
+    case 7: return pttr_pick_le<CW, 7, 1>(le, nacc);
+    case 8: return pttr_pick_le<CW, 8, 1>(le, nacc);
+    case 9: return pttr_pick_le<CW, 9, 1>(le, nacc);
+    case 10: return pttr_pick_le<CW, 10, 1>(le, nacc);
+    default: return nullptr;
+  }
+}
+
+// two rows per lane (pre-pass codes, D >= 3)
+template <int CW>
+static PttrFn pttr_pick_rpl2(int D, bool le, int nacc) {
+  switch (D) {
+    case 3: return pttr_pick_le<CW, 3, 2>(le, nacc);
+    case 4: return pttr_pick_le<CW, 4, 2>(le, nacc);
+    case 5: return pttr_pick_le<CW, 5, 2>(le, nacc);
+    case 6: return pttr_pick_le<CW, 6, 2>(le, nacc);
+    case 7: return pttr_pick_le<CW, 7, 2>(le, nacc);
+    case 8: return pttr_pick_le<CW, 8, 2>(le, nacc);
+    case 9: return pttr_pick_le<CW, 9, 2>(le, nacc);
+    case 10: return pttr_pick_le<CW, 10, 2>(le, nacc);
     default: return nullptr;
   }
 }
 
 PttrFn pttr_fn32(int D, bool le, int nacc);
 PttrFn pttr_fn16(int D, bool le, int nacc);
+PttrFn pttr_fn32_rpl2(int D, bool le, int nacc);
+PttrFn pttr_fn16_rpl2(int D, bool le, int nacc);
 
 }  // namespace hb

@@ -15,7 +15,7 @@ POST_IDENTITY, POST_SIGMOID, POST_SOFTMAX, POST_ISOLATION = 0, 1, 2, 3
 TASK_REGRESSION, TASK_CLASSIFICATION = 0, 1
 STRATEGY = {"auto": 0, "gemm": 1, "tt": 2, "ptt": 3}
 STRATEGY_NAME = {v: k for k, v in STRATEGY.items()}
-ABI_VERSION = 5
+ABI_VERSION = 6
 KERNEL_NAME = {0: "ptt_kernel", 1: "pttr_kernel", 2: "tt_kernel", 3: "tt_wide_kernel",
                4: "gemm_tc_kernel", 5: "gemm_kernel"}
 OUT = {"predict": 0, "proba": 1, "raw": 2, "margin": 3, "leaf": 4, "leaf_hash": 5, "raw64": 6}
@@ -54,7 +54,7 @@ class _Info(C.Structure):
                 ("code_cell_bits", C.c_int32), ("rank_prepass", C.c_int32),
                 ("tt_sector", C.c_int32), ("tt_chunk_trees", C.c_int32),
                 ("small_batch_max_rows", C.c_int32), ("tt_walks_per_lane", C.c_int32),
-                ("tt_record_bytes", C.c_int64), ("rank_prepass_tma", C.c_int32), ("reserved0", C.c_int32)]
+                ("tt_record_bytes", C.c_int64), ("rank_prepass_tma", C.c_int32), ("rows_per_lane", C.c_int32)]
 
 
 def _load():

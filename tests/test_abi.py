@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     missing = [s for s in declared if s not in exported]
     assert not missing, missing
     assert sorted(hb.exported_symbols) == declared
-    assert hb.lib.hb_abi_version() == 5
+    assert hb.lib.hb_abi_version() == 6
 
 
 def test_sm100a_cubin_embedded():

@@ -1095,6 +1095,8 @@ def test_auto_layout_per_config():
         got = (info["strategy_name"], info["code_cell_bits"], info["rank_prepass"])
         assert got == (strat, cw, pre), (name, got)
         assert info["node_record_bytes"] == 4
+        # two rows per lane for scalar-output models with pre-pass codes (C2, C3)
+        assert info["rows_per_lane"] == (2 if pre and e.n_outputs == 1 else 1), name
         # TMA pre-pass groups where a contiguous X has a 16-B row pitch (C3: F = 28)
         assert info["rank_prepass_tma"] == (1 if pre and e.n_features % 4 == 0 else 0), name
     _, e = synth.make_config("C5")
@@ -1120,3 +1122,31 @@ def test_tt_wide_tree_chunks(chunk, monkeypatch):
         assert m.info["kernel_name"] == "tt_wide_kernel"
         Xd, Xh = X_pair(seed, 1000 + seed, 37, special_q24=SPECIAL_Q24)
         check_all(e, m, Xd, Xh)
+
+
+@pytest.mark.parametrize("cw", ["32", "16"])
+@pytest.mark.parametrize("D", [3, 5, 8])
+@pytest.mark.parametrize("kind", ["binary", "reg", "multiclass", "rf", "k12"])
+def test_pttr_two_rows_per_lane(kind, D, cw, monkeypatch):
+    """Rank-coded PTT with two rows per lane (pttr_kernel<RPL = 2>, pre-pass
+    codes): the top three levels are loaded once for a lane's two rows (root
+    LDS, nodes 2-3 LDS.64, nodes 4-7 LDS.128) and selected per row; every
+    output kind against the oracle, with row counts that end on a half-filled
+    64-row warp tile (row B beyond n) and on a whole one, and the leaf ids
+    equal to the one-row-per-lane kernel's."""
+    monkeypatch.setenv("HB_RANK_PRE", "1")
+    monkeypatch.setenv("HB_PTT_RANK", "1")
+    monkeypatch.setenv("HB_RANK_CW", cw)
+    seed = zlib.crc32(f"rpl2{kind}{D}{cw}".encode()) & 0xFFFF
+    e = _forest(kind, 37, D, 23, seed, FAMILIES[seed % 3], seed % 2)
+    monkeypatch.setenv("HB_PTTR_RPL", "1")
+    m1 = hb.Model(e, strategy="ptt", device=0)
+    assert m1.info["rows_per_lane"] == 1
+    monkeypatch.setenv("HB_PTTR_RPL", "2")
+    m = hb.Model(e, strategy="ptt", device=0)
+    assert m.info["rows_per_lane"] == 2 and m.info["rank_prepass"] == 1 and m.info["code_cell_bits"] == int(cw)
+    rpc = m.info["rows_per_cta"]
+    for n in (2 * 148 * rpc + 32 * 5 + 17, 3 * rpc):
+        Xd, Xh = X_pair(seed + n, n, 23, special_q24=SPECIAL_Q24)
+        check_all(e, m, Xd, Xh)
+        assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), m1.predict_leaf(Xd).cpu().numpy())
