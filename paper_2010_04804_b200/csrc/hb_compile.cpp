@@ -595,10 +595,15 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     // level than 16-bit ones) at no fewer warps, it wins: the scorer then
     // only copies codes and its ring carries trees only (C3: 742.8M vs 704.1M
     // rows/s; C4, whose in-kernel layout needs 16-bit cells: 107.0M vs
-    // 98.9M). With 16-bit pre-pass cells it does not (C4': 404.8M vs 420.8M).
+    // 98.9M). With 16-bit pre-pass cells it did not in round 1 (C4': 404.8M
+    // vs 420.8M); since the window-search pre-pass (round 2) it does when
+    // the walk is long next to the feature count (C4', T*D / n_fc = 74:
+    // 427.9M vs 416.8M rows/s), HB_PRE16_MIN_RATIO (64)
     LaunchCfg pc;
     int pcw = 32;
-    if (pick_cw(true, pc, pcw) && pcw == 32 && pc.nw >= cfg.nw) {
+    const double walk_ratio = (double)Tpad * (double)std::max(D, 1) / std::max(1, A.n_fc);
+    if (pick_cw(true, pc, pcw) && pc.nw >= cfg.nw &&
+        (pcw == 32 || walk_ratio >= (double)env_int2("HB_PRE16_MIN_RATIO", 64))) {
       pre = true;
       cfg = pc;
       cw = pcw;

@@ -1085,10 +1085,10 @@ def test_auto_layout_per_config():
     """AUTO picks, for each BASELINE config, the layout DESIGN.md §4 measured
     fastest: C1 any strategy (small-batch path per call), C2 rank-coded PTT
     with 16-bit cells and the pre-pass, C3 and C4 rank-coded PTT with 32-bit
-    cells and the pre-pass, C4' in-kernel codes with 16-bit cells, C5's 1/8
+    cells and the pre-pass, C4' the pre-pass with 16-bit cells, C5's 1/8
     tree shard TT over BFS records in one launch, all 10k C5 trees TT in
     L2-resident tree chunks (their records exceed L2)."""
-    want = {"C2": ("ptt", 16, 1), "C3": ("ptt", 32, 1), "C4": ("ptt", 32, 1), "C4p": ("ptt", 16, 0)}
+    want = {"C2": ("ptt", 16, 1), "C3": ("ptt", 32, 1), "C4": ("ptt", 32, 1), "C4p": ("ptt", 16, 1)}
     for name, (strat, cw, pre) in want.items():
         _, e = synth.make_config(name)
         info = hb.Model(e, device=0).info
