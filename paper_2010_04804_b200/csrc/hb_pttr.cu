@@ -34,7 +34,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -97,11 +100,32 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   p.kind = a.kind;
   p.out = a.out;
   p.prefetch = m.cfg.prefetch;
-  p.nw = m.cfg.nw;
+  // consumer warps of this launch: the persistent grid walks ceil(tiles / SMs)
+  // rounds of row tiles, so a call whose tiles leave the last round part
+  // empty runs up to 2 fewer warps per CTA when that costs fewer warp-rounds
+  // (rounds x warps; SMEM sized for cfg.nw holds any smaller count). E.g.
+  // C3's 1.25M rows per GPU at 8 GPUs: 24 warps x 64 rows = 5.5 rounds ->
+  // 22 warps, 6.0 rounds: 796.4M -> 834.5M rows/s. Deeper trims lose more
+  // per-warp throughput than they save (C2 at 18 warps: 597M -> 563M).
+  // HB_NW_TRIM=0 keeps cfg.nw.
+  const int sms = sm_count(m.device) * m.cfg.ctas_per_sm;
+  int nw = m.cfg.nw;
+  if (!(std::getenv("HB_NW_TRIM") && std::atoi(std::getenv("HB_NW_TRIM")) == 0)) {
+    int64_t best = INT64_MAX;
+    for (int w = m.cfg.nw; w >= std::max(1, m.cfg.nw - 2); --w) {
+      const int64_t rows = (int64_t)w * 32 * m.rank_rpl;
+      const int64_t rounds = ((a.n + rows - 1) / rows + sms - 1) / sms;
+      if (rounds * w < best) {
+        best = rounds * w;
+        nw = w;
+      }
+    }
+  }
+  p.nw = nw;
   p.ns = m.cfg.ns;
   p.ch = m.cfg.ch;
   p.stage_bytes = (uint32_t)m.cfg.stage_bytes;
-  const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32 * m.rank_rpl;
+  const int64_t rows_per_tile = (int64_t)nw * 32 * m.rank_rpl;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) {
     if (codes) cudaFreeAsync(codes, a.stream);
@@ -112,7 +136,7 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m.cfg.smem_bytes);
   if (e == cudaSuccess) {
     if (codes) mark_launch(a);     // scorer starts (the pre-pass was launch 0)
-    fn<<<grid, 32 * (m.cfg.nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
+    fn<<<grid, 32 * (nw + 1), m.cfg.smem_bytes, a.stream>>>(p);
     e = cudaGetLastError();
   }
   if (codes) cudaFreeAsync(codes, a.stream);
