@@ -67,6 +67,7 @@ struct RankCodeParams {
   uint32_t stage_off;     // staged kernel: SMEM byte offset of the X staging buffers
   int gorder;             // 1 = blockIdx.x is the table group and each CTA owns a contiguous
                           // row range (the groups of the same rows run together); 0 = strided
+  int rw;                 // direct kernel, pair_loads: lanes = (row, word) (rank_code_body_rw)
 };
 
 // Table reads: SMEM-resident groups are plain shared-memory loads (LDS), the
@@ -242,6 +243,72 @@ __device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const ui
   }
 }
 
+// 16-bit cells with every word one aligned float2 of X (pair_loads, C2): lanes
+// = (row, word) instead of lane = row, so a warp's X load reads WQ adjacent
+// words (8 WQ bytes) of 32 / WQ rows — a few sectors per row — instead of
+// one float2 from each of 32 rows (32 sectors per load, the L1 cost that
+// bound the row-per-lane body: 48M sectors + 41M SMEM wavefronts per C2
+// call). WQ = 4 words (8 rows per load) when the group has >= 3 words, else
+// 2 (16 rows). Each lane runs 4 rows x its word's 2 features = 8 searches in
+// lockstep; the window-step count is the warp's maximum.
+template <bool LE, bool SM>
+__device__ __forceinline__ void rank_code_body_rw(const RankCodeParams &p, const uint4 g, const uint8_t *tb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int ROWS = kRcRows;                       // 32-row blocks per warp iteration
+  const int nwg = (int)(g.w - g.z);
+  const int WQ = nwg >= 3 ? 4 : 2;                    // words per load
+  const int RI = 32 / WQ;                             // rows per load
+  const int wo = lane % WQ, ro = lane / WQ;
+  const int64_t nbat = (p.nblocks + ROWS - 1) / ROWS;
+  const int64_t nparts = p.gorder ? gridDim.y : gridDim.x;
+  const int64_t part = p.gorder ? blockIdx.y : blockIdx.x;
+  const int64_t bend = p.gorder ? (part + 1) * nbat / nparts : nbat;
+  const int64_t bstep = p.gorder ? (int64_t)kRcWarps : nparts * kRcWarps;
+  for (int w0 = (int)g.z; w0 < (int)g.w; w0 += WQ) {
+    const int wd = w0 + wo;
+    const bool wok = wd < (int)g.w;
+    const int wc = wok ? wd : w0;                     // clamped: loads stay unconditional
+    uint4 M0[2], M1[2];
+    uint32_t sl = 0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = min(2 * wc + e, p.n_fc - 1);
+      M0[e] = __ldg(p.feat + 2 * c);
+      M1[e] = __ldg(p.feat + 2 * c + 1);
+      sl = max(sl, (wok && 2 * wc + e < p.n_fc) ? M0[e].z : 0u);
+    }
+    const uint32_t smax = __reduce_max_sync(0xFFFFFFFFu, sl);
+    const int mi8[2 * 4] = {0, 0, 0, 0, 1, 1, 1, 1};
+    for (int64_t bt = (p.gorder ? part * nbat / nparts : part * kRcWarps) + warp; bt < bend; bt += bstep) {
+      const int64_t r0 = bt * ROWS * 32;
+      // this lane's rows of the batch: r0 + ro + RI k, k < 4 * 32 / RI, four at a time
+      for (int k0 = 0; k0 < ROWS * 32 / RI; k0 += 4) {
+        float x8[8];
+        int64_t rw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          rw[i] = r0 + ro + (int64_t)RI * (k0 + i);
+          const int64_t rr = rw[i] < p.n ? rw[i] : 0;
+          const float2 v = __ldg(reinterpret_cast<const float2 *>(p.X + rr * p.ldx + 2 * wc));
+          x8[i] = v.x;
+          x8[4 + i] = v.y;
+        }
+        uint32_t code[8];
+        rank_codes_lockstep<LE, SM, 8>(x8, M0, M1, mi8, smax, tb, code);
+        if (wok) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int64_t blk = rw[i] >> 5;
+            if (rw[i] < p.nblocks * 32 && blk < (bt + 1) * ROWS)
+              p.codes[((size_t)blk * p.n_words + wd) * 32 + (rw[i] & 31)] =
+                  code[i] | ((2 * wd + 1 < p.n_fc ? code[4 + i] : 0u) << 16);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <bool LE, int CW, int ROWS>
 __global__ void __launch_bounds__(32 * kRcWarps, ROWS == 4 ? 4 : 3) rank_code_kernel(const RankCodeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -252,9 +319,11 @@ __global__ void __launch_bounds__(32 * kRcWarps, ROWS == 4 ? 4 : 3) rank_code_ke
     uint4 *dst = reinterpret_cast<uint4 *>(smem);
     for (uint32_t i = threadIdx.x; i < g.y / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
-    rank_code_body<LE, CW, true, ROWS>(p, g, smem);
+    if (CW == 16 && ROWS == kRcRows && p.pair_loads && p.rw) rank_code_body_rw<LE, true>(p, g, smem);
+    else rank_code_body<LE, CW, true, ROWS>(p, g, smem);
   } else {
-    rank_code_body<LE, CW, false, ROWS>(p, g, tb);
+    if (CW == 16 && ROWS == kRcRows && p.pair_loads && p.rw) rank_code_body_rw<LE, false>(p, g, tb);
+    else rank_code_body<LE, CW, false, ROWS>(p, g, tb);
   }
 }
 
@@ -803,6 +872,7 @@ hb_status launch_rank_codes(const Model &m, const RunArgs &a, uint32_t *codes, i
   p.codes = codes;
   p.nblocks = nblocks;
   p.smem_cap = (uint32_t)m.rb_smem_cap;
+  p.rw = env_int_rc("HB_RC_RW", 1);
   p.pair_loads = m.rank_cw == 16 && m.rank_nfc == m.n_features && m.n_features % 2 == 0 &&
                  a.ldx % 2 == 0 && (reinterpret_cast<uintptr_t>(a.X) & 7) == 0;
   const size_t tbytes = (m.rb_smem + 15) & ~size_t(15);
