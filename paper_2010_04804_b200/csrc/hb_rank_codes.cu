@@ -248,17 +248,20 @@ __device__ __forceinline__ void rank_code_body(const RankCodeParams &p, const ui
 // words (8 WQ bytes) of 32 / WQ rows — a few sectors per row — instead of
 // one float2 from each of 32 rows (32 sectors per load, the L1 cost that
 // bound the row-per-lane body: 48M sectors + 41M SMEM wavefronts per C2
-// call). WQ = 4 words (8 rows per load) when the group has >= 3 words, else
-// 2 (16 rows). Each lane runs 4 rows x its word's 2 features = 8 searches in
-// lockstep; the window-step count is the warp's maximum.
+// call). WQ = min(words in the group, 4) words of 32 / WQ rows per load (a
+// 3-word group: 10 rows, lanes 30-31 idle). Each lane runs 4 rows x its
+// word's 2 features = 8 searches in lockstep; the window-step count is the
+// warp's maximum.
 template <bool LE, bool SM>
 __device__ __forceinline__ void rank_code_body_rw(const RankCodeParams &p, const uint4 g, const uint8_t *tb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int ROWS = kRcRows;                       // 32-row blocks per warp iteration
   const int nwg = (int)(g.w - g.z);
-  const int WQ = nwg >= 3 ? 4 : 2;                    // words per load
-  const int RI = 32 / WQ;                             // rows per load
+  const int WQ = min(nwg, 4);                         // words per load
+  const int RI = 32 / WQ;                             // rows per load (lanes >= RI WQ idle)
   const int wo = lane % WQ, ro = lane / WQ;
+  const bool lact = lane < RI * WQ;
+  const int nk = (ROWS * 32 + RI - 1) / RI;           // loads per lane and batch
   const int64_t nbat = (p.nblocks + ROWS - 1) / ROWS;
   const int64_t nparts = p.gorder ? gridDim.y : gridDim.x;
   const int64_t part = p.gorder ? blockIdx.y : blockIdx.x;
@@ -282,7 +285,7 @@ __device__ __forceinline__ void rank_code_body_rw(const RankCodeParams &p, const
     for (int64_t bt = (p.gorder ? part * nbat / nparts : part * kRcWarps) + warp; bt < bend; bt += bstep) {
       const int64_t r0 = bt * ROWS * 32;
       // this lane's rows of the batch: r0 + ro + RI k, k < 4 * 32 / RI, four at a time
-      for (int k0 = 0; k0 < ROWS * 32 / RI; k0 += 4) {
+      for (int k0 = 0; k0 < nk; k0 += 4) {
         float x8[8];
         int64_t rw[4];
 #pragma unroll
@@ -295,11 +298,11 @@ __device__ __forceinline__ void rank_code_body_rw(const RankCodeParams &p, const
         }
         uint32_t code[8];
         rank_codes_lockstep<LE, SM, 8>(x8, M0, M1, mi8, smax, tb, code);
-        if (wok) {
+        if (wok && lact) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int64_t blk = rw[i] >> 5;
-            if (rw[i] < p.nblocks * 32 && blk < (bt + 1) * ROWS)
+            if (rw[i] < p.nblocks * 32 && rw[i] < r0 + ROWS * 32)
               p.codes[((size_t)blk * p.n_words + wd) * 32 + (rw[i] & 31)] =
                   code[i] | ((2 * wd + 1 < p.n_fc ? code[4 + i] : 0u) << 16);
           }
