@@ -731,7 +731,11 @@ hb_status compile_ptt_rank(const hb_ensemble *e, int t0, int t1, int D, Model *m
     // single-feature column kernel (hb_rank_codes.cu), one table per CTA;
     // HB_RC_ONE_DENS / HB_RC_ONE_CAP_KB size those tables (measured, §4.6.1)
     const int nwords_colk = cw == 32 ? A.n_fc : (A.n_fc + 1) / 2;
-    const bool colk = nwords_colk <= env_int2("HB_RC_ONEK_MAX_GROUPS", 32);
+    // 16-bit cells whose words are aligned float2 pairs of X (every feature
+    // used, F even) group several words for the direct kernel's (row, word)
+    // lanes instead (C4': 1.164 -> 0.922 ms, 428.3M -> 437.5M rows/s)
+    const bool pairs16 = cw == 16 && A.n_fc == F && F % 2 == 0;
+    const bool colk = !pairs16 && nwords_colk <= env_int2("HB_RC_ONEK_MAX_GROUPS", 32);
     // TMA pre-pass (rank_code_tma_kernel, HB_RC_TMA=0 turns it off): one
     // group per aligned 4-column block of X (fewer when the tables outgrow
     // kRcTmaTableMax), every table SMEM-resident. Only for F % 4 == 0, where
