@@ -285,17 +285,28 @@ __device__ __forceinline__ void rank_code_body_rw(const RankCodeParams &p, const
     for (int64_t bt = (p.gorder ? part * nbat / nparts : part * kRcWarps) + warp; bt < bend; bt += bstep) {
       const int64_t r0 = bt * ROWS * 32;
       // this lane's rows of the batch: r0 + ro + RI k, k < 4 * 32 / RI, four at a time
+      // X of the next four rows is loaded before the current four are
+      // searched (register double buffer: one X latency per batch, not per 4 rows)
+      float2 nx[4];
+      auto load4 = [&](int k0, float2 (&v)[4]) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t r = r0 + ro + (int64_t)RI * (k0 + i);
+          const int64_t rr = r < p.n ? r : 0;
+          v[i] = __ldg(reinterpret_cast<const float2 *>(p.X + rr * p.ldx + 2 * wc));
+        }
+      };
+      load4(0, nx);
       for (int k0 = 0; k0 < nk; k0 += 4) {
         float x8[8];
         int64_t rw[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           rw[i] = r0 + ro + (int64_t)RI * (k0 + i);
-          const int64_t rr = rw[i] < p.n ? rw[i] : 0;
-          const float2 v = __ldg(reinterpret_cast<const float2 *>(p.X + rr * p.ldx + 2 * wc));
-          x8[i] = v.x;
-          x8[4 + i] = v.y;
+          x8[i] = nx[i].x;
+          x8[4 + i] = nx[i].y;
         }
+        if (k0 + 4 < nk) load4(k0 + 4, nx);
         uint32_t code[8];
         rank_codes_lockstep<LE, SM, 8>(x8, M0, M1, mi8, smax, tb, code);
         if (wok && lact) {
