@@ -110,7 +110,10 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   // HB_NW_TRIM=0 keeps cfg.nw.
   const int sms = sm_count(m.device) * m.cfg.ctas_per_sm;
   int nw = m.cfg.nw;
-  if (!(std::getenv("HB_NW_TRIM") && std::atoi(std::getenv("HB_NW_TRIM")) == 0)) {
+  // interleaved warp units (HB_PTTR_INTERLEAVE, default on) spread a partial
+  // last round over every SM, which makes the warp trim below unnecessary
+  p.interleave = !(std::getenv("HB_PTTR_INTERLEAVE") && std::atoi(std::getenv("HB_PTTR_INTERLEAVE")) == 0);
+  if (!p.interleave && !(std::getenv("HB_NW_TRIM") && std::atoi(std::getenv("HB_NW_TRIM")) == 0)) {
     int64_t best = INT64_MAX;
     for (int w = m.cfg.nw; w >= std::max(1, m.cfg.nw - 2); --w) {
       const int64_t rows = (int64_t)w * 32 * m.rank_rpl;
@@ -126,13 +129,19 @@ hb_status launch_ptt_rank(const Model &m, const RunArgs &a) {
   p.ch = m.cfg.ch;
   p.stage_bytes = (uint32_t)m.cfg.stage_bytes;
   const int64_t rows_per_tile = (int64_t)nw * 32 * m.rank_rpl;
-  const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
+  int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) {
     if (codes) cudaFreeAsync(codes, a.stream);
     return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
   }
-  p.ntiles = (int)ntiles;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
+  // interleaved warp units: ntiles becomes the number of rounds every CTA runs
+  if (p.interleave) {
+    const int64_t unit_rows = 32 * (int64_t)m.rank_rpl;
+    const int64_t units = (a.n + unit_rows - 1) / unit_rows;
+    ntiles = (units + (int64_t)grid * nw - 1) / ((int64_t)grid * nw);
+  }
+  p.ntiles = (int)ntiles;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, m.cfg.smem_bytes);
   if (e == cudaSuccess) {
     if (codes) mark_launch(a);     // scorer starts (the pre-pass was launch 0)

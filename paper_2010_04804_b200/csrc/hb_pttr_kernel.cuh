@@ -30,6 +30,8 @@ struct PttrParams {
   uint32_t stage_bytes;
   const uint32_t *codes;  // pre-pass output [row block][n_words][32] (null: codes computed in-kernel)
   int n_words;
+  int interleave;         // 1: warp units interleaved over the grid (ntiles = rounds, every CTA
+                          // runs all of them; the last round's rows spread over every SM)
 };
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
@@ -76,7 +78,16 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
   __syncthreads();
   const int nchunks = (p.n_trees_pad + ch - 1) / ch;
   const int items = p.n_groups + nchunks;          // per tile: feature groups, then tree chunks
-  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  // row tiles of this CTA. Contiguous tiles: tile t = blockIdx.x + k grid,
+  // warp w owns unit t nw + w. Interleaved units (p.interleave): round k,
+  // warp w owns unit (k nw + w) grid + blockIdx.x, so a partial last round
+  // leaves every SM some warps instead of leaving whole SMs idle.
+  const int my_tiles = p.interleave ? p.ntiles
+                                    : (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  auto unit_of = [&](int k) -> int64_t {
+    return p.interleave ? ((int64_t)k * nw + warp) * gridDim.x + blockIdx.x
+                        : ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * nw + warp;
+  };
 
   if (warp == nw) {
     if (lane == 0) {
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
       for (long it = 0; it < total; ++it, r.next(), q = (q + 1 == items) ? 0 : q + 1) {
         const int s = r.s;
         dev::mbar_wait(&empty[s], r.ph ^ 1u);
-        if (q == 0 && p.prefetch) {
+        if (q == 0 && p.prefetch && !p.interleave) {
           // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
           // (of code words, which are contiguous per tile, with the pre-pass)
           const long tile_i = it / items;
@@ -132,10 +143,17 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
       return (nd & 0xFFFFu) >= lds_u16(cbase + (nd >> 16));
     };
     dev::Ring ring(ns);
-    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-      const int64_t wrow0 = (int64_t)tile * (nw * 64) + warp * 64;
+    for (int k = 0; k < my_tiles; ++k) {
+      const int64_t wrow0 = unit_of(k) * 64;
       const int64_t rowA = wrow0 + lane, rowB = rowA + 32;
       const bool active = wrow0 < p.n;
+      if (p.interleave && p.prefetch && lane == 0) {
+        // warm L2 with this warp's next unit of code words
+        const int64_t nb = (p.n + 31) / 32, b1 = (unit_of(k + 1) * 64) >> 5;
+        if (b1 < nb)
+          dev::prefetch_rows_l2(reinterpret_cast<const float *>(p.codes), b1, min((int64_t)2, nb - b1), nb,
+                                (int64_t)p.n_words * 32);
+      }
       __syncwarp();   // previous tile's cell reads done before the fill (WAR)
       if (active) {
         const int nblk = wrow0 + 32 < p.n ? 2 : 1;
@@ -300,10 +318,21 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
   const uint32_t stage0 = dev::smem_u32(stages);
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   dev::Ring ring(ns);
-  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
+  for (int k = 0; k < my_tiles; ++k) {
+    const int64_t wrow0 = unit_of(k) * 32;
     const int64_t row = wrow0 + lane;
     const bool active = wrow0 < p.n;
+    if (p.interleave && p.prefetch && lane == 0) {
+      // warm L2 with this warp's next unit: code words, or its X rows
+      const int64_t r1 = unit_of(k + 1) * 32;
+      if (p.codes) {
+        const int64_t nb = (p.n + 31) / 32;
+        if ((r1 >> 5) < nb)
+          dev::prefetch_rows_l2(reinterpret_cast<const float *>(p.codes), r1 >> 5, 1, nb, (int64_t)p.n_words * 32);
+      } else {
+        dev::prefetch_rows_l2(p.X, r1, 32, p.n, p.ldx);
+      }
+    }
     const float *xr = p.X + (row < p.n ? row : 0) * p.ldx;
     // the tile fills below write other lanes' cells: every lane is done
     // reading the previous tile's (WAR within the warp; racecheck)
