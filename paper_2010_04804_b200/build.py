@@ -32,7 +32,12 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked: the bounds-checked test library libhb_checked.so (-DHB_CHECKED:
+    device-side HB_DCHECK traps), built into its own object directory."""
+    OBJ = globals()["OBJ"] if not checked else os.path.join(PKG, "build_checked")
+    SO = globals()["SO"] if not checked else os.path.join(PKG, "libhb_checked.so")
+    flags = FLAGS + (["-DHB_CHECKED"] if checked else [])
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
@@ -43,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(OBJ, os.path.splitext(os.path.basename(s))[0] + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            jobs.append([NVCC] + ARCH + FLAGS + ["-c", s, "-o", o])
+            jobs.append([NVCC] + ARCH + flags + ["-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,4 +66,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

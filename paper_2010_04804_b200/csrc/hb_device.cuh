@@ -7,6 +7,23 @@
 
 #include "hb.h"
 
+// Device-side bounds checks of the checked build (libhb_checked.so, -DHB_CHECKED;
+// DESIGN.md §7.1): a failed check prints its site and traps, so the launch
+// fails with cudaErrorLaunchFailure. Compiled out of the product library.
+#ifdef HB_CHECKED
+#include <cstdio>
+#define HB_DCHECK(c)                                                                  \
+  do {                                                                                \
+    if (!(c)) {                                                                       \
+      printf("HB_DCHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                      \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define HB_DCHECK(c) ((void)0)
+#endif
+
 namespace hb {
 namespace dev {
 

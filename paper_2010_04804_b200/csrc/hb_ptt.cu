@@ -133,10 +133,16 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
           for (int l = 0; l < D; ++l) {
             uint2 nd[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) nd[g] = dev::lds_v2(a[g]);
+            for (int g = 0; g < G; ++g) {
+              HB_DCHECK(a[g] - tb[g] >= (8u << l) && a[g] - tb[g] < (16u << l));   // heap node of level l
+              nd[g] = dev::lds_v2(a[g]);
+            }
             float x[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) x[g] = dev::lds_f32(xlane + (nd[g].x << 7));
+            for (int g = 0; g < G; ++g) {
+              HB_DCHECK(nd[g].x < (uint32_t)p.F);                                  // column of the X slice
+              x[g] = dev::lds_f32(xlane + (nd[g].x << 7));
+            }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               const float t = __uint_as_float(nd[g].y);

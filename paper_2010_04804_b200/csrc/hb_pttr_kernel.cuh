@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
     // go left <=> k >= c(x) (node and 32-bit cell share the high half; 16-bit
     // cells compare the low half)
     auto left_of = [&](uint32_t nd, uint32_t cbase) -> bool {
+      HB_DCHECK((nd >> 16) < tile_bytes);               // code cell inside this row block's tile
       if (CW == 32) return nd >= dev::lds_u32(cbase + (nd >> 16));
       return (nd & 0xFFFFu) >= lds_u16(cbase + (nd >> 16));
     };
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
       __syncwarp();   // previous tile's cell reads done before the fill (WAR)
       if (active) {
         const int nblk = wrow0 + 32 < p.n ? 2 : 1;
+        HB_DCHECK((wrow0 >> 5) + nblk <= (p.n + 31) / 32);   // pre-pass blocks that exist
         const uint4 *src = reinterpret_cast<const uint4 *>(p.codes + (size_t)(wrow0 >> 5) * p.n_words * 32);
         const uint32_t dst = codesA - 4u * lane;
         for (int i = lane; i < nblk * p.n_words * 8; i += 32) {
@@ -222,6 +224,8 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
               uint32_t ndA[G], ndB[G];
 #pragma unroll
               for (int g = 0; g < G; ++g) {
+                HB_DCHECK(aA[g] - tb[g] >= (4u << l) && aA[g] - tb[g] < (8u << l));   // heap node of level l
+                HB_DCHECK(aB[g] - tb[g] >= (4u << l) && aB[g] - tb[g] < (8u << l));
                 ndA[g] = dev::lds_u32(aA[g]);
                 ndB[g] = dev::lds_u32(aB[g]);
               }
@@ -236,6 +240,7 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               const uint32_t offA = aA[g] - tb[g], offB = aB[g] - tb[g];
+              HB_DCHECK(offA >= (4u << D) && offA < (8u << D) && offB >= (4u << D) && offB < (8u << D));
               if (p.w == 1) {
                 const double vA = (double)dev::lds_f32(tb[g] + offA);
                 const double vB = (double)dev::lds_f32(tb[g] + offB);
@@ -434,8 +439,13 @@ __global__ void __launch_bounds__(32 * 25, 1) pttr_kernel(const PttrParams p) {
           for (int l = 0; l < D; ++l) {
             uint32_t nd[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) nd[g] = dev::lds_u32(a[g]);
+            for (int g = 0; g < G; ++g) {
+              HB_DCHECK(a[g] - tb[g] >= (4u << l) && a[g] - tb[g] < (8u << l));   // heap node of level l
+              nd[g] = dev::lds_u32(a[g]);
+            }
             uint32_t xc[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) HB_DCHECK((nd[g] >> 16) < tile_bytes);   // code cell in the tile
 #pragma unroll
             for (int g = 0; g < G; ++g)
               xc[g] = CW == 32 ? dev::lds_u32(codes + (nd[g] >> 16)) : lds_u16(codes + (nd[g] >> 16));

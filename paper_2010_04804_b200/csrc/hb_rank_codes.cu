@@ -313,6 +313,7 @@ __device__ __forceinline__ void rank_code_body_rw(const RankCodeParams &p, const
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int64_t blk = rw[i] >> 5;
+            HB_DCHECK(wd < p.n_words && 2 * wd < p.n_fc);
             if (rw[i] < p.nblocks * 32 && rw[i] < r0 + ROWS * 32)
               p.codes[((size_t)blk * p.n_words + wd) * 32 + (rw[i] & 31)] =
                   code[i] | ((2 * wd + 1 < p.n_fc ? code[4 + i] : 0u) << 16);

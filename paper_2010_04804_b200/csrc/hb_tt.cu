@@ -209,6 +209,7 @@ template <bool LE>
 __device__ __forceinline__ void wide_step(const uint4 *tr, uint32_t &q, uint32_t &pay, uint32_t &done,
                                           uint32_t xlane) {
   if (done == 0u) {
+    HB_DCHECK(q < __ldg(&tr->x));               // record index inside the tree (header: n_records)
     const uint4 d = __ldg(tr + 1 + q);          // record q follows the 16-B tree header
     const float x = dev::lds_f32(xlane + (d.x & ~3u));
     const float t = __uint_as_float(d.y);

@@ -7,7 +7,9 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_PKG, "libhb.so")
+# HB_LIB: another build of the same library (tests: the bounds-checked
+# libhb_checked.so); never a fallback — a missing library still fails loudly
+lib_path = os.environ.get("HB_LIB") or os.path.join(_PKG, "libhb.so")
 
 CMP_LT, CMP_LE = 0, 1
 AGG_SUM, AGG_MEAN = 0, 1

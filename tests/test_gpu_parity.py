@@ -1150,3 +1150,30 @@ def test_pttr_two_rows_per_lane(kind, D, cw, monkeypatch):
         Xd, Xh = X_pair(seed + n, n, 23, special_q24=SPECIAL_Q24)
         check_all(e, m, Xd, Xh)
         assert np.array_equal(m.predict_leaf(Xd).cpu().numpy(), m1.predict_leaf(Xd).cpu().numpy())
+
+
+def test_checked_build_bounds():
+    """compute-sanitizer is closed on this pool, so every kernel family also
+    runs under the bounds-checked build (libhb_checked.so, -DHB_CHECKED:
+    HB_DCHECK traps on a heap node outside its level, a code cell outside the
+    row block's tile, a pre-pass block or code word that does not exist, a TT
+    record index past its tree, an X-slice column past F): tools/sanitize.py's
+    cases (every strategy, layout and pre-pass kernel, wrapping rings, tree
+    chunks, small batches, two rows per lane, row-word pre-pass), every output
+    kind, in a subprocess that loads the checked library instead of libhb.so."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    so = os.path.join(root, "paper_2010_04804_b200", "libhb_checked.so")
+    if not os.path.exists(so):
+        from paper_2010_04804_b200 import build
+        build.build(checked=True)
+    env = dict(os.environ, HB_LIB=so)
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize.py")], env=env,
+                       capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "library " + so in out, out[:500]
+    assert "HB_DCHECK failed" not in out, out[-4000:]
+    assert out.count("\nok ") + out.startswith("ok ") >= 20, out[-2000:]

@@ -43,6 +43,14 @@ cases = [
                                             post=synth.POST_SOFTMAX, task=synth.TASK_CLASSIFICATION),
      {"HB_TT_WIDE": "1"}, "tt"),
     ("gemm-cuda", synth.gen_forest(40, 5, 12, seed=3), {}, "gemm"),
+    # round 2 paths: direct pre-pass with (row, word) lanes (16-bit pair loads),
+    # two rows per lane in the scorer (pre-pass, K = 1, D >= 3), interleaved units
+    ("ptt-rank-prepass-16-rowword", synth.gen_forest(40, 6, 12, seed=1),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RC_TMA": "0", "HB_RANK_CW": "16", "HB_RC_STAGED": "0"}, "ptt",
+     (3000, 50_000)),
+    ("ptt-rank-rpl2-multiclass", synth.gen_forest(42, 7, 12, seed=8, n_outputs=3, post=synth.POST_SOFTMAX,
+                                                  task=synth.TASK_CLASSIFICATION),
+     {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "32"}, "ptt", (3000, 50_000)),
     # TMA pre-pass (F = 12: three 4-column groups); 250K rows wrap every
     # warp's 3-stage ring several times
     ("ptt-rank-prepass-tma-32", synth.gen_forest(4, 4, 12, seed=7),
@@ -51,6 +59,7 @@ cases = [
      {"HB_PTT_RANK": "1", "HB_RANK_PRE": "1", "HB_RANK_CW": "16", "HB_RC_TMA": "1"}, "ptt", (3000, 250_000)),
 ]
 only = set(sys.argv[1:])   # optional case names; default: every case
+print("library", hb.lib_path, flush=True)
 for name, e, env, strat, *rows in cases:
     if only and name not in only:
         continue
