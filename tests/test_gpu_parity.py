@@ -1177,3 +1177,20 @@ def test_checked_build_bounds():
     assert "library " + so in out, out[:500]
     assert "HB_DCHECK failed" not in out, out[-4000:]
     assert out.count("\nok ") + out.startswith("ok ") >= 20, out[-2000:]
+
+
+def test_randomized_differential_fuzz():
+    """tools/gpu_fuzz.py in the suite (bounded): random ensembles (depth 0-12,
+    regression / binary / per-class / vector-leaf RF, LT / LE, tie-heavy
+    grids) under random forced layouts and row pitches, every output kind
+    against the oracle. Longer runs, on the product and the bounds-checked
+    library, are in profiles/r02_gpu_fuzz_*.txt."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if not k.startswith("HB_")}
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "gpu_fuzz.py"), "40", "2024"], env=env,
+                       capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert "gpu_fuzz:" in r.stdout, r.stdout[-2000:]
