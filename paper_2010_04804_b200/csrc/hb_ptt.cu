@@ -18,6 +18,8 @@
 //    stream simply restarts for every tile.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "hb_device.cuh"
 #include "hb_internal.h"
 
@@ -39,6 +41,7 @@ struct PttParams {
   void *out;
   int nw, ns, ch, ntiles;
   int prefetch;           // L2 prefetch of the next tile's X rows
+  int interleave;         // 1: warp units interleaved over the grid (ntiles = rounds; hb_pttr_kernel.cuh)
 };
 
 template <int D, bool LE, int NACC, int G>
@@ -61,7 +64,14 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
   __syncthreads();
 
   const int nchunks = (p.n_trees_pad + ch - 1) / ch;
-  const int my_tiles = (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  // contiguous CTA tiles, or warp units interleaved over the grid so that a
+  // partial last round leaves every SM some warps (as pttr_kernel)
+  const int my_tiles = p.interleave ? p.ntiles
+                                    : (p.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  auto unit_of = [&](int k) -> int64_t {
+    return p.interleave ? ((int64_t)k * nw + warp) * gridDim.x + blockIdx.x
+                        : ((int64_t)blockIdx.x + (int64_t)k * gridDim.x) * nw + warp;
+  };
 
   if (warp == nw) {
     // ---------------- producer warp: stream tree chunks through the ring
@@ -72,7 +82,7 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
       for (long it = 0; it < total; ++it, r.next(), c = (c + 1 == nchunks) ? 0 : c + 1) {
         const int s = r.s;
         dev::mbar_wait(&empty[s], r.ph ^ 1u);
-        if (c == 0 && p.prefetch) {
+        if (c == 0 && p.prefetch && !p.interleave) {
           // first item of a tile: warm L2 with this CTA's NEXT tile of X rows
           const long tile_i = it / nchunks;
           const int64_t next = (int64_t)(blockIdx.x + (tile_i + 1) * gridDim.x) * (nw * 32);
@@ -96,8 +106,10 @@ __global__ void __launch_bounds__(32 * 25, 1) ptt_kernel(const PttParams p) {
   const uint32_t leaf_off = 4u << D;                      // leaf(i) at tree + leaf_off + 4 i ... (w = 1)
   const int lm = p.kind == HB_OUT_LEAF ? 1 : (p.kind == HB_OUT_LEAF_HASH ? 2 : 0);
   dev::Ring ring(ns);
-  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-    const int64_t wrow0 = (int64_t)tile * (nw * 32) + warp * 32;
+  for (int k = 0; k < my_tiles; ++k) {
+    const int64_t wrow0 = unit_of(k) * 32;
+    if (p.interleave && p.prefetch && lane == 0)   // warm L2 with this warp's next rows
+      dev::prefetch_rows_l2(p.X, unit_of(k + 1) * 32, 32, p.n, p.ldx);
     const int64_t row = wrow0 + lane;
     const bool active = wrow0 < p.n;        // whole warp beyond n: only keep the ring in step
     if (active) {
@@ -286,8 +298,14 @@ hb_status launch_ptt(const Model &m, const RunArgs &a) {
   const int64_t rows_per_tile = (int64_t)m.cfg.nw * 32;
   const int64_t ntiles = (a.n + rows_per_tile - 1) / rows_per_tile;
   if (ntiles > INT32_MAX) return fail(HB_E_UNSUPPORTED, "too many rows for one launch");
-  p.ntiles = (int)ntiles;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count(m.device) * m.cfg.ctas_per_sm);
+  p.interleave = !(std::getenv("HB_PTTR_INTERLEAVE") && std::atoi(std::getenv("HB_PTTR_INTERLEAVE")) == 0);
+  if (p.interleave) {
+    const int64_t units = (a.n + 31) / 32;
+    p.ntiles = (int)((units + (int64_t)grid * m.cfg.nw - 1) / ((int64_t)grid * m.cfg.nw));
+  } else {
+    p.ntiles = (int)ntiles;
+  }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        m.cfg.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(ptt)");
