@@ -2,6 +2,7 @@
 // (Sec. 5.1), layout compilation for the three strategies
 // (Tables 3/5/6) and the scoring entry points.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -869,9 +870,27 @@ static hb_status run(const Model &m, const RunArgs &a) {
   return fail(HB_E_INVALID, "corrupt model");
 }
 
+// NVTX ranges around compile / predict (SURVEY §5 tracing): header-only
+// nvtx3, a no-op unless a profiler (ncu, nsys) injects its collector
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+const char *kind_range(int kind) {
+  // indexed by hb_output (PREDICT, PROBA, RAW, MARGIN, LEAF, LEAF_HASH, RAW64)
+  static const char *names[] = {"hb_predict", "hb_predict_proba", "hb_predict_raw", "hb_predict_margin",
+                                "hb_predict_leaf", "hb_predict_leaf_hash", "hb_predict_raw64"};
+  return kind >= 0 && kind < (int)(sizeof(names) / sizeof(names[0])) ? names[kind] : "hb_predict";
+}
+}  // namespace
+
 static hb_status predict_impl(const hb_model *hm, const float *X, int64_t n, int64_t ldx, int kind,
                               void *out, void *stream, bool check_ptrs, void **events = nullptr,
                               int nev = 0, int32_t *n_launches = nullptr) {
+  NvtxRange range(kind_range(kind));
   if (n_launches) *n_launches = 0;
   if (!hm) return fail(HB_E_INVALID, "model is NULL");
   const Model &m = *M(hm);
@@ -931,6 +950,7 @@ static HostStage &host_stage(int device) {
 
 static hb_status host_impl(const hb_model *hm, const float *Xh, int64_t n, int64_t ldx, int kind,
                            void *outh) {
+  NvtxRange range("hb_predict_host");
   if (!hm) return fail(HB_E_INVALID, "model is NULL");
   const Model &m = *M(hm);
   hb_status st = check_kind(m, kind);
@@ -994,12 +1014,14 @@ extern "C" {
 hb_status hb_validate(const hb_ensemble *e) { return validate_impl(e, nullptr); }
 
 hb_status hb_compile(const hb_ensemble *e, int32_t strategy, int32_t device, hb_model **out) {
+  NvtxRange range("hb_compile");
   if (!e) return fail(HB_E_INVALID, "ensemble is NULL");
   return compile_impl(e, 0, e->n_trees, strategy, device, reinterpret_cast<Model **>(out));
 }
 
 hb_status hb_compile_range(const hb_ensemble *e, int32_t tree_begin, int32_t tree_end,
                            int32_t strategy, int32_t device, hb_model **out) {
+  NvtxRange range("hb_compile_range");
   return compile_impl(e, tree_begin, tree_end, strategy, device, reinterpret_cast<Model **>(out));
 }
 
