@@ -635,6 +635,14 @@ def run_ours(args):
                     output=kind, rows_per_gpu=n, trees_per_gpu=t1 - t0,
                     timing=("CUDA graph of %d calls per timed step, value per call" % calls)
                     if calls > 1 else "one call per timed step")
+        # seeds of the synthetic inputs, the compiled layout and its device memory
+        # (SURVEY §5 metrics: seeds, peak memory)
+        cfgd["seeds"] = {"x": cfg.seed_x, "trees": cfg.seed_t}
+        cfgd["layout"] = {k: info.get(k) for k in ("kernel_name", "node_record_bytes", "code_cell_bits",
+                                                   "rank_prepass", "rank_prepass_tma", "rows_per_lane",
+                                                   "rows_per_cta", "tt_chunk_trees", "small_batch_max_rows")}
+        cfgd["model_device_bytes"] = info.get("device_bytes")
+        cfgd["torch_peak_bytes"] = int(torch.cuda.max_memory_allocated(local))   # X, outputs (torch allocator)
         if mode == "trees" and args.emulate_gpus and world == 1:
             cfgd["emulated_shard_of"] = args.emulate_gpus
             cfgd["trees_scored"] = t1 - t0
